@@ -1,0 +1,197 @@
+/*
+ * sfcnl_cu.h — C-ABI of the B200-native (sm_100a) compressed clustered neighbor
+ * list: SFC keygen + sort + permute, cornerstone-style octree, cluster geometry,
+ * warp-cooperative traversal + interaction masks, nibble-codec encode, and the
+ * in-kernel-decoding neighborhood pass.
+ *
+ * This is the drop-in boundary for the reference's build-and-query path
+ * (reference = /root/reference/proj, C++20, CPU only). Each entry point names the
+ * reference interface it replaces. Plain pointers and sizes only; no exceptions
+ * and no C++ types cross it. The C++ drop-in (include/sfcnl/*.hpp, the
+ * reference's public API re-implemented over this ABI) maps the status codes
+ * back to the reference exception types:
+ *
+ *   SFCNL_OK 0, SFCNL_INPUT_ERROR 1 -> sfcnl::InputError (core.hpp:18),
+ *   SFCNL_BUILD_ERROR 2 -> sfcnl::BuildError (core.hpp:23),
+ *   SFCNL_DECODE_ERROR 3 -> sfcnl::DecodeError{byte_offset} (core.hpp:28),
+ *   SFCNL_CUDA_ERROR 4 -> std::runtime_error.
+ *
+ * Memory model: a context owns one CUDA stream on one device and the device
+ * copies of everything it computes. "set_*" calls copy host arrays in,
+ * "get_*" calls copy results out; every call is synchronous at return unless
+ * its comment says otherwise. All host pointers may be pageable or pinned.
+ */
+#ifndef SFCNL_CU_H
+#define SFCNL_CU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFCNL_OK 0
+#define SFCNL_INPUT_ERROR 1
+#define SFCNL_BUILD_ERROR 2
+#define SFCNL_DECODE_ERROR 3
+#define SFCNL_CUDA_ERROR 4
+
+typedef struct sfcnl_cu_ctx sfcnl_cu_ctx;
+
+/* SimulationBox (core.hpp:50-74). */
+typedef struct {
+    double lo[3];
+    double hi[3];
+    int32_t periodic[3];
+} sfcnl_box;
+
+/* OctreeNode (octree.hpp:11-21), identical 32-byte layout. */
+typedef struct {
+    uint64_t key_first;
+    uint64_t key_last;
+    uint32_t particle_begin;
+    uint32_t particle_end;
+    int32_t first_child;
+    uint8_t depth;
+    uint8_t pad_[3];
+} sfcnl_node;
+
+/* BuildParams + ClusterParams (neighbor_store.hpp:18-29, cluster.hpp:12-29).
+ * mode: 0 gather, 1 symmetric. sc_size is fixed at 64 (cluster.hpp:9). */
+typedef struct {
+    uint32_t ci;
+    uint32_t cj;
+    int32_t w;
+    int32_t mode;
+    int32_t compress;
+    double build_radius_scale;
+} sfcnl_build_params;
+
+/* Built-in pair kernels (builtin_kernels.hpp:24-95). */
+#define SFCNL_KERNEL_COUNT 0      /* CountKernel: 1 output "count"            */
+#define SFCNL_KERNEL_DENSITY 1    /* SphDensityKernel: 1 output "rho", in "m" */
+#define SFCNL_KERNEL_LJ 2         /* LjKernel<Real,false>: fx, fy, fz, energy */
+#define SFCNL_KERNEL_LJ_COULOMB 3 /* LjKernel<Real,true>: + Coulomb on "q"    */
+
+/* precision: 0 = fp64, bitwise equal to reduce<double> (reference summation
+ *                 order, no FMA);
+ *            1 = mixed (fp32 pair math on SC-relative coordinates, exact fp64
+ *                 cutoff decisions via a guard band, fp64 lane combine);
+ *                 neighbor_count exact, values within 1e-5 of reduce<double>. */
+typedef struct {
+    int32_t kernel;
+    int32_t precision;
+    double query_scale;
+    double epsilon;
+    double sigma;
+    double coulomb_k;
+} sfcnl_pass_params;
+
+/* ---- context ------------------------------------------------------------ */
+int sfcnl_cu_ctx_create(int device, sfcnl_cu_ctx** out);
+void sfcnl_cu_ctx_destroy(sfcnl_cu_ctx* ctx);
+/* Message of the last failed call on this context (or of a failed create when
+ * ctx == NULL); *byte_offset receives DecodeError::byte_offset. */
+const char* sfcnl_cu_last_error(sfcnl_cu_ctx* ctx, uint64_t* byte_offset);
+/* cudaStream_t of the context (for event timing by the caller). */
+void* sfcnl_cu_stream(sfcnl_cu_ctx* ctx);
+int sfcnl_cu_synchronize(sfcnl_cu_ctx* ctx);
+/* Number of kernels this context has launched so far. */
+uint64_t sfcnl_cu_launch_count(sfcnl_cu_ctx* ctx);
+/* Per-stage device times (ms) of the most recent calls, in the order
+ * keygen, sort, permute, octree, node_geometry, cluster_geometry, build, encode,
+ * pass; returns the number written (<= cap). Enabled by sfcnl_cu_set_timing. */
+int sfcnl_cu_set_timing(sfcnl_cu_ctx* ctx, int enabled);
+int sfcnl_cu_stage_times(sfcnl_cu_ctx* ctx, double* ms, int cap);
+
+/* ---- particles ------------------------------------------------------------
+ * ParticleSet (core.hpp:168-198) in original (unsorted) order. Fields are named
+ * payload arrays ("m", "q", ...). Replaces nothing by itself: it is the upload
+ * half of every reference call that takes `const ParticleSet&`. */
+int sfcnl_cu_set_particles(sfcnl_cu_ctx* ctx, uint64_t n, const double* x, const double* y,
+                           const double* z, const double* h, const sfcnl_box* box);
+int sfcnl_cu_set_field(sfcnl_cu_ctx* ctx, const char* name, const double* values);
+/* Same, for a set that is ALREADY in SFC order (the `sorted` argument of
+ * build_neighbor_store / reduce): marks it as the sorted slot directly. */
+int sfcnl_cu_set_sorted_particles(sfcnl_cu_ctx* ctx, uint64_t n, const double* x,
+                                  const double* y, const double* z, const double* h,
+                                  const sfcnl_box* box);
+int sfcnl_cu_set_sorted_field(sfcnl_cu_ctx* ctx, const char* name, const double* values);
+
+/* ---- (1) SFC keys + stable radix sort ---------------------------------------
+ * Replaces sort_by_sfc (hilbert.hpp:126, hilbert.cpp:8-26): keys = sfc_key of every
+ * particle (hilbert.hpp:110-113), perm = stable ascending order. Results stay on
+ * the device; sfcnl_cu_get_order downloads them. */
+int sfcnl_cu_sort_by_sfc(sfcnl_cu_ctx* ctx, int bits);
+int sfcnl_cu_get_order(sfcnl_cu_ctx* ctx, uint64_t* keys, uint32_t* perm);
+/* Upload an SfcOrder computed elsewhere (keys ascending, perm a permutation). */
+int sfcnl_cu_set_order(sfcnl_cu_ctx* ctx, uint64_t n, const uint64_t* keys, const uint32_t* perm,
+                       int bits);
+
+/* Replaces apply_sfc_order (hilbert.hpp:129, hilbert.cpp:28-44): gathers x,y,z,h
+ * and every field into the sorted slot. */
+int sfcnl_cu_apply_order(sfcnl_cu_ctx* ctx);
+/* Download one sorted array: "x","y","z","h" or a field name. */
+int sfcnl_cu_get_sorted(sfcnl_cu_ctx* ctx, const char* name, double* out);
+
+/* ---- (3) octree --------------------------------------------------------------
+ * Replaces build_octree (octree.hpp:51, octree.cpp:43-59) on the current keys:
+ * same node set and the same node numbering (parent before children, children
+ * contiguous, DFS allocation order). */
+int sfcnl_cu_build_octree(sfcnl_cu_ctx* ctx, uint32_t bucket_size, uint64_t* num_nodes);
+int sfcnl_cu_get_octree(sfcnl_cu_ctx* ctx, sfcnl_node* nodes);
+/* Upload a caller-provided Octree (e.g. the `tree` argument of build_neighbor_store). */
+int sfcnl_cu_set_octree(sfcnl_cu_ctx* ctx, uint64_t num_nodes, const sfcnl_node* nodes, int bits,
+                        uint64_t n);
+/* Replaces compute_node_aabbs + compute_node_max_radius (octree.hpp:57-60,
+ * octree.cpp:68-96) on the sorted slot. lo/hi: 3 doubles per node; radius: 1. */
+int sfcnl_cu_node_geometry(sfcnl_cu_ctx* ctx, double* lo, double* hi, double* radius);
+
+/* ---- (2)(3)(4) list build ----------------------------------------------------
+ * Replaces build_neighbor_store (neighbor_build.hpp:18-19, neighbor_build.cpp:74-184)
+ * on the sorted slot and the current octree: cluster geometry, traversal, masks,
+ * nibble-codec encode (nibble_codec.cpp:117-134). Output is byte-identical to the
+ * reference NeighborStore (counts, offsets, blob). */
+int sfcnl_cu_build_store(sfcnl_cu_ctx* ctx, const sfcnl_build_params* params,
+                         uint64_t* num_superclusters, uint64_t* blob_bytes);
+int sfcnl_cu_get_store(sfcnl_cu_ctx* ctx, uint32_t* counts, uint64_t* offsets, uint8_t* blob);
+/* Upload a NeighborStore (neighbor_store.hpp:44-59) for a later reduce. */
+int sfcnl_cu_set_store(sfcnl_cu_ctx* ctx, const sfcnl_build_params* params, uint64_t n,
+                       uint64_t num_superclusters, const uint32_t* counts,
+                       const uint64_t* offsets, const uint8_t* blob, uint64_t blob_bytes);
+
+/* ---- (5) neighborhood pass ---------------------------------------------------
+ * Replaces reduce<Real,K> (reduce.hpp:38-231) for the built-in kernels, gather
+ * and symmetric stores, on the sorted slot and the current store. outs: 1 or 4
+ * host arrays of n doubles (NULL = keep on device); count: n uint32 (nullable). */
+int sfcnl_cu_reduce(sfcnl_cu_ctx* ctx, const sfcnl_pass_params* params, double* const* outs,
+                    uint32_t* neighbor_count);
+
+/* ---- host-side codec (no device work) ----------------------------------------
+ * codec::encode / codec::decode_into (nibble_codec.hpp:54-60), used by the C++
+ * drop-in and by the parity tests. encode: *len receives the byte length; bytes
+ * are written only when *len <= cap. */
+int sfcnl_codec_encode(const uint32_t* indices, uint64_t count, int w, uint8_t* out,
+                       uint64_t cap, uint64_t* len);
+int sfcnl_codec_decode_into(const uint8_t* data, uint64_t size, uint32_t count, int w,
+                            uint32_t* out, uint64_t* consumed);
+/* hilbert_encode / hilbert_decode (hilbert.hpp:66-90), host-side. */
+int sfcnl_hilbert_encode(uint32_t ix, uint32_t iy, uint32_t iz, int bits, uint64_t* key);
+int sfcnl_hilbert_decode(uint64_t key, int bits, uint32_t* xyz);
+const char* sfcnl_last_host_error(uint64_t* byte_offset);
+
+/* ---- fixtures ---------------------------------------------------------------
+ * make_uniform / make_evrard (generators.hpp:34-35): host generators, seeded,
+ * byte-identical to the reference's. box6 = lo[3], hi[3]. */
+int sfcnl_make_uniform(uint64_t n, double density, double target, const int32_t* periodic,
+                       double h_jitter, uint64_t seed, double* x, double* y, double* z,
+                       double* h, double* m, double* q, double* box6);
+int sfcnl_make_evrard(uint64_t n, double target, int32_t constant_h, const int32_t* periodic,
+                      uint64_t seed, double* x, double* y, double* z, double* h, double* m,
+                      double* q, double* box6);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFCNL_CU_H */

@@ -1,0 +1,144 @@
+"""ctypes binding of the C-ABI in ``include/sfcnl_cu.h`` (``libsfcnl_b200.so``).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_2602_19873_b200``). There is no fallback: if the library is
+missing, importing the GPU API raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsfcnl_b200.so")
+
+# status codes (sfcnl_cu.h)
+OK, INPUT_ERROR, BUILD_ERROR, DECODE_ERROR, CUDA_ERROR = 0, 1, 2, 3, 4
+
+
+class InputError(ValueError):
+    """sfcnl::InputError (core.hpp:18)."""
+
+
+class BuildError(RuntimeError):
+    """sfcnl::BuildError (core.hpp:23)."""
+
+
+class DecodeError(RuntimeError):
+    """sfcnl::DecodeError (core.hpp:28); carries ``byte_offset``."""
+
+    def __init__(self, msg, byte_offset=0):
+        super().__init__(msg)
+        self.byte_offset = byte_offset
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def raise_for(code: int, msg: str, offset: int = 0):
+    if code == OK:
+        return
+    if code == INPUT_ERROR:
+        raise InputError(msg)
+    if code == BUILD_ERROR:
+        raise BuildError(msg)
+    if code == DECODE_ERROR:
+        raise DecodeError(msg, offset)
+    raise CudaError(msg)
+
+
+class Box(C.Structure):
+    _fields_ = [("lo", C.c_double * 3), ("hi", C.c_double * 3), ("periodic", C.c_int32 * 3)]
+
+
+class Node(C.Structure):
+    _fields_ = [("key_first", C.c_uint64), ("key_last", C.c_uint64), ("particle_begin", C.c_uint32),
+                ("particle_end", C.c_uint32), ("first_child", C.c_int32), ("depth", C.c_uint8),
+                ("pad_", C.c_uint8 * 3)]
+
+
+class BuildParamsC(C.Structure):
+    _fields_ = [("ci", C.c_uint32), ("cj", C.c_uint32), ("w", C.c_int32), ("mode", C.c_int32),
+                ("compress", C.c_int32), ("build_radius_scale", C.c_double)]
+
+
+class PassParamsC(C.Structure):
+    _fields_ = [("kernel", C.c_int32), ("precision", C.c_int32), ("query_scale", C.c_double),
+                ("epsilon", C.c_double), ("sigma", C.c_double), ("coulomb_k", C.c_double)]
+
+
+# every symbol the header declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "sfcnl_cu_ctx_create", "sfcnl_cu_ctx_destroy", "sfcnl_cu_last_error", "sfcnl_cu_stream",
+    "sfcnl_cu_synchronize", "sfcnl_cu_launch_count", "sfcnl_cu_set_timing", "sfcnl_cu_stage_times",
+    "sfcnl_cu_set_particles", "sfcnl_cu_set_field", "sfcnl_cu_set_sorted_particles",
+    "sfcnl_cu_set_sorted_field", "sfcnl_cu_sort_by_sfc", "sfcnl_cu_get_order", "sfcnl_cu_set_order",
+    "sfcnl_cu_apply_order", "sfcnl_cu_get_sorted", "sfcnl_cu_build_octree", "sfcnl_cu_get_octree",
+    "sfcnl_cu_set_octree", "sfcnl_cu_node_geometry", "sfcnl_cu_build_store", "sfcnl_cu_get_store",
+    "sfcnl_cu_set_store", "sfcnl_cu_reduce", "sfcnl_codec_encode", "sfcnl_codec_decode_into",
+    "sfcnl_hilbert_encode", "sfcnl_hilbert_decode", "sfcnl_last_host_error", "sfcnl_make_uniform",
+    "sfcnl_make_evrard",
+]
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run __graft_entry__.build() or make -C paper_2602_19873_b200")
+    L = C.CDLL(LIB_PATH)
+    P = C.c_void_p
+    pd = C.POINTER(C.c_double)
+    u64, u32, i32 = C.c_uint64, C.c_uint32, C.c_int32
+    sig = {
+        "sfcnl_cu_ctx_create": (C.c_int, [C.c_int, C.POINTER(P)]),
+        "sfcnl_cu_ctx_destroy": (None, [P]),
+        "sfcnl_cu_last_error": (C.c_char_p, [P, C.POINTER(u64)]),
+        "sfcnl_cu_stream": (P, [P]),
+        "sfcnl_cu_synchronize": (C.c_int, [P]),
+        "sfcnl_cu_launch_count": (u64, [P]),
+        "sfcnl_cu_set_timing": (C.c_int, [P, C.c_int]),
+        "sfcnl_cu_stage_times": (C.c_int, [P, pd, C.c_int]),
+        "sfcnl_cu_set_particles": (C.c_int, [P, u64, P, P, P, P, C.POINTER(Box)]),
+        "sfcnl_cu_set_field": (C.c_int, [P, C.c_char_p, P]),
+        "sfcnl_cu_set_sorted_particles": (C.c_int, [P, u64, P, P, P, P, C.POINTER(Box)]),
+        "sfcnl_cu_set_sorted_field": (C.c_int, [P, C.c_char_p, P]),
+        "sfcnl_cu_sort_by_sfc": (C.c_int, [P, C.c_int]),
+        "sfcnl_cu_get_order": (C.c_int, [P, P, P]),
+        "sfcnl_cu_set_order": (C.c_int, [P, u64, P, P, C.c_int]),
+        "sfcnl_cu_apply_order": (C.c_int, [P]),
+        "sfcnl_cu_get_sorted": (C.c_int, [P, C.c_char_p, P]),
+        "sfcnl_cu_build_octree": (C.c_int, [P, u32, C.POINTER(u64)]),
+        "sfcnl_cu_get_octree": (C.c_int, [P, P]),
+        "sfcnl_cu_set_octree": (C.c_int, [P, u64, P, C.c_int, u64]),
+        "sfcnl_cu_node_geometry": (C.c_int, [P, P, P, P]),
+        "sfcnl_cu_build_store": (C.c_int, [P, C.POINTER(BuildParamsC), C.POINTER(u64), C.POINTER(u64)]),
+        "sfcnl_cu_get_store": (C.c_int, [P, P, P, P]),
+        "sfcnl_cu_set_store": (C.c_int, [P, C.POINTER(BuildParamsC), u64, u64, P, P, P, u64]),
+        "sfcnl_cu_reduce": (C.c_int, [P, C.POINTER(PassParamsC), C.POINTER(P), P]),
+        "sfcnl_codec_encode": (C.c_int, [P, u64, C.c_int, P, u64, C.POINTER(u64)]),
+        "sfcnl_codec_decode_into": (C.c_int, [P, u64, u32, C.c_int, P, C.POINTER(u64)]),
+        "sfcnl_hilbert_encode": (C.c_int, [u32, u32, u32, C.c_int, C.POINTER(u64)]),
+        "sfcnl_hilbert_decode": (C.c_int, [u64, C.c_int, C.POINTER(u32)]),
+        "sfcnl_last_host_error": (C.c_char_p, [C.POINTER(u64)]),
+        "sfcnl_make_uniform": (C.c_int, [u64, C.c_double, C.c_double, C.POINTER(i32), C.c_double, u64,
+                                         P, P, P, P, P, P, P]),
+        "sfcnl_make_evrard": (C.c_int, [u64, C.c_double, i32, C.POINTER(i32), u64, P, P, P, P, P, P, P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def host_check(rc):
+    if rc:
+        off = C.c_uint64(0)
+        msg = lib().sfcnl_last_host_error(C.byref(off)).decode()
+        raise_for(rc, msg, off.value)

@@ -1,0 +1,590 @@
+// (2)(3)(4) Neighbor-list build: per-super-cluster traversal, interaction masks
+// and nibble-codec encode, then a size scan and a compaction into the final blob.
+//
+// Replaces build_neighbor_store (neighbor_build.cpp:74-184) including
+// collect_candidates (:43-65), the mask loop (:128-161) and the serial
+// serialization + codec::encode (:164-182, nibble_codec.cpp:117-134).
+//
+// One CTA (128 threads) per super-cluster (SC, 64 particles):
+//  * traversal: level-synchronous BFS over the octree with an ORDERED frontier in
+//    shared memory (stable block-scan compaction keeps key order; accepted leaves
+//    ride along tagged). A node is accepted iff non-empty and
+//    aabb_dist_sq(sc_aabb, node_aabb) <= r^2 (bit-exact fp64, common.cuh). Because
+//    node boxes nest and aabb_dist_sq is monotone under containment, BFS accepts
+//    exactly the leaves the reference's DFS accepts, in the same key order.
+//  * candidates: union of the accepted leaves' j-cluster ranges, deduplicated
+//    against the previous leaf exactly like `out.back() != j` (:57-58).
+//  * masks: one thread per candidate j-cluster runs the reference loop for its 8
+//    i-clusters: half-list rule (symmetric), AABB prefilter, exact pair test with
+//    early exit -- all predicates in round-to-nearest fp64.
+//  * encode: entries with mask != 0 are compacted in order; masks are written
+//    little-endian, the index list is delta/nibble encoded one 32/64-wide block at
+//    a time by warp 0 (ballot for the block mask, warp scans for nibble offsets,
+//    smem atomicOr to pack nibbles low-first).
+//  * the SC's bytes go to a bump-allocated scratch area; a u32->u64 scan of the
+//    per-SC sizes gives NeighborStore::offsets and a warp-per-SC copy builds the blob.
+// SCs whose frontier/candidates/bytes exceed the shared-memory capacities are
+// re-run by the same code with global-memory workspaces (fallback launch).
+#include <algorithm>
+#include <vector>
+
+#include "ctx.hpp"
+#include "scan.hpp"
+
+namespace sfcnl_cu {
+namespace {
+
+constexpr int kBuildThreads = 128;
+constexpr uint32_t kTag = 0x80000000u;
+constexpr uint32_t kFCap = 1024, kCCap = 1024, kECap = 8192;
+
+struct BuildArgs {
+    uint64_t n;
+    Box box;
+    double scale;
+    uint32_t ci, cj, icl_per_sc, mask_bytes;
+    int w, compress, symmetric;
+    uint64_t num_icl;
+    const double* x;
+    const double* y;
+    const double* z;
+    const double* h;
+    const Node* nodes;
+    const Geo* ngeo;
+    const Geo* igeo;
+    const Geo* jgeo;
+    uint32_t* counts;
+    uint32_t* sizes;
+    uint64_t* soff;
+    uint8_t* scratch;
+    unsigned long long* ctl;  // [0] scratch top, [1] overflow count, [2] scratch overflow flag
+    uint64_t scratch_cap;
+    uint32_t* overflow_list;
+    DevError* err;
+};
+
+struct Workspace {
+    uint32_t* fa;
+    uint32_t* fb;
+    uint32_t* cand;
+    unsigned long long* cmask;
+    uint8_t* ebuf;
+    uint32_t fcap, ccap, ecap;
+};
+
+__device__ __forceinline__ int nibble_count(uint64_t v) { return (64 - __clzll(v) + 3) / 4; }
+
+// Returns false on capacity overflow (caller re-runs the SC in global-memory mode).
+__device__ bool build_sc(const BuildArgs& A, const Workspace& W, uint64_t sc) {
+    __shared__ Geo s_igeo[64];
+    __shared__ double s_x[64], s_y[64], s_z[64], s_h[64];
+    __shared__ Geo s_sc;
+    __shared__ double s_r2;
+    __shared__ uint32_t scratch[33];
+    __shared__ int s_flag, s_over;
+    __shared__ uint32_t s_n[2];
+    const unsigned tid = threadIdx.x;
+    const uint64_t n = A.n;
+    const uint64_t icl_base = sc * A.icl_per_sc;
+    const uint64_t icl_end = tmin<uint64_t>(icl_base + A.icl_per_sc, A.num_icl);
+    const uint32_t nicl = uint32_t(icl_end - icl_base);
+    const uint64_t p0 = sc * kSC;
+    const uint32_t np = uint32_t(tmin<uint64_t>(p0 + kSC, n) - p0);
+    for (uint32_t b = tid; b < nicl; b += blockDim.x) s_igeo[b] = A.igeo[icl_base + b];
+    for (uint32_t k = tid; k < np; k += blockDim.x) {
+        s_x[k] = A.x[p0 + k], s_y[k] = A.y[p0 + k], s_z[k] = A.z[p0 + k], s_h[k] = A.h[p0 + k];
+    }
+    if (tid == 0) s_over = 0;
+    __syncthreads();
+    if (tid == 0) {
+        Geo g;
+        geo_init(g);
+        for (uint32_t b = 0; b < nicl; ++b) {
+            geo_extend(g, s_igeo[b]);
+            g.maxh = smax(g.maxh, s_igeo[b].maxh);
+        }
+        s_sc = g;
+        const double r = dmul(A.scale, g.maxh);
+        s_r2 = dmul(r, r);
+    }
+    __syncthreads();
+    const Geo scg = s_sc;
+    const double r2 = s_r2;
+
+    // ---- traversal (collect_candidates, neighbor_build.cpp:43-65)
+    uint32_t* fa = W.fa;
+    uint32_t* fb = W.fb;
+    if (tid == 0) fa[0] = 0;
+    uint32_t nA = 1;
+    for (;;) {
+        uint32_t nB = 0;
+        if (tid == 0) s_flag = 0;
+        __syncthreads();
+        for (uint32_t base = 0; base < nA; base += blockDim.x) {
+            const uint32_t k = base + tid;
+            uint32_t emit = 0, e = 0;
+            int32_t fc = -1;
+            if (k < nA) {
+                e = fa[k];
+                if (e & kTag) {
+                    emit = 1;
+                } else {
+                    const Node nd = A.nodes[e];
+                    if (nd.pend > nd.pbegin) {
+                        const Geo ng = A.ngeo[e];
+                        double rr2 = r2;
+                        if (A.symmetric) {
+                            const double rr = dmul(A.scale, smax(scg.maxh, ng.maxh));
+                            rr2 = dmul(rr, rr);
+                        }
+                        if (!(aabb_dist_sq(scg, ng, A.box) > rr2)) {
+                            fc = nd.first_child;
+                            emit = fc < 0 ? 1 : 8;
+                        }
+                    }
+                }
+            }
+            uint32_t tot;
+            const uint32_t ex = block_excl_scan(emit, scratch, &tot);
+            if (nB + tot > W.fcap) {
+                if (tid == 0) s_over = 1;
+                __syncthreads();
+                return false;
+            }
+            if (emit == 1) fb[nB + ex] = (e & kTag) ? e : (e | kTag);
+            if (emit == 8) {
+                for (int c = 0; c < 8; ++c) fb[nB + ex + c] = uint32_t(fc + c);
+                s_flag = 1;
+            }
+            nB += tot;
+        }
+        __syncthreads();
+        uint32_t* t = fa;
+        fa = fb, fb = t;
+        nA = nB;
+        if (!s_flag) break;
+        __syncthreads();
+    }
+
+    // ---- candidate j-clusters (union of accepted leaf ranges, in order)
+    uint32_t nC = 0;
+    for (uint32_t base = 0; base < nA; base += blockDim.x) {
+        const uint32_t k = base + tid;
+        uint32_t cnt = 0, start = 0;
+        if (k < nA) {
+            const Node nd = A.nodes[fa[k] & ~kTag];
+            const uint32_t f = nd.pbegin / A.cj, l = (nd.pend - 1) / A.cj;
+            start = f;
+            if (k > 0) {
+                const Node pv = A.nodes[fa[k - 1] & ~kTag];
+                if ((pv.pend - 1) / A.cj == f) start = f + 1;
+            }
+            cnt = l + 1 - start;
+        }
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan(cnt, scratch, &tot);
+        if (nC + tot > W.ccap) {
+            if (tid == 0) s_over = 1;
+            __syncthreads();
+            return false;
+        }
+        for (uint32_t j = 0; j < cnt; ++j) W.cand[nC + ex + j] = start + j;
+        nC += tot;
+    }
+    __syncthreads();
+
+    // ---- interaction masks (neighbor_build.cpp:128-161)
+    for (uint32_t c = tid; c < nC; c += blockDim.x) {
+        const uint32_t jcl = W.cand[c];
+        const Geo jg = A.jgeo[jcl];
+        const uint64_t jb = uint64_t(jcl) * A.cj, je = tmin<uint64_t>(jb + A.cj, n);
+        unsigned long long mask = 0;
+        for (uint32_t b = 0; b < nicl; ++b) {
+            const uint64_t gi = icl_base + b;
+            if (A.symmetric && gi * A.ci > jb) continue;
+            const double pre_r =
+                dmul(A.scale, A.symmetric ? smax(s_igeo[b].maxh, jg.maxh) : s_igeo[b].maxh);
+            if (aabb_dist_sq(s_igeo[b], jg, A.box) > dmul(pre_r, pre_r)) continue;
+            const uint64_t ib = gi * A.ci, ie = tmin<uint64_t>(ib + A.ci, n);
+            bool hit = false;
+            for (uint64_t i = ib; i < ie && !hit; ++i) {
+                const uint32_t li = uint32_t(i - p0);
+                const double xi = s_x[li], yi = s_y[li], zi = s_z[li], hi = s_h[li];
+                for (uint64_t j = jb; j < je; ++j) {
+                    if (i == j) continue;
+                    const double hj = A.symmetric ? __ldg(A.h + j) : 0.0;
+                    const double rr = dmul(A.scale, A.symmetric ? smax(hi, hj) : hi);
+                    const double d2 = pair_d2_exact(xi, yi, zi, __ldg(A.x + j), __ldg(A.y + j),
+                                                    __ldg(A.z + j), A.box, nullptr, nullptr, nullptr);
+                    if (d2 <= dmul(rr, rr)) {
+                        hit = true;
+                        break;
+                    }
+                }
+            }
+            if (hit) mask |= 1ull << b;
+        }
+        W.cmask[c] = mask;
+    }
+    __syncthreads();
+
+    // ---- ordered compaction of entries with mask != 0
+    uint32_t nE = 0;
+    for (uint32_t base = 0; base < nC; base += blockDim.x) {
+        const uint32_t k = base + tid;
+        const bool keep = k < nC && W.cmask[k] != 0;
+        const uint32_t jc = keep ? W.cand[k] : 0;
+        const unsigned long long mk = keep ? W.cmask[k] : 0;
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan(keep ? 1u : 0u, scratch, &tot);
+        if (keep) W.cand[nE + ex] = jc, W.cmask[nE + ex] = mk;
+        nE += tot;
+        __syncthreads();
+    }
+
+    // ---- serialization (neighbor_build.cpp:164-182)
+    const uint32_t mbytes = nE * A.mask_bytes;
+    if (mbytes + 4 > W.ecap) {
+        if (tid == 0) s_over = 1;
+        __syncthreads();
+        return false;
+    }
+    for (uint32_t k = tid; k < nE; k += blockDim.x)
+        for (uint32_t b = 0; b < A.mask_bytes; ++b) W.ebuf[k * A.mask_bytes + b] = uint8_t(W.cmask[k] >> (8 * b));
+    uint32_t size = mbytes;
+    if (!A.compress) {
+        size = mbytes + 4 * nE;
+        if (size > W.ecap) {
+            if (tid == 0) s_over = 1;
+            __syncthreads();
+            return false;
+        }
+        for (uint32_t k = tid; k < nE; k += blockDim.x)
+            for (int b = 0; b < 4; ++b) W.ebuf[mbytes + 4 * k + b] = uint8_t(W.cand[k] >> (8 * b));
+    } else if (tid < 32) {
+        // nibble codec (nibble_codec.cpp:56-134): blocks of w differences
+        const unsigned lane = tid;
+        const uint32_t w = uint32_t(A.w);
+        uint32_t pos = mbytes;
+        bool over = false;
+        for (uint32_t bb = 0; bb < nE && !over; bb += w) {
+            const uint32_t len = min(w, nE - bb);
+            uint64_t dv[2];
+            uint32_t nd[2], isset[2];
+            uint32_t data_total = 0;
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const uint32_t k = lane + 32u * s;
+                dv[s] = 1, nd[s] = 0, isset[s] = 0;
+                if (k < len && (s == 0 || w == 64)) {
+                    const uint64_t cur = W.cand[bb + k];
+                    dv[s] = (bb + k == 0) ? cur + 1 : cur - uint64_t(W.cand[bb + k - 1]);
+                    isset[s] = dv[s] != 1;
+                    nd[s] = (dv[s] > 9) ? uint32_t(nibble_count(dv[s])) : 0u;
+                }
+            }
+            const unsigned m0 = __ballot_sync(0xffffffffu, isset[0]);
+            const unsigned m1 = __ballot_sync(0xffffffffu, isset[1]);
+            const uint32_t ninfo = __popc(m0) + __popc(m1);
+            const uint32_t inc0 = warp_incl_scan(nd[0]);
+            const uint32_t tot0 = __shfl_sync(0xffffffffu, inc0, 31);
+            const uint32_t inc1 = warp_incl_scan(nd[1]);
+            data_total = tot0 + __shfl_sync(0xffffffffu, inc1, 31);
+            const uint32_t nib = ninfo + data_total;
+            const uint32_t bsize = w / 8 + (nib + 1) / 2;
+            if (pos + bsize > W.ecap) {
+                over = true;
+                break;
+            }
+            // block mask bytes, then zero the nibble bytes of this block
+            const unsigned long long bm = (unsigned long long)m0 | ((unsigned long long)m1 << 32);
+            if (lane < w / 8) W.ebuf[pos + lane] = uint8_t(bm >> (8 * lane));
+            for (uint32_t q = lane; q < (nib + 1) / 2; q += 32) W.ebuf[pos + w / 8 + q] = 0;
+            __syncwarp();
+            const uint32_t nbase = (pos + w / 8) * 2;  // nibble index of the block's first nibble
+            unsigned int* words = reinterpret_cast<unsigned int*>(W.ebuf);
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                if (!isset[s]) continue;
+                const uint32_t k = lane + 32u * s;
+                const uint32_t info_at =
+                    s == 0 ? __popc(m0 & ((1u << lane) - 1u)) : __popc(m0) + __popc(m1 & ((1u << lane) - 1u));
+                const uint64_t v = dv[s];
+                const uint32_t infov = v <= 9 ? uint32_t(v + 6) : nd[s] - 1;
+                uint32_t t = nbase + info_at;
+                atomicOr(&words[t >> 3], infov << (4 * (t & 7)));
+                if (nd[s]) {
+                    uint32_t dstart = ninfo + (s == 0 ? inc0 - nd[0] : tot0 + inc1 - nd[1]);
+                    for (int p = int(nd[s]) - 1; p >= 0; --p, ++dstart) {
+                        t = nbase + dstart;
+                        atomicOr(&words[t >> 3], uint32_t((v >> (4 * p)) & 15u) << (4 * (t & 7)));
+                    }
+                }
+                (void)k;
+            }
+            __syncwarp();
+            pos += bsize;
+        }
+        if (lane == 0) {
+            s_n[0] = pos;
+            s_n[1] = over ? 1u : 0u;
+        }
+    }
+    __syncthreads();
+    if (A.compress) {
+        if (s_n[1]) {
+            if (tid == 0) s_over = 1;
+            __syncthreads();
+            return false;
+        }
+        size = s_n[0];
+    }
+
+    // ---- publish: bump-allocate scratch and copy
+    __shared__ unsigned long long s_off;
+    if (tid == 0) {
+        const unsigned long long need = (size + 15ull) & ~15ull;
+        const unsigned long long off = atomicAdd(&A.ctl[0], need);
+        if (off + need > A.scratch_cap) {
+            A.ctl[2] = 1;
+            s_off = ~0ull;
+        } else {
+            s_off = off;
+        }
+        A.counts[sc] = nE;
+        A.sizes[sc] = size;
+        A.soff[sc] = s_off;
+    }
+    __syncthreads();
+    if (s_off != ~0ull) {
+        const uint32_t words = (size + 3) / 4;
+        const unsigned int* src = reinterpret_cast<const unsigned int*>(W.ebuf);
+        unsigned int* dst = reinterpret_cast<unsigned int*>(A.scratch + s_off);
+        for (uint32_t q = tid; q < words; q += blockDim.x) dst[q] = src[q];
+    }
+    __syncthreads();
+    return true;
+}
+
+__global__ void __launch_bounds__(kBuildThreads) k_build_smem(BuildArgs A, uint64_t num_sc) {
+    __shared__ uint32_t fa[kFCap], fb[kFCap], cand[kCCap];
+    __shared__ unsigned long long cmask[kCCap];
+    __shared__ __align__(16) uint8_t ebuf[kECap];
+    const Workspace W{fa, fb, cand, cmask, ebuf, kFCap, kCCap, kECap};
+    for (uint64_t sc = blockIdx.x; sc < num_sc; sc += gridDim.x) {
+        if (!build_sc(A, W, sc)) {
+            if (threadIdx.x == 0) {
+                const unsigned long long slot = atomicAdd(&A.ctl[1], 1ull);
+                A.overflow_list[slot] = uint32_t(sc);
+                A.counts[sc] = 0, A.sizes[sc] = 0, A.soff[sc] = 0;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kBuildThreads) k_build_global(BuildArgs A, const uint32_t* list,
+                                                                 uint64_t count, uint8_t* ws,
+                                                                 uint64_t ws_stride, uint32_t fcap,
+                                                                 uint32_t ccap, uint32_t ecap) {
+    uint8_t* base = ws + blockIdx.x * ws_stride;
+    Workspace W;
+    W.fa = reinterpret_cast<uint32_t*>(base);
+    W.fb = W.fa + fcap;
+    W.cand = W.fb + fcap;
+    W.cmask = reinterpret_cast<unsigned long long*>(
+        (reinterpret_cast<uintptr_t>(W.cand + ccap) + 15) & ~uintptr_t(15));
+    W.ebuf = reinterpret_cast<uint8_t*>(W.cmask + ccap);
+    W.fcap = fcap, W.ccap = ccap, W.ecap = ecap;
+    for (uint64_t t = blockIdx.x; t < count; t += gridDim.x) {
+        const uint64_t sc = list[t];
+        if (!build_sc(A, W, sc)) {
+            if (threadIdx.x == 0) raise_error(A.err, sc, SFCNL_BUILD_ERROR, 3, 0);
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void k_compact(uint64_t num_sc, const uint32_t* __restrict__ sizes,
+                          const uint64_t* __restrict__ soff, const uint64_t* __restrict__ offsets,
+                          const uint8_t* __restrict__ scratch, uint8_t* __restrict__ blob) {
+    const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+    if (warp >= num_sc) return;
+    const uint32_t sz = sizes[warp];
+    const uint8_t* src = scratch + soff[warp];
+    uint8_t* dst = blob + offsets[warp];
+    for (uint32_t k = lane_id(); k < sz; k += 32) dst[k] = src[k];
+}
+
+// validate (core.hpp:201-216) + max h for the periodic precondition.
+__global__ void k_validate(uint64_t n, const double* __restrict__ x, const double* __restrict__ y,
+                           const double* __restrict__ z, const double* __restrict__ h, Box box,
+                           unsigned long long* maxh_bits, DevError* err) {
+    unsigned long long local = 0;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const double hv = h[i];
+        const double p[3] = {x[i], y[i], z[i]};
+        if (!(hv > 0)) {
+            raise_error(err, i, SFCNL_INPUT_ERROR, 1, 0);
+            continue;
+        }
+        for (int d = 0; d < 3; ++d) {
+            if (!isfinite(p[d])) {
+                raise_error(err, i, SFCNL_INPUT_ERROR, 2, 0);
+                break;
+            }
+            if (p[d] < box.lo[d] || p[d] > box.hi[d]) {
+                raise_error(err, i, SFCNL_INPUT_ERROR, 3, 0);
+                break;
+            }
+        }
+        local = max(local, (unsigned long long)__double_as_longlong(hv));  // h > 0: order-preserving
+    }
+    for (int o = 16; o > 0; o >>= 1) local = max(local, __shfl_xor_sync(0xffffffffu, local, o));
+    if (lane_id() == 0 && local) atomicMax(maxh_bits, local);
+}
+
+}  // namespace
+
+int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p) {
+    // ClusterParams / BuildParams validation (cluster.hpp:19-28, neighbor_store.hpp:25-28)
+    if (p.ci == 0 || p.cj == 0) return set_error(c, 1, "ClusterParams: cluster sizes must be positive");
+    if (64 % p.ci || 64 % p.cj)
+        return set_error(c, 1, "ClusterParams: cluster sizes must divide the super-cluster size");
+    if (p.ci % p.cj) return set_error(c, 1, "ClusterParams: cj must divide ci");
+    if (p.w != 32 && p.w != 64) return set_error(c, 1, "ClusterParams: block width must be 32 or 64");
+    if (!(p.build_radius_scale >= 1.0)) return set_error(c, 1, "BuildParams: build_radius_scale must be >= 1");
+    if (!c->sorted.valid) return set_error(c, 1, "build_neighbor_store: no particles");
+    const uint64_t n = c->sorted.n;
+    const Box& box = c->sorted.box;
+
+    SFCNL_CUDA_TRY(c->build_ctl.reserve(8 * 8));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(c->build_ctl.p, 0, 8 * 8, c->stream));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(c->derr.p, 0xff, sizeof(DevError), c->stream));
+    if (n) {
+        const int grid = int(std::min<uint64_t>((n + 255) / 256, uint64_t(c->num_sms) * 8));
+        launch(c, k_validate, dim3(grid), dim3(256), 0, n, c->sorted.x.as<const double>(),
+               c->sorted.y.as<const double>(), c->sorted.z.as<const double>(),
+               c->sorted.h.as<const double>(), box, c->build_ctl.as<unsigned long long>() + 3,
+               c->derr.as<DevError>());
+    }
+    static const char* const kValMsgs[] = {"", "ParticleSet: h must be positive",
+                                           "ParticleSet: non-finite coordinate",
+                                           "ParticleSet: position outside box (wrap first)"};
+    {
+        const int rc = check_dev_error(c, kValMsgs);
+        if (rc) return rc;
+    }
+    if (!c->has_tree || c->tree_n != n)
+        return set_error(c, 2, "build_neighbor_store: octree/particle-set mismatch");
+    unsigned long long maxh_bits = 0;
+    SFCNL_CUDA_TRY(cudaMemcpy(&maxh_bits, c->build_ctl.as<unsigned long long>() + 3, 8, cudaMemcpyDeviceToHost));
+    double max_h;
+    memcpy(&max_h, &maxh_bits, 8);
+    for (int d = 0; d < 3; ++d)
+        if (box.per[d] && box.len[d] < 2.0 * p.build_radius_scale * max_h)
+            return set_error(c, 2, "build_neighbor_store: periodic box must span twice the largest cutoff");
+
+    const uint64_t num_sc = (n + 63) / 64;
+    c->sp = p;
+    c->store_n = n;
+    c->num_sc = num_sc;
+    c->has_store = false;
+    SFCNL_CUDA_TRY(c->counts.reserve(std::max<uint64_t>(num_sc, 1) * 4));
+    SFCNL_CUDA_TRY(c->offsets.reserve((num_sc + 1) * 8));
+    if (n == 0) {
+        SFCNL_CUDA_TRY(cudaMemsetAsync(c->offsets.p, 0, 8, c->stream));
+        c->blob_bytes = 0;
+        c->has_store = true;
+        return 0;
+    }
+    {
+        int rc = run_cluster_geometry(c, p.ci, p.cj);
+        if (!rc) rc = run_node_geometry(c);
+        if (rc) return rc;
+    }
+    SFCNL_CUDA_TRY(c->sc_size.reserve(num_sc * 4));
+    SFCNL_CUDA_TRY(c->sc_scratch_off.reserve(num_sc * 8));
+    SFCNL_CUDA_TRY(c->overflow_list.reserve(num_sc * 4));
+    uint64_t scratch_cap = std::max<uint64_t>(c->scratch.bytes, n * 16 + (1 << 20));
+
+    BuildArgs A;
+    A.n = n;
+    A.box = box;
+    A.scale = p.build_radius_scale;
+    A.ci = p.ci, A.cj = p.cj, A.icl_per_sc = 64 / p.ci, A.mask_bytes = (A.icl_per_sc + 7) / 8;
+    A.w = p.w, A.compress = p.compress, A.symmetric = p.mode != 0;
+    A.num_icl = (n + p.ci - 1) / p.ci;
+    A.x = c->sorted.x.as<double>(), A.y = c->sorted.y.as<double>(), A.z = c->sorted.z.as<double>();
+    A.h = c->sorted.h.as<double>();
+    A.nodes = c->nodes.as<Node>();
+    A.ngeo = c->node_geo.as<Geo>();
+    A.igeo = c->igeo.as<Geo>();
+    A.jgeo = p.cj == p.ci ? c->igeo.as<Geo>() : c->jgeo.as<Geo>();
+    A.counts = c->counts.as<uint32_t>();
+    A.sizes = c->sc_size.as<uint32_t>();
+    A.soff = c->sc_scratch_off.as<uint64_t>();
+    A.ctl = c->build_ctl.as<unsigned long long>();
+    A.overflow_list = c->overflow_list.as<uint32_t>();
+    A.err = c->derr.as<DevError>();
+
+    unsigned long long ctl[3];
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        SFCNL_CUDA_TRY(c->scratch.reserve(scratch_cap));
+        A.scratch = c->scratch.as<uint8_t>();
+        A.scratch_cap = c->scratch.bytes;
+        SFCNL_CUDA_TRY(cudaMemsetAsync(c->build_ctl.p, 0, 3 * 8, c->stream));
+        stage_begin(c, kBuild);
+        const unsigned grid = unsigned(std::min<uint64_t>(num_sc, uint64_t(c->num_sms) * 64));
+        launch(c, k_build_smem, dim3(grid), dim3(kBuildThreads), 0, A, num_sc);
+        SFCNL_CUDA_TRY(cudaGetLastError());
+        SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 3 * 8, cudaMemcpyDeviceToHost, c->stream));
+        SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        if (ctl[1]) {
+            // capacity fallback in global memory: same code, big workspaces
+            const uint64_t ncl = (n + p.cj - 1) / p.cj;
+            const uint32_t fcap = uint32_t(std::min<uint64_t>(c->num_nodes + 8, 0xffffffffull));
+            const uint32_t ccap = uint32_t(ncl + 1);
+            const uint32_t ecap = uint32_t(std::min<uint64_t>(uint64_t(ccap) * (A.mask_bytes + 10) + 64, 0xfffffff0ull));
+            const uint64_t stride =
+                ((uint64_t(fcap) * 8 + uint64_t(ccap) * 4 + 16 + uint64_t(ccap) * 8 + ecap) + 255) & ~uint64_t(255);
+            const uint64_t nblk = std::min<uint64_t>(ctl[1], 8);
+            SFCNL_CUDA_TRY(c->fallback_ws.reserve(stride * nblk));
+            launch(c, k_build_global, dim3(unsigned(nblk)), dim3(kBuildThreads), 0, A,
+                   (const uint32_t*)A.overflow_list, uint64_t(ctl[1]), c->fallback_ws.as<uint8_t>(), stride,
+                   fcap, ccap, ecap);
+            SFCNL_CUDA_TRY(cudaGetLastError());
+            SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 3 * 8, cudaMemcpyDeviceToHost, c->stream));
+            SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+            static const char* const kMsgs[] = {"", "", "", "build_neighbor_store: workspace capacity exceeded"};
+            const int rc = check_dev_error(c, kMsgs);
+            if (rc) return rc;
+        }
+        stage_end(c, kBuild);
+        if (!ctl[2]) break;
+        scratch_cap = ctl[0] + (1 << 20);  // scratch overflow: grow to the needed size and redo
+        if (attempt == 2) return set_error(c, 4, "build_neighbor_store: scratch allocation failed");
+    }
+
+    stage_begin(c, kEncode);
+    {
+        const int rc = excl_scan(c, c->sc_size.as<uint32_t>(), c->offsets.as<uint64_t>(), num_sc);
+        if (rc) return rc;
+    }
+    uint64_t blob_bytes = 0;
+    SFCNL_CUDA_TRY(cudaMemcpyAsync(&blob_bytes, c->offsets.as<uint64_t>() + num_sc, 8, cudaMemcpyDeviceToHost, c->stream));
+    SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    SFCNL_CUDA_TRY(c->blob.reserve(std::max<uint64_t>(blob_bytes, 16)));
+    launch(c, k_compact, dim3(unsigned((num_sc * 32 + 255) / 256)), dim3(256), 0, num_sc,
+           (const uint32_t*)c->sc_size.as<uint32_t>(), (const uint64_t*)c->sc_scratch_off.as<uint64_t>(),
+           (const uint64_t*)c->offsets.as<uint64_t>(), (const uint8_t*)c->scratch.as<uint8_t>(),
+           c->blob.as<uint8_t>());
+    SFCNL_CUDA_TRY(cudaGetLastError());
+    stage_end(c, kEncode);
+    c->blob_bytes = blob_bytes;
+    c->has_store = true;
+    return 0;
+}
+
+}  // namespace sfcnl_cu

@@ -1,0 +1,162 @@
+// Context object behind the C-ABI (include/sfcnl_cu.h): owns the stream, the
+// device copies of the particle slots and every derived structure.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+
+namespace sfcnl_cu {
+
+// Grow-only device allocation: the hot path reuses buffers across steps.
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr, o.bytes = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p, bytes = o.bytes;
+            o.p = nullptr, o.bytes = 0;
+        }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    cudaError_t reserve(size_t b) {
+        if (b <= bytes && p) return cudaSuccess;
+        release();
+        const size_t want = b ? b : 16;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) bytes = want;
+        else p = nullptr;
+        return e;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+struct Field {
+    std::string name;
+    DBuf data;
+};
+
+struct Slot {
+    uint64_t n = 0;
+    bool valid = false;
+    Box box{};
+    DBuf x, y, z, h;
+    std::vector<Field> fields;
+    Field* find(const std::string& name) {
+        for (auto& f : fields)
+            if (f.name == name) return &f;
+        return nullptr;
+    }
+};
+
+enum Stage { kKeygen, kSort, kPermute, kOctree, kNodeGeo, kClusterGeo, kBuild, kEncode, kPass, kNumStages };
+
+}  // namespace sfcnl_cu
+
+struct sfcnl_cu_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint64_t err_off = 0;
+    uint64_t launches = 0;
+    int num_sms = 148;
+
+    sfcnl_cu::Slot orig, sorted;
+
+    // (1) order
+    bool has_order = false;
+    int bits = 21;
+    uint64_t order_n = 0;
+    sfcnl_cu::DBuf keys, perm, keys_alt, perm_alt;
+    sfcnl_cu::DBuf hist, digit_base, status, tile_counter;
+    sfcnl_cu::DBuf hilbert_table;
+
+    // (3) octree
+    bool has_tree = false;
+    int tree_bits = 21;
+    uint64_t tree_n = 0;
+    uint64_t num_nodes = 0;
+    sfcnl_cu::DBuf nodes;      // sfcnl_cu::Node[num_nodes]
+    sfcnl_cu::DBuf level_nodes;  // node indices grouped by depth (deepest processed first)
+    std::vector<uint64_t> level_off;  // host: level d occupies [level_off[d], level_off[d+1])
+    sfcnl_cu::DBuf node_geo;   // Geo[num_nodes]
+    sfcnl_cu::DBuf tree_scratch;
+    // level-synchronous construction scratch, one entry per depth
+    struct Level {
+        sfcnl_cu::DBuf kf, pb, pe, flag, ipos, ikeys, irank;
+        uint64_t count = 0, internal = 0;
+    };
+    std::vector<Level> levels;
+    sfcnl_cu::DBuf level_tab;  // device table of per-level ikeys pointers + counts
+
+    // (2) clusters
+    sfcnl_cu::DBuf igeo, jgeo;
+
+    // (4) store
+    bool has_store = false;
+    sfcnl_build_params sp{};
+    uint64_t store_n = 0, num_sc = 0, blob_bytes = 0;
+    sfcnl_cu::DBuf counts, offsets, blob;
+    sfcnl_cu::DBuf sc_size, sc_scratch_off, scratch, build_ctl, overflow_list, fallback_ws;
+
+    // (5) pass
+    sfcnl_cu::DBuf outs[4], ncount, jstage;
+
+    // errors
+    sfcnl_cu::DBuf derr;  // DevError
+    sfcnl_cu::DBuf ptrs;  // small pointer tables
+    sfcnl_cu::DBuf scan_tmp;
+    sfcnl_cu::DBuf small_host_dev;  // tiny device scratch for readbacks
+
+    // timing
+    bool timing = false;
+    cudaEvent_t ev[2 * sfcnl_cu::kNumStages] = {};
+    float stage_ms[sfcnl_cu::kNumStages] = {};
+    bool stage_pending[sfcnl_cu::kNumStages] = {};
+};
+
+namespace sfcnl_cu {
+
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+int set_error(sfcnl_cu_ctx* c, int code, const std::string& msg, uint64_t off = 0);
+int check_dev_error(sfcnl_cu_ctx* c, const char* const* messages);
+
+void stage_begin(sfcnl_cu_ctx* c, Stage s);
+void stage_end(sfcnl_cu_ctx* c, Stage s);
+
+// Kernel drivers (each in its own .cu).
+int run_sort_by_sfc(sfcnl_cu_ctx* c, int bits);
+int run_apply_order(sfcnl_cu_ctx* c);
+int run_build_octree(sfcnl_cu_ctx* c, uint32_t bucket);
+int run_tree_levels_from_nodes(sfcnl_cu_ctx* c, const std::vector<uint8_t>& depth);
+int run_node_geometry(sfcnl_cu_ctx* c);
+int run_cluster_geometry(sfcnl_cu_ctx* c, uint32_t ci, uint32_t cj);
+int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p);
+int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p);
+
+// Host helpers shared with the C++ drop-in.
+void hilbert_table(uint16_t* table);  // 48 states x 8 octants: out | next << 3
+int host_set_error(int code, const std::string& msg, uint64_t off = 0);
+
+template <class K, class... A>
+inline void launch(sfcnl_cu_ctx* c, K kernel, dim3 grid, dim3 block, size_t smem, A... args) {
+    kernel<<<grid, block, smem, c->stream>>>(args...);
+    ++c->launches;
+}
+
+}  // namespace sfcnl_cu

@@ -1,0 +1,206 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the golden fixtures of
+the compiled reference and against the plain-C restatement on seeded inputs.
+
+Bar (north star): SFC keys/perm, octree nodes, node/cluster geometry and the
+NeighborStore bytes bit-exact; neighbor_count exact; fp64 pass bit-equal to
+reduce<double> in gather mode (1e-12 relative in symmetric mode, whose j-side
+accumulation order differs); mixed pass within 1e-5 (density relative, LJ force
+normwise against sum_j |F_ij|)."""
+import numpy as np
+import pytest
+
+import paper_2602_19873_b200 as S
+from conftest import golden_particles, oracle_particles, oracle_store
+from oracle.oracle import Oracle, Particles
+
+pytestmark = pytest.mark.gpu
+P = Oracle("port")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return S.Context(0)
+
+
+def _bp(g):
+    ci, cj, w, mode, comp = (int(v) for v in g["params"])
+    return S.BuildParams(S.ClusterParams(ci, cj, w), mode, bool(comp), float(g["scale"][0]))
+
+
+def _lj_norm_err(out, ref, absref):
+    err = np.sqrt(sum((out[k] - ref[k]) ** 2 for k in range(3)))
+    return np.max(err / np.maximum(absref, 1e-300))
+
+
+def test_sort_octree_store_match_reference(golden, ctx):
+    g = golden
+    ps, box = golden_particles(g)
+    order = S.sort_by_sfc(ps, box, ctx=ctx)
+    assert np.array_equal(order.keys, g["keys"])
+    assert np.array_equal(order.perm, g["perm"])
+    tree = S.build_octree(order, 64, ctx=ctx)
+    for f in ("key_first", "key_last", "first_child", "depth"):
+        assert np.array_equal(tree.nodes[f], g[f]), f
+    assert np.array_equal(tree.nodes["particle_begin"], g["pbegin"])
+    assert np.array_equal(tree.nodes["particle_end"], g["pend"])
+    sorted_ps = S.apply_sfc_order(ps, order, ctx=ctx)
+    sp, _ = golden_particles(g, sorted_=True)
+    for f in "xyzh":
+        assert np.array_equal(getattr(sorted_ps, f), getattr(sp, f))
+    lo, hi = S.compute_node_aabbs(tree, sorted_ps, ctx=ctx)
+    assert np.array_equal(lo, g["node_lo"]) and np.array_equal(hi, g["node_hi"])
+    assert np.array_equal(S.compute_node_max_radius(tree, sorted_ps, ctx=ctx), g["node_radius"])
+    store = S.build_neighbor_store(sorted_ps, box, tree, _bp(g), ctx=ctx)
+    assert np.array_equal(store.counts, g["counts"])
+    assert np.array_equal(store.offsets, g["offsets"])
+    assert np.array_equal(store.blob, g["blob"])
+
+
+def test_pass_fp64_matches_reference(golden, ctx):
+    g = golden
+    sp, box = golden_particles(g, sorted_=True)
+    store = S.NeighborStore(_bp(g), len(g["x"]), g["counts"], g["offsets"], g["blob"])
+    qs, sigma = float(g["scale"][1]), float(g["scale"][2])
+    mode = int(g["params"][3])
+    for kern, k in (("count", S.count_kernel()), ("density", S.sph_density_kernel()), ("lj", S.lj_kernel(1.0, sigma))):
+        res = S.reduce(sp, box, store, k, S.PassConfig(qs, S.F64), ctx=ctx)
+        assert np.array_equal(res.neighbor_count, g[f"{kern}_double_count"]), kern
+        for o in range(len(k.names)):
+            ref = g[f"{kern}_double_{o}"]
+            if mode == 0:
+                assert np.array_equal(res.outputs[o], ref), (kern, o)
+            else:
+                np.testing.assert_allclose(res.outputs[o], ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+
+
+def test_pass_mixed_within_tolerance(golden, ctx):
+    g = golden
+    sp, box = golden_particles(g, sorted_=True)
+    store = S.NeighborStore(_bp(g), len(g["x"]), g["counts"], g["offsets"], g["blob"])
+    qs, sigma = float(g["scale"][1]), float(g["scale"][2])
+    res = S.reduce(sp, box, store, S.sph_density_kernel(), S.PassConfig(qs, S.MIXED), ctx=ctx)
+    assert np.array_equal(res.neighbor_count, g["density_double_count"])
+    ref = g["density_double_0"]
+    assert np.max(np.abs(res.outputs[0] - ref) / np.abs(ref)) <= 1e-5
+    res = S.reduce(sp, box, store, S.lj_kernel(1.0, sigma), S.PassConfig(qs, S.MIXED), ctx=ctx)
+    assert np.array_equal(res.neighbor_count, g["lj_double_count"])
+    # normwise bound: |F - F_ref| <= 1e-5 * sum_j |F_ij|
+    op = oracle_particles(g, sorted_=True)
+    absf = _sum_abs_pair_forces(op, oracle_store(g), qs, sigma)
+    assert _lj_norm_err(res.outputs, [g[f"lj_double_{k}"] for k in range(3)], absf) <= 1e-5
+
+
+def _sum_abs_pair_forces(op, st, qs, sigma):
+    """sum_j |F_ij| per i, via the restatement on a unit-force trick: evaluate LJ
+    with the same pair set and accumulate |coef| * |dx| on the host."""
+    # The restatement returns signed sums; recover sum |F_ij| from a brute pass.
+    n = op.n
+    out = np.zeros(n)
+    L = op.box6[3:] - op.box6[:3]
+    pos = np.stack([op.x, op.y, op.z], 1)
+    from oracle.oracle import Oracle as _O  # noqa: F401
+    idx = _pairs_from_store(st, n)
+    for i, js in idx.items():
+        d = pos[i] - pos[js]
+        for a in range(3):
+            if op.periodic[a]:
+                d[:, a] -= L[a] * np.rint(d[:, a] / L[a])
+        d2 = (d * d).sum(1)
+        r = qs * op.h[i]
+        d2 = d2[(d2 <= r * r) & (d2 > 0)]
+        inv2 = 1.0 / d2
+        s6 = (sigma * sigma * inv2) ** 3
+        coef = 24.0 * inv2 * (2 * s6 * s6 - s6)
+        out[i] = np.sum(np.abs(coef) * np.sqrt(d2))
+    return out
+
+
+def _pairs_from_store(st, n):
+    from collections import defaultdict
+    P_ = Oracle("port")
+    pairs = defaultdict(list)
+    mb = (64 // st.ci + 7) // 8
+    for sc in range(len(st.counts)):
+        c = int(st.counts[sc])
+        if not c:
+            continue
+        b, e = int(st.offsets[sc]), int(st.offsets[sc + 1])
+        rec = st.blob[b:b + c * mb]
+        data = st.blob[b + c * mb:e]
+        if st.compress:
+            idx, _ = P_.decode(data, c, st.w)
+        else:
+            idx = np.frombuffer(data.tobytes(), "<u4")
+        for k, jcl in enumerate(idx):
+            mask = int.from_bytes(bytes(rec[k * mb:(k + 1) * mb]), "little")
+            js = list(range(int(jcl) * st.cj, min(int(jcl) * st.cj + st.cj, n)))
+            for bit in range(64 // st.ci):
+                if (mask >> bit) & 1:
+                    for i in range(sc * 64 + bit * st.ci, min(sc * 64 + (bit + 1) * st.ci, n)):
+                        pairs[i].extend(j for j in js if j != i)
+    return {i: np.array(v) for i, v in pairs.items()}
+
+
+@pytest.mark.parametrize("gen,n,cfg", [
+    ("uniform", 40000, (8, 8, 32, 0, 1, 1.0)),
+    ("evrard", 40000, (8, 8, 32, 0, 1, 1.0)),
+    ("uniform", 20011, (8, 4, 64, 0, 1, 1.0)),
+    ("uniform", 12345, (8, 8, 32, 1, 1, 1.0)),
+    ("uniform", 30000, (8, 8, 32, 0, 0, 1.15)),
+    ("uniform", 3001, (1, 1, 32, 0, 1, 1.0)),
+])
+def test_pipeline_vs_restatement(ctx, gen, n, cfg):
+    ci, cj, w, mode, comp, scale = cfg
+    if gen == "uniform":
+        op = P.make_uniform(n, float(n), 150.0, (1, 1, 1), 0.2 if mode else 0.0, 7)
+    else:
+        op = P.make_evrard(n, 120.0, False, (0, 0, 0), 7)
+    keys, perm, sp, tree, st = P.pipeline(op, ci=ci, cj=cj, w=w, mode=mode, compress=comp, scale=scale)
+    ps = S.ParticleSet(op.x, op.y, op.z, op.h, {"m": op.m, "q": op.q})
+    box = S.SimulationBox(tuple(op.box6[:3]), tuple(op.box6[3:]), tuple(bool(v) for v in op.periodic))
+    order = S.sort_by_sfc(ps, box, ctx=ctx)
+    assert np.array_equal(order.keys, keys) and np.array_equal(order.perm, perm)
+    gtree = S.build_octree(order, 64, ctx=ctx)
+    assert np.array_equal(gtree.nodes["particle_end"], tree.pend)
+    assert np.array_equal(gtree.nodes["first_child"], tree.first_child)
+    sps = S.apply_sfc_order(ps, order, ctx=ctx)
+    bp = S.BuildParams(S.ClusterParams(ci, cj, w), mode, bool(comp), scale)
+    store = S.build_neighbor_store(sps, box, gtree, bp, ctx=ctx)
+    assert np.array_equal(store.counts, st.counts)
+    assert np.array_equal(store.offsets, st.offsets)
+    assert np.array_equal(store.blob, st.blob)
+    outs, cnt = P.reduce("density", sp, st, query_scale=1.0)
+    res = S.reduce(sps, box, store, S.sph_density_kernel(), S.PassConfig(1.0, S.F64), ctx=ctx)
+    assert np.array_equal(res.neighbor_count, cnt)
+    if mode == 0:
+        assert np.array_equal(res.outputs[0], outs[0])
+    else:
+        np.testing.assert_allclose(res.outputs[0], outs[0], rtol=1e-12)
+    res = S.reduce(sps, box, store, S.sph_density_kernel(), S.PassConfig(1.0, S.MIXED), ctx=ctx)
+    assert np.array_equal(res.neighbor_count, cnt)
+    assert np.max(np.abs(res.outputs[0] - outs[0]) / np.abs(outs[0])) <= 1e-5
+
+
+def test_errors_map_to_reference_exceptions(ctx):
+    ps, box = S.make_uniform(S.UniformSpec(n=2000, density=2000.0, target_neighbors=50.0))
+    bad = S.ParticleSet(ps.x.copy(), ps.y, ps.z, ps.h)
+    bad.x[17] = np.nan
+    with pytest.raises(S.InputError):
+        S.sort_by_sfc(bad, box, ctx=ctx)
+    order = S.sort_by_sfc(ps, box, ctx=ctx)
+    tree = S.build_octree(order, ctx=ctx)
+    sps = S.apply_sfc_order(ps, order, ctx=ctx)
+    small = S.SimulationBox(box.lo, box.hi, box.periodic)
+    big_h = S.ParticleSet(sps.x, sps.y, sps.z, sps.h * 20, sps.fields)
+    with pytest.raises(S.BuildError):  # periodic box < 2 * cutoff (neighbor_build.cpp:83-87)
+        S.build_neighbor_store(big_h, small, tree, S.BuildParams(), ctx=ctx)
+    store = S.build_neighbor_store(sps, box, tree, S.BuildParams(), ctx=ctx)
+    with pytest.raises(S.InputError):  # query_scale > build scale (reduce.hpp:47-48)
+        S.reduce(sps, box, store, S.count_kernel(), S.PassConfig(1.5), ctx=ctx)
+    broken = S.NeighborStore(store.build, store.n, store.counts, store.offsets, store.blob.copy())
+    sc = int(np.argmax(store.counts))
+    broken.offsets = store.offsets.copy()
+    broken.offsets[sc + 1:] -= 3  # truncate one super-cluster's index stream
+    broken.blob = np.delete(store.blob, slice(int(store.offsets[sc + 1]) - 3, int(store.offsets[sc + 1])))
+    with pytest.raises(S.DecodeError):
+        S.reduce(sps, box, broken, S.count_kernel(), S.PassConfig(1.0), ctx=ctx)
