@@ -1,0 +1,308 @@
+"""Benchmark: neighbor-list build + neighborhood pass (BASELINE.json metric).
+
+One step = the reference's build-and-query sequence on one batch of particles
+(bench.cpp:147-186, with every stage timed, including the sort/permute/octree
+that run_bench leaves out): sort_by_sfc -> apply_sfc_order -> build_octree ->
+build_neighbor_store -> reduce(SPH density) -> reduce(Lennard-Jones).
+
+Workload (BASELINE.json configs[1], "C2"): 2^26 uniform random particles per GPU in
+a periodic unit cube, h for ~200 neighbours, ClusterParams(8,8,32), gather,
+compressed; LJ sigma = 0.5 * N^-1/3 (bench.cpp:73-74); mixed-precision pass
+(exact pair set, values within 1e-5). Inputs (2.7 GB) exceed L2 (126 MB).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference] [--n N]
+
+Multi-GPU (torchrun): each rank owns its own 2^26-particle domain (weak scaling,
+no data-path collective); the step time is the max over ranks.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ns/particle for list build + neighborhood pass (SPH density + LJ)"
+UNIT = "ns/particle"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--n", type=int, default=1 << 26)
+    p.add_argument("--target", type=float, default=200.0)
+    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--cpu-sample", type=int, default=1 << 20)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_init(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def allreduce_max(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index, self.samples, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) == 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[3 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+# ---------------------------------------------------------------- CPU reference
+def cpu_reference(n, target, steps=1):
+    """The unmodified reference (oracle/_ref) on all host threads; every stage timed."""
+    from oracle.oracle import Oracle
+    import ctypes as C
+    R = Oracle("reference")
+    ps = R.make_uniform(n, float(n), target, (1, 1, 1), 0.0, 42)
+    threads = os.cpu_count() or 1
+    sigma = 0.5 * (1.0 / n) ** (1.0 / 3.0)
+    times = []
+    per = (C.c_int * 3)(1, 1, 1)
+    D = C.c_double
+    stages = None
+    for _ in range(steps):
+        t = (C.c_double * 7)()
+        st = (C.c_double * 4)()
+        rc = R.lib.ref_pipeline(C.c_uint64(n), *(a.ctypes.data_as(C.POINTER(D)) for a in (ps.x, ps.y, ps.z, ps.h, ps.m)),
+                                ps.box6.ctypes.data_as(C.POINTER(D)), per, C.c_uint32(8), C.c_uint32(8), C.c_int(32),
+                                D(1.0), C.c_int(threads), D(1.0), D(sigma), C.c_int(1), t, st, None)
+        R._check(rc)
+        times.append(t[6])
+        stages = {k: t[i] for i, k in enumerate(["sort_by_sfc", "apply_sfc_order", "build_octree",
+                                                 "build_neighbor_store", "reduce_density", "reduce_lj", "total"])}
+    ms = float(np.median(times))
+    return {"value": ms * 1e6 / n, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"uniform {n} particles (same density/h for {target:.0f} nbrs), full build + density + LJ, "
+                      f"median of {steps}", "stages_ms": stages, "bytes_per_particle": st[0]}
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    n = args.cpu_sample
+    t0 = time.time()
+    for _ in range(args.warmup if args.warmup < 2 else 1):
+        cpu_reference(n, args.target, 1)
+    res = cpu_reference(n, args.target, max(1, min(args.steps, 3)))
+    out = {"metric": METRIC, "value": res["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+           "steps": max(1, min(args.steps, 3)), "warmup": args.warmup, "ms_per_step": res["value"] * n / 1e6,
+           "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (reference make_uniform, seed 42)",
+           "config": {"workload": "C2 uniform periodic, 200 nbrs, 8x8 gather compressed, build+density+LJ",
+                      "n_per_gpu": args.n, "sample_n": n},
+           "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+           "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "stages_ms": res["stages_ms"], "wall_s": round(time.time() - t0, 1)}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------- B200 arm
+def run_b200(args, ws, rank, local):
+    import torch
+    import paper_2602_19873_b200 as S
+
+    n = args.n
+    ctx = S.Context(local)
+    spec = S.UniformSpec(n=n, density=float(n), target_neighbors=args.target, seed=42 + rank)
+    ps, box = S.make_uniform(spec)
+    # pinned host buffers for the end-to-end leg
+    pinned = {}
+    for name in ("x", "y", "z", "h"):
+        t = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        t.numpy()[:] = getattr(ps, name)
+        pinned[name] = t
+    t = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    t.numpy()[:] = ps.fields["m"]
+    pinned["m"] = t
+    pps = S.ParticleSet(pinned["x"].numpy(), pinned["y"].numpy(), pinned["z"].numpy(), pinned["h"].numpy(),
+                        {"m": pinned["m"].numpy()})
+    sigma = 0.5 * (1.0 / n) ** (1.0 / 3.0)
+    kernels = [S.sph_density_kernel(), S.lj_kernel(1.0, sigma)]
+    bp = S.BuildParams(S.ClusterParams(8, 8, 32), S.GATHER, True, 1.0)
+    pipe = S.Pipeline(ctx, pps, box, bp, kernels, S.PassConfig(1.0, S.MIXED))
+    pipe.upload()
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
+
+    for _ in range(args.warmup):
+        pipe.run()
+    ctx.synchronize()
+    # per-stage breakdown from one instrumented step (not part of the timed steps)
+    ctx.set_timing(True)
+    stage = {}
+    ctx.sort(pipe.bits)
+    ctx.apply_order()
+    ctx.octree(pipe.bucket)
+    ctx.build_store(bp)
+    st = ctx.stage_times()
+    stage.update({k: v for k, v in st.items() if k != "pass"})
+    for k in kernels:
+        ctx.reduce(k, pipe.cfg, n, download=False)
+        stage["pass_" + k.names[0]] = ctx.stage_times()["pass"]
+    ctx.set_timing(False)
+
+    barrier(ws)
+    ctx.synchronize()
+    launches0 = ctx.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            pipe.run()
+        ev1.record(stream)
+        ev1.synchronize()
+    ctx.synchronize()
+    barrier(ws)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    launches = (ctx.launch_count() - launches0) // args.steps
+    ms_max = allreduce_max(ms, ws)
+    value = ms_max * 1e6 / n  # whole job: ws*n particles in ms_max -> per particle of the job * ws / ws
+    value_job = ms_max * 1e6 / (n * ws)
+
+    # end-to-end through the C-ABI with host (pinned) buffers
+    e2e_ms = []
+    for _ in range(args.e2e_steps):
+        ctx.synchronize()
+        barrier(ws)
+        t0 = time.perf_counter()
+        pipe.run_e2e()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e = allreduce_max(float(np.median(e2e_ms)), ws)
+
+    bpp = (pipe.blob_bytes + 4 * pipe.num_sc + 8 * (pipe.num_sc + 1)) / n
+    pk, pk_kind = peaks()
+    # dominant kernel + its algorithmic bytes
+    algo_bytes = {
+        "build": 32 + 8 + 3.77,            # sorted x,y,z,h read + node/cluster geo (amortised) + store write
+        "pass_rho": 32 + 8 + 3.77 + 12,    # i x,y,z,h + j m + list + rho/count written
+        "pass_fx": 32 + 3.77 + 36,         # i x,y,z,h + list + 4 outputs + count written
+        "sort": 24 * ((3 * 21 + 7) // 8),
+    }
+    dom = max(stage, key=lambda k: stage[k])
+    dom_ms = stage[dom]
+    ab = algo_bytes.get(dom, 48.0) * n
+    achieved = ab / (dom_ms * 1e-3) / 1e9
+    out = {
+        "metric": METRIC, "value": round(value_job, 4), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_max, 3), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "mixed f32/f64 (exact f64 cutoff decisions)",
+        "data": "synthetic (make_uniform, seed 42+rank)",
+        "config": {"workload": "C2: 2^26 uniform periodic unit cube per GPU, 200 nbrs, ClusterParams(8,8,32) "
+                               "gather compressed, build + SPH density + LJ (mixed)",
+                   "n_per_gpu": n, "global_particles": n * ws, "l2": "inputs 2.7 GB > L2, no flush",
+                   "bytes_per_particle": round(bpp, 4), "parallelism": f"domain-replica x{ws}"},
+        "e2e": {"value": round(e2e * 1e6 / n, 4), "unit": UNIT, "ms_per_step": round(e2e, 2),
+                "h2d_bytes_per_step": pipe.h2d_bytes(), "d2h_bytes_per_step": pipe.d2h_bytes()},
+        "gpu_launches": int(launches),
+        "stages_ms": {k: round(v, 3) for k, v in stage.items()},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
+                     "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": None,
+                     "peak_kind": pk_kind,
+                     "note": "pass/build are FP32/FP64-pipe bound (SURVEY §8(d)); HBM frac is per the schema"},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_reference(args.cpu_sample, args.target, 1)
+            out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            out["cpu_baseline"]["stages_ms"] = cb["stages_ms"]
+        except Exception as e:  # the checker library is absent
+            out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                                   "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_init(args)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_b200(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

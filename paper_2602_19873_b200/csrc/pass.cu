@@ -171,6 +171,7 @@ __device__ __forceinline__ bool open_sc(const PassArgs& A, uint64_t sc, ScStream
 // number of entries (0 at the end), or -1 on a decode error (recorded).
 __device__ int next_block(const PassArgs& A, uint64_t sc, ScStream& s, uint32_t first,
                           uint32_t* idx, unsigned long long* msk, int* s_len) {
+    __syncthreads();  // every warp is done with the previous block's idx/msk
     if (threadIdx.x < 32) {
         const uint32_t len = tmin<uint32_t>(uint32_t(A.w), s.count - first);
         int result = int(len);
@@ -253,19 +254,33 @@ constexpr int nout() { return (K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COUL
 constexpr int kExactThreads = 64;
 
 template <int K>
+__device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& st, uint32_t* s_idx,
+                         unsigned long long* s_msk, int* s_len);
+
+template <int K>
 __global__ void __launch_bounds__(kExactThreads) k_pass_exact(PassArgs A) {
     __shared__ uint32_t s_idx[64];
     __shared__ unsigned long long s_msk[64];
     __shared__ int s_len;
-    constexpr int NO = nout<K>();
-    const uint32_t t = threadIdx.x;
     for (uint64_t sc = blockIdx.x; sc < A.num_sc; sc += gridDim.x) {
         ScStream st;
         if (!open_sc(A, sc, st)) continue;
+        sc_exact<K>(A, sc, st, s_idx, s_msk, &s_len);
+    }
+}
+
+// One SC of the fp64 reference-order pass; threads >= 64 only take part in the
+// block barriers (the fast kernel uses this for SCs it cannot handle safely).
+template <int K>
+__device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& st, uint32_t* s_idx,
+                         unsigned long long* s_msk, int* s_len) {
+    constexpr int NO = nout<K>();
+    const uint32_t t = threadIdx.x;
+    {
         const uint64_t i = sc * kSC + t;
         const uint32_t b = t / A.ci;
         const uint64_t gi = sc * A.icl_per_sc + b;
-        const bool active = i < A.n && gi < A.num_icl;
+        const bool active = t < kSC && i < A.n && gi < A.num_icl;
         double hi = 0, xi = 0, yi = 0, zi = 0;
         if (active) hi = A.h[i], xi = A.x[i], yi = A.y[i], zi = A.z[i];
         const double r = dmul(A.qs, hi);
@@ -273,7 +288,7 @@ __global__ void __launch_bounds__(kExactThreads) k_pass_exact(PassArgs A) {
         uint32_t cnt = 0;
         bool coincident = false;
         for (uint32_t first = 0; first < st.count; first += uint32_t(A.w)) {
-            const int len = next_block(A, sc, st, first, s_idx, s_msk, &s_len);
+            const int len = next_block(A, sc, st, first, s_idx, s_msk, s_len);
             if (len < 0) break;
             if (!active) continue;
             for (int e = 0; e < len; ++e) {
@@ -322,30 +337,83 @@ __global__ void __launch_bounds__(kExactThreads) k_pass_exact(PassArgs A) {
 constexpr int kFastThreads = 256;  // 8 warps = 8 i-clusters of 8
 constexpr float kFar = 1.0e30f;
 
+typedef unsigned long long f2;  // two packed fp32 lanes for the sm_100 FFMA2/FADD2/FMUL2 pipe
+__device__ __forceinline__ f2 f2p(float a, float b) {
+    f2 r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2u(f2 v, float& a, float& b) { asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
+__device__ __forceinline__ f2 f2add(f2 a, f2 b) {
+    f2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 f2sub(f2 a, f2 b) {
+    f2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 f2mul(f2 a, f2 b) {
+    f2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 f2fma(f2 a, f2 b, f2 c) {
+    f2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+// Rare slot: cutoff inside the guard band, or an LJ pair closer than 1.22 sigma
+// (force-zero crossing / overflow range): the exact reference predicate and fp64
+// kernel value, accumulated into the SC's shared fp64 side sums.
 template <int K>
-__global__ void __launch_bounds__(kFastThreads) k_pass_fast(PassArgs A) {
+__device__ __noinline__ int rare_slot(const PassArgs& A, uint64_t i, uint64_t j, double r2,
+                                      double* side) {
+    const double xi = A.x[i], yi = A.y[i], zi = A.z[i], hi = A.h[i];
+    double dx, dy, dz;
+    const double d2 = pair_d2_exact(xi, yi, zi, A.x[j], A.y[j], A.z[j], A.box, &dx, &dy, &dz);
+    if (d2 > r2) return 0;
+    double v[4];
+    if (eval_exact<K>(A, i, j, d2, dx, dy, dz, hi, v)) return -1;
+    constexpr int NO = nout<K>();
+#pragma unroll
+    for (int o = 0; o < NO; ++o) atomicAdd(side + o, v[o]);
+    return 1;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kFastThreads, 2) k_pass_fast(PassArgs A) {
+    constexpr bool LJ = (K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB);
+    constexpr int NO = nout<K>();
     __shared__ uint32_t s_idx[64];
     __shared__ unsigned long long s_msk[64];
     __shared__ float4 s_j[64 * 8];
-    __shared__ float s_emax[8];
+    __shared__ float4 s_jl[LJ ? 64 * 8 : 1];
+    __shared__ double s_side[kSC][NO];
+    __shared__ float s_red[8][4];
     __shared__ double s_o[3];
-    __shared__ int s_len;
-    constexpr int NO = nout<K>();
+    __shared__ int s_len, s_unsafe;
     const unsigned tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
     const uint32_t il = lane >> 2, jq = lane & 3;
     const uint32_t cj = A.cj;
+    const int i_local = int(warp * 8 + il);
+    const float sig2 = float(A.sigma * A.sigma);
+    const float eps24 = float(24.0 * A.eps), eps4 = float(4.0 * A.eps);
+    const float close2 = 1.5f * sig2;  // (1.22 sigma)^2: LJ pairs this close go to fp64
     for (uint64_t sc = blockIdx.x; sc < A.num_sc; sc += gridDim.x) {
         ScStream st;
         if (!open_sc(A, sc, st)) continue;
         const uint64_t p0 = sc * kSC;
         if (tid == 0) s_o[0] = A.x[p0], s_o[1] = A.y[p0], s_o[2] = A.z[p0];
+        for (uint32_t k = tid; k < kSC * NO; k += kFastThreads) (&s_side[0][0])[k] = 0.0;
         __syncthreads();
         const double ox = s_o[0], oy = s_o[1], oz = s_o[2];
-        const uint64_t i = p0 + warp * 8 + il;
+        const uint64_t i = p0 + uint64_t(i_local);
         const bool active = i < A.n;
-        double xi = 0, yi = 0, zi = 0, hi = 1;
-        if (active) xi = A.x[i], yi = A.y[i], zi = A.z[i], hi = A.h[i];
-        // SC-relative fp32 coordinates of i (same rounding path as the staged j)
+        double hi = 1.0;
+        double rx = 0, ry = 0, rz = 0;
         auto rel = [&](double v, double o, int d) {
             double r = dsub(v, o);
             if (A.box.per[d]) {
@@ -355,116 +423,194 @@ __global__ void __launch_bounds__(kFastThreads) k_pass_fast(PassArgs A) {
             }
             return r;
         };
-        const float fxi = float(rel(xi, ox, 0)), fyi = float(rel(yi, oy, 1)), fzi = float(rel(zi, oz, 2));
-        const float ei = active ? fmaxf(fabsf(fxi), fmaxf(fabsf(fyi), fabsf(fzi))) : 0.f;
+        if (active) {
+            hi = A.h[i];
+            rx = rel(A.x[i], ox, 0), ry = rel(A.y[i], oy, 1), rz = rel(A.z[i], oz, 2);
+        }
         const double r = dmul(A.qs, hi);
         const double r2 = dmul(r, r);
+        // Per-particle min-imaging against the SC origin is exact for every in-range
+        // pair when max|rel_i| + max r < L/2 on each periodic axis; otherwise this SC
+        // takes the exact path.
+        {
+            float ax = active ? float(fabs(rx)) : 0.f, ay = active ? float(fabs(ry)) : 0.f;
+            float az = active ? float(fabs(rz)) : 0.f, ar = active ? float(r) : 0.f;
+            for (int o = 16; o > 0; o >>= 1) {
+                ax = fmaxf(ax, __shfl_xor_sync(0xffffffffu, ax, o));
+                ay = fmaxf(ay, __shfl_xor_sync(0xffffffffu, ay, o));
+                az = fmaxf(az, __shfl_xor_sync(0xffffffffu, az, o));
+                ar = fmaxf(ar, __shfl_xor_sync(0xffffffffu, ar, o));
+            }
+            if (lane == 0) s_red[warp][0] = ax, s_red[warp][1] = ay, s_red[warp][2] = az, s_red[warp][3] = ar;
+            __syncthreads();
+            if (tid == 0) {
+                float m[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int w = 0; w < 8; ++w)
+                    for (int k = 0; k < 4; ++k) m[k] = fmaxf(m[k], s_red[w][k]);
+                int unsafe = 0;
+                for (int d = 0; d < 3; ++d)
+                    if (A.box.per[d] && double(m[d]) + double(m[3]) >= 0.49 * A.box.len[d]) unsafe = 1;
+                s_unsafe = unsafe;
+            }
+            __syncthreads();
+        }
+        if (s_unsafe) {
+            sc_exact<K>(A, sc, st, s_idx, s_msk, &s_len);
+            continue;
+        }
+        const float fxi = float(rx), fyi = float(ry), fzi = float(rz);
+        const float lxi = float(rx - double(fxi)), lyi = float(ry - double(fyi)), lzi = float(rz - double(fzi));
+        const f2 xi2 = f2p(fxi, fxi), yi2 = f2p(fyi, fyi), zi2 = f2p(fzi, fzi);
+        const f2 lxi2 = f2p(lxi, lxi), lyi2 = f2p(lyi, lyi), lzi2 = f2p(lzi, lzi);
+        const float ei = active ? fmaxf(fabsf(fxi), fmaxf(fabsf(fyi), fabsf(fzi))) : 0.f;
         const float inv_h = float(1.0 / hi);
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        double side[4] = {0.0, 0.0, 0.0, 0.0};
+        const f2 invh2 = f2p(inv_h, inv_h);
+        f2 acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;  // packed (slot a, slot b) partial sums
         uint32_t cnt = 0;
         bool coincident = false;
-        const float sig2 = float(A.sigma * A.sigma);
-        const float eps24 = float(24.0 * A.eps), eps4 = float(4.0 * A.eps);
         for (uint32_t first = 0; first < st.count; first += uint32_t(A.w)) {
             const int len = next_block(A, sc, st, first, s_idx, s_msk, &s_len);
             if (len < 0) break;
-            // stage the block's j particles (fp64 relative -> fp32)
+            // stage the block's j particles: fp64 relative -> fp32 (hi [+ lo for LJ])
             float emax = 0.f;
             for (uint32_t t = tid; t < uint32_t(len) * cj; t += kFastThreads) {
                 const uint32_t e = t / cj, jj = t - e * cj;
                 const uint64_t j = uint64_t(s_idx[e]) * cj + jj;
                 float4 v = make_float4(kFar, kFar, kFar, 0.f);
+                float4 vl = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (j < A.n) {
-                    v.x = float(rel(A.x[j], ox, 0));
-                    v.y = float(rel(A.y[j], oy, 1));
-                    v.z = float(rel(A.z[j], oz, 2));
+                    const double qx = rel(A.x[j], ox, 0), qy = rel(A.y[j], oy, 1), qz = rel(A.z[j], oz, 2);
+                    v.x = float(qx), v.y = float(qy), v.z = float(qz);
                     v.w = (K == SFCNL_KERNEL_DENSITY) ? float(A.m[j]) : 0.f;
+                    if (LJ) vl = make_float4(float(qx - double(v.x)), float(qy - double(v.y)), float(qz - double(v.z)), 0.f);
                     emax = fmaxf(emax, fmaxf(fabsf(v.x), fmaxf(fabsf(v.y), fabsf(v.z))));
                 }
                 s_j[e * 8 + jj] = v;
+                if (LJ) s_jl[e * 8 + jj] = vl;
             }
             for (int o = 16; o > 0; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-            if (lane == 0) s_emax[warp] = emax;
+            if (lane == 0) s_red[warp][0] = emax;
             __syncthreads();
             float E = ei;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) E = fmaxf(E, s_emax[k]);
+            for (int k = 0; k < 8; ++k) E = fmaxf(E, s_red[k][0]);
             // rounding-error guard band for d2 (see file header)
             const double ex = 1.1920928955078125e-07 * double(E) + 5.9604644775390625e-08 * r;
             const double guard = 4.0 * (1.7881393432617188e-07 * r2 + 3.5 * r * ex + 3.0 * ex * ex) + 1e-300;
-            const float lo = __double2float_rd(r2 - guard);
-            const float hi_t = __double2float_ru(r2 + guard);
-            if (active) {
-                for (int e = 0; e < len; ++e) {
-                    if (!((s_msk[e] >> warp) & 1ull)) continue;
-                    const uint64_t jbase = uint64_t(s_idx[e]) * cj;
-                    for (uint32_t jj = jq; jj < cj; jj += 4) {
-                        const float4 pj = s_j[e * 8 + jj];
-                        const float dx = fxi - pj.x, dy = fyi - pj.y, dz = fzi - pj.z;
-                        const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-                        if (d2 > hi_t) continue;
-                        const uint64_t j = jbase + jj;
-                        if (j == i) continue;
-                        bool exact = !(d2 < lo);
-                        if (K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB)
-                            exact = exact || d2 < 1e-4f * sig2;  // close pairs: fp64 (overflow / coincidence)
-                        if (exact) {
-                            double ddx, ddy, ddz;
-                            const double dd2 = pair_d2_exact(xi, yi, zi, A.x[j], A.y[j], A.z[j], A.box, &ddx, &ddy, &ddz);
-                            if (dd2 > r2) continue;
-                            double v[4];
-                            if (eval_exact<K>(A, i, j, dd2, ddx, ddy, ddz, hi, v)) {
-                                coincident = true;
-                                continue;
-                            }
-#pragma unroll
-                            for (int o = 0; o < NO; ++o) side[o] += v[o];
-                            ++cnt;
-                            continue;
-                        }
-                        ++cnt;
-                        if (K == SFCNL_KERNEL_DENSITY) {
-                            const float qv = sqrtf(d2) * inv_h;
-                            const float tq = fmaxf(1.f - qv, 0.f);
-                            const float w = qv <= 0.5f ? fmaf(6.f * qv * qv, qv - 1.f, 1.f) : 2.f * tq * tq * tq;
-                            acc[0] = fmaf(pj.w, w, acc[0]);
-                        } else if (K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB) {
-                            const float inv2 = __frcp_rn(d2);
-                            const float s2 = sig2 * inv2;
-                            const float s6 = s2 * s2 * s2;
-                            const float coef = eps24 * inv2 * s6 * fmaf(2.f, s6, -1.f);
-                            float en = eps4 * s6 * (s6 - 1.f);
-                            float cf = coef;
-                            if (K == SFCNL_KERNEL_LJ_COULOMB) {
-                                const float qq = float(A.ck * A.q[i] * A.q[j]);
-                                const float inv_r = rsqrtf(d2);
-                                en = fmaf(qq, inv_r, en);
-                                cf = fmaf(qq * inv_r, inv2, cf);
-                            }
-                            acc[0] = fmaf(cf, dx, acc[0]);
-                            acc[1] = fmaf(cf, dy, acc[1]);
-                            acc[2] = fmaf(cf, dz, acc[2]);
-                            acc[3] += en;
-                        }
+            const float lo = active ? __double2float_rd(r2 - guard) : -1.f;
+            const float hi_t = active ? __double2float_ru(r2 + guard) : -1.f;
+            // this warp's entries: bit `warp` of each entry mask
+            unsigned long long mine = 0;
+            {
+                const bool b0 = lane < uint32_t(len) && ((s_msk[lane] >> warp) & 1ull);
+                const bool b1 = lane + 32 < uint32_t(len) && ((s_msk[lane + 32] >> warp) & 1ull);
+                mine = (unsigned long long)__ballot_sync(0xffffffffu, b0) |
+                       ((unsigned long long)__ballot_sync(0xffffffffu, b1) << 32);
+            }
+            while (mine) {
+                const int e = __ffsll(mine) - 1;
+                mine &= mine - 1;
+                const int jl0 = int(int64_t(s_idx[e]) * cj - int64_t(p0));
+                // slots a = jq, b = jq + 4 (cj == 8); cj == 4 uses slot a only
+                const float4 pa = s_j[e * 8 + jq];
+                const float4 pb = cj == 8 ? s_j[e * 8 + jq + 4] : make_float4(kFar, kFar, kFar, 0.f);
+                f2 dx = f2sub(xi2, f2p(pa.x, pb.x));
+                f2 dy = f2sub(yi2, f2p(pa.y, pb.y));
+                f2 dz = f2sub(zi2, f2p(pa.z, pb.z));
+                if (LJ) {
+                    const float4 la = s_jl[e * 8 + jq];
+                    const float4 lb = cj == 8 ? s_jl[e * 8 + jq + 4] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    dx = f2add(dx, f2sub(lxi2, f2p(la.x, lb.x)));
+                    dy = f2add(dy, f2sub(lyi2, f2p(la.y, lb.y)));
+                    dz = f2add(dz, f2sub(lzi2, f2p(la.z, lb.z)));
+                }
+                const f2 d2p = f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx)));
+                float d2a, d2b;
+                f2u(d2p, d2a, d2b);
+                const bool self_a = jl0 + int(jq) == i_local, self_b = jl0 + int(jq) + 4 == i_local;
+                bool in_a = d2a < lo && !self_a, in_b = d2b < lo && !self_b;
+                bool rare_a = !in_a && !(d2a > hi_t) && !self_a;
+                bool rare_b = !in_b && !(d2b > hi_t) && !self_b;
+                if (LJ) {
+                    rare_a = rare_a || (in_a && d2a < close2);
+                    rare_b = rare_b || (in_b && d2b < close2);
+                    in_a = in_a && !(d2a < close2);
+                    in_b = in_b && !(d2b < close2);
+                }
+                if (rare_a | rare_b) {
+                    double* side = &s_side[i_local][0];
+                    const uint64_t jb = uint64_t(s_idx[e]) * cj;
+                    if (rare_a) {
+                        const int rc = rare_slot<K>(A, i, jb + jq, r2, side);
+                        cnt += rc > 0, coincident |= rc < 0;
+                    }
+                    if (rare_b) {
+                        const int rc = rare_slot<K>(A, i, jb + jq + 4, r2, side);
+                        cnt += rc > 0, coincident |= rc < 0;
                     }
                 }
+                cnt += uint32_t(in_a) + uint32_t(in_b);
+                const f2 ma = f2p(in_a ? 1.f : 0.f, in_b ? 1.f : 0.f);
+                if (K == SFCNL_KERNEL_DENSITY) {
+                    // W(q)/sigma_i: 1 + 6q^2(q-1) for q <= 1/2, 2(1-q)^3 otherwise
+                    float qa, qb;
+                    asm("sqrt.approx.f32 %0, %1;" : "=f"(qa) : "f"(d2a));
+                    asm("sqrt.approx.f32 %0, %1;" : "=f"(qb) : "f"(d2b));
+                    const f2 q = f2mul(f2p(qa, qb), invh2);
+                    const f2 q2 = f2mul(q, q);
+                    const f2 wa = f2fma(f2mul(f2p(6.f, 6.f), q2), f2sub(q, f2p(1.f, 1.f)), f2p(1.f, 1.f));
+                    float q0, q1;
+                    f2u(q, q0, q1);
+                    const f2 t = f2p(fmaxf(1.f - q0, 0.f), fmaxf(1.f - q1, 0.f));
+                    const f2 wb = f2mul(f2mul(f2p(2.f, 2.f), t), f2mul(t, t));
+                    float wa0, wa1, wb0, wb1;
+                    f2u(wa, wa0, wa1);
+                    f2u(wb, wb0, wb1);
+                    const f2 w = f2p(q0 <= 0.5f ? wa0 : wb0, q1 <= 0.5f ? wa1 : wb1);
+                    acc0 = f2fma(f2mul(f2p(pa.w, pb.w), ma), w, acc0);
+                } else if (LJ) {
+                    float ia, ib;
+                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ia) : "f"(d2a));
+                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ib) : "f"(d2b));
+                    const f2 inv2 = f2p(in_a ? ia : 0.f, in_b ? ib : 0.f);  // out/rare/self slots contribute 0
+                    const f2 s2 = f2mul(f2p(sig2, sig2), inv2);
+                    const f2 s6 = f2mul(f2mul(s2, s2), s2);
+                    const f2 coef = f2mul(f2mul(f2mul(f2p(eps24, eps24), inv2), s6),
+                                          f2fma(f2p(2.f, 2.f), s6, f2p(-1.f, -1.f)));
+                    const f2 en = f2mul(f2mul(f2p(eps4, eps4), s6), f2sub(s6, f2p(1.f, 1.f)));
+                    f2 cf = coef, ee = en;
+                    if (K == SFCNL_KERNEL_LJ_COULOMB) {
+                        const uint64_t jb = uint64_t(s_idx[e]) * cj;
+                        const float qi = float(A.ck * A.q[i]);
+                        const float qa = in_a ? qi * float(A.q[jb + jq]) : 0.f;
+                        const float qb = in_b && cj == 8 ? qi * float(A.q[jb + jq + 4]) : 0.f;
+                        float ra, rb;
+                        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(d2a));
+                        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rb) : "f"(d2b));
+                        const f2 qr = f2mul(f2p(qa, qb), f2p(ra, rb));
+                        ee = f2add(ee, qr);
+                        cf = f2fma(qr, inv2, cf);
+                    }
+                    acc0 = f2fma(cf, dx, acc0);
+                    acc1 = f2fma(cf, dy, acc1);
+                    acc2 = f2fma(cf, dz, acc2);
+                    acc3 = f2add(acc3, ee);
+                }
             }
-            __syncthreads();
         }
         if (coincident) raise_error(A.err, sc, SFCNL_INPUT_ERROR, kMsgCoincident, 0);
-        // combine the 4 j-quarter lanes of each i in fp64
+        __syncthreads();  // s_side complete
+        // combine: slot pair, then the 4 j-quarter lanes of each i, in fp64
         double tot[4];
+        const f2 accs[4] = {acc0, acc1, acc2, acc3};
 #pragma unroll
         for (int o = 0; o < 4; ++o) {
-            double v = double(acc[o]);
+            float a, b;
+            f2u(accs[o], a, b);
+            double v = double(a) + double(b);
             v += __shfl_xor_sync(0xffffffffu, v, 1);
             v += __shfl_xor_sync(0xffffffffu, v, 2);
             tot[o] = v;
-            double sv = side[o];
-            sv += __shfl_xor_sync(0xffffffffu, sv, 1);
-            sv += __shfl_xor_sync(0xffffffffu, sv, 2);
-            side[o] = sv;
         }
         uint32_t c = cnt;
         c += __shfl_xor_sync(0xffffffffu, c, 1);
@@ -472,12 +618,12 @@ __global__ void __launch_bounds__(kFastThreads) k_pass_fast(PassArgs A) {
         if (active && jq == 0) {
             if (K == SFCNL_KERNEL_DENSITY) {
                 const double sg = 8.0 / (kPi * hi * hi * hi);
-                A.out[0][i] = sg * tot[0] + side[0];
+                A.out[0][i] = sg * tot[0] + s_side[i_local][0];
             } else if (K == SFCNL_KERNEL_COUNT) {
                 A.out[0][i] = double(c);
             } else {
 #pragma unroll
-                for (int o = 0; o < 4; ++o) A.out[o][i] = tot[o] + side[o];
+                for (int o = 0; o < 4; ++o) A.out[o][i] = tot[o] + s_side[i_local][o < NO ? o : 0];
             }
             A.cnt[i] = c;
         }
