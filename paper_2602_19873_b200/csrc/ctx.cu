@@ -387,6 +387,7 @@ int sfcnl_cu_set_store(sfcnl_cu_ctx* c, const sfcnl_build_params* p, uint64_t n,
     c->num_sc = num_sc;
     c->blob_bytes = blob_bytes;
     c->has_store = true;
+    c->btab_valid = false;  // rebuilt on demand by the pass
     return finish(c);
 }
 

@@ -112,6 +112,8 @@ struct sfcnl_cu_ctx {
     sfcnl_build_params sp{};
     uint64_t store_n = 0, num_sc = 0, blob_bytes = 0;
     sfcnl_cu::DBuf counts, offsets, blob;
+    sfcnl_cu::DBuf btab;  // device-side codec block offsets per SC (u16 x 16), not part of the store
+    bool btab_valid = false;
     sfcnl_cu::DBuf sc_size, sc_scratch_off, scratch, build_ctl, overflow_list, fallback_ws;
 
     // (5) pass

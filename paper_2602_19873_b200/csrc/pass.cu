@@ -44,6 +44,7 @@ struct PassArgs {
     const uint32_t* counts;
     const uint64_t* offsets;
     const uint8_t* blob;
+    const uint16_t* btab;  // per-SC codec block offsets (device-side index, may be null)
     const double* x;
     const double* y;
     const double* z;
@@ -333,308 +334,46 @@ __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& 
     }
 }
 
-// ---------------------------------------------------------------- fast kernel
-constexpr int kFastThreads = 256;  // 8 warps = 8 i-clusters of 8
-constexpr float kFar = 1.0e30f;
+#include "pass_fast.cuh"
 
-typedef unsigned long long f2;  // two packed fp32 lanes for the sm_100 FFMA2/FADD2/FMUL2 pipe
-__device__ __forceinline__ f2 f2p(float a, float b) {
-    f2 r;
-    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ void f2u(f2 v, float& a, float& b) { asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
-__device__ __forceinline__ f2 f2add(f2 a, f2 b) {
-    f2 r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ f2 f2sub(f2 a, f2 b) {
-    f2 r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ f2 f2mul(f2 a, f2 b) {
-    f2 r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ f2 f2fma(f2 a, f2 b, f2 c) {
-    f2 r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-    return r;
-}
-
-// Rare slot: cutoff inside the guard band, or an LJ pair closer than 1.22 sigma
-// (force-zero crossing / overflow range): the exact reference predicate and fp64
-// kernel value, accumulated into the SC's shared fp64 side sums.
-template <int K>
-__device__ __noinline__ int rare_slot(const PassArgs& A, uint64_t i, uint64_t j, double r2,
-                                      double* side) {
-    const double xi = A.x[i], yi = A.y[i], zi = A.z[i], hi = A.h[i];
-    double dx, dy, dz;
-    const double d2 = pair_d2_exact(xi, yi, zi, A.x[j], A.y[j], A.z[j], A.box, &dx, &dy, &dz);
-    if (d2 > r2) return 0;
-    double v[4];
-    if (eval_exact<K>(A, i, j, d2, dx, dy, dz, hi, v)) return -1;
-    constexpr int NO = nout<K>();
-#pragma unroll
-    for (int o = 0; o < NO; ++o) atomicAdd(side + o, v[o]);
-    return 1;
-}
-
-template <int K>
-__global__ void __launch_bounds__(kFastThreads, 2) k_pass_fast(PassArgs A) {
-    constexpr bool LJ = (K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB);
-    constexpr int NO = nout<K>();
-    __shared__ uint32_t s_idx[64];
-    __shared__ unsigned long long s_msk[64];
-    __shared__ float4 s_j[64 * 8];
-    __shared__ float4 s_jl[LJ ? 64 * 8 : 1];
-    __shared__ double s_side[kSC][NO];
-    __shared__ float s_red[8][4];
-    __shared__ double s_o[3];
-    __shared__ int s_len, s_unsafe;
-    const unsigned tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
-    const uint32_t il = lane >> 2, jq = lane & 3;
-    const uint32_t cj = A.cj;
-    const int i_local = int(warp * 8 + il);
-    const float sig2 = float(A.sigma * A.sigma);
-    const float eps24 = float(24.0 * A.eps), eps4 = float(4.0 * A.eps);
-    const float close2 = 1.5f * sig2;  // (1.22 sigma)^2: LJ pairs this close go to fp64
-    for (uint64_t sc = blockIdx.x; sc < A.num_sc; sc += gridDim.x) {
-        ScStream st;
-        if (!open_sc(A, sc, st)) continue;
-        const uint64_t p0 = sc * kSC;
-        if (tid == 0) s_o[0] = A.x[p0], s_o[1] = A.y[p0], s_o[2] = A.z[p0];
-        for (uint32_t k = tid; k < kSC * NO; k += kFastThreads) (&s_side[0][0])[k] = 0.0;
-        __syncthreads();
-        const double ox = s_o[0], oy = s_o[1], oz = s_o[2];
-        const uint64_t i = p0 + uint64_t(i_local);
-        const bool active = i < A.n;
-        double hi = 1.0;
-        double rx = 0, ry = 0, rz = 0;
-        auto rel = [&](double v, double o, int d) {
-            double r = dsub(v, o);
-            if (A.box.per[d]) {
-                const double L = A.box.len[d];
-                if (r > 0.5 * L) r = dsub(r, L);
-                else if (r < -0.5 * L) r = dadd(r, L);
-            }
-            return r;
-        };
-        if (active) {
-            hi = A.h[i];
-            rx = rel(A.x[i], ox, 0), ry = rel(A.y[i], oy, 1), rz = rel(A.z[i], oz, 2);
-        }
-        const double r = dmul(A.qs, hi);
-        const double r2 = dmul(r, r);
-        // Per-particle min-imaging against the SC origin is exact for every in-range
-        // pair when max|rel_i| + max r < L/2 on each periodic axis; otherwise this SC
-        // takes the exact path.
-        {
-            float ax = active ? float(fabs(rx)) : 0.f, ay = active ? float(fabs(ry)) : 0.f;
-            float az = active ? float(fabs(rz)) : 0.f, ar = active ? float(r) : 0.f;
-            for (int o = 16; o > 0; o >>= 1) {
-                ax = fmaxf(ax, __shfl_xor_sync(0xffffffffu, ax, o));
-                ay = fmaxf(ay, __shfl_xor_sync(0xffffffffu, ay, o));
-                az = fmaxf(az, __shfl_xor_sync(0xffffffffu, az, o));
-                ar = fmaxf(ar, __shfl_xor_sync(0xffffffffu, ar, o));
-            }
-            if (lane == 0) s_red[warp][0] = ax, s_red[warp][1] = ay, s_red[warp][2] = az, s_red[warp][3] = ar;
-            __syncthreads();
-            if (tid == 0) {
-                float m[4] = {0.f, 0.f, 0.f, 0.f};
-                for (int w = 0; w < 8; ++w)
-                    for (int k = 0; k < 4; ++k) m[k] = fmaxf(m[k], s_red[w][k]);
-                int unsafe = 0;
-                for (int d = 0; d < 3; ++d)
-                    if (A.box.per[d] && double(m[d]) + double(m[3]) >= 0.49 * A.box.len[d]) unsafe = 1;
-                s_unsafe = unsafe;
-            }
-            __syncthreads();
-        }
-        if (s_unsafe) {
-            sc_exact<K>(A, sc, st, s_idx, s_msk, &s_len);
-            continue;
-        }
-        const float fxi = float(rx), fyi = float(ry), fzi = float(rz);
-        const float lxi = float(rx - double(fxi)), lyi = float(ry - double(fyi)), lzi = float(rz - double(fzi));
-        const f2 xi2 = f2p(fxi, fxi), yi2 = f2p(fyi, fyi), zi2 = f2p(fzi, fzi);
-        const f2 lxi2 = f2p(lxi, lxi), lyi2 = f2p(lyi, lyi), lzi2 = f2p(lzi, lzi);
-        const float ei = active ? fmaxf(fabsf(fxi), fmaxf(fabsf(fyi), fabsf(fzi))) : 0.f;
-        const float inv_h = float(1.0 / hi);
-        const f2 invh2 = f2p(inv_h, inv_h);
-        f2 acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;  // packed (slot a, slot b) partial sums
-        uint32_t cnt = 0;
-        bool coincident = false;
-        for (uint32_t first = 0; first < st.count; first += uint32_t(A.w)) {
-            const int len = next_block(A, sc, st, first, s_idx, s_msk, &s_len);
-            if (len < 0) break;
-            // stage the block's j particles: fp64 relative -> fp32 (hi [+ lo for LJ])
-            float emax = 0.f;
-            for (uint32_t t = tid; t < uint32_t(len) * cj; t += kFastThreads) {
-                const uint32_t e = t / cj, jj = t - e * cj;
-                const uint64_t j = uint64_t(s_idx[e]) * cj + jj;
-                float4 v = make_float4(kFar, kFar, kFar, 0.f);
-                float4 vl = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (j < A.n) {
-                    const double qx = rel(A.x[j], ox, 0), qy = rel(A.y[j], oy, 1), qz = rel(A.z[j], oz, 2);
-                    v.x = float(qx), v.y = float(qy), v.z = float(qz);
-                    v.w = (K == SFCNL_KERNEL_DENSITY) ? float(A.m[j]) : 0.f;
-                    if (LJ) vl = make_float4(float(qx - double(v.x)), float(qy - double(v.y)), float(qz - double(v.z)), 0.f);
-                    emax = fmaxf(emax, fmaxf(fabsf(v.x), fmaxf(fabsf(v.y), fabsf(v.z))));
-                }
-                s_j[e * 8 + jj] = v;
-                if (LJ) s_jl[e * 8 + jj] = vl;
-            }
-            for (int o = 16; o > 0; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-            if (lane == 0) s_red[warp][0] = emax;
-            __syncthreads();
-            float E = ei;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) E = fmaxf(E, s_red[k][0]);
-            // rounding-error guard band for d2 (see file header)
-            const double ex = 1.1920928955078125e-07 * double(E) + 5.9604644775390625e-08 * r;
-            const double guard = 4.0 * (1.7881393432617188e-07 * r2 + 3.5 * r * ex + 3.0 * ex * ex) + 1e-300;
-            const float lo = active ? __double2float_rd(r2 - guard) : -1.f;
-            const float hi_t = active ? __double2float_ru(r2 + guard) : -1.f;
-            // this warp's entries: bit `warp` of each entry mask
-            unsigned long long mine = 0;
-            {
-                const bool b0 = lane < uint32_t(len) && ((s_msk[lane] >> warp) & 1ull);
-                const bool b1 = lane + 32 < uint32_t(len) && ((s_msk[lane + 32] >> warp) & 1ull);
-                mine = (unsigned long long)__ballot_sync(0xffffffffu, b0) |
-                       ((unsigned long long)__ballot_sync(0xffffffffu, b1) << 32);
-            }
-            while (mine) {
-                const int e = __ffsll(mine) - 1;
-                mine &= mine - 1;
-                const int jl0 = int(int64_t(s_idx[e]) * cj - int64_t(p0));
-                // slots a = jq, b = jq + 4 (cj == 8); cj == 4 uses slot a only
-                const float4 pa = s_j[e * 8 + jq];
-                const float4 pb = cj == 8 ? s_j[e * 8 + jq + 4] : make_float4(kFar, kFar, kFar, 0.f);
-                f2 dx = f2sub(xi2, f2p(pa.x, pb.x));
-                f2 dy = f2sub(yi2, f2p(pa.y, pb.y));
-                f2 dz = f2sub(zi2, f2p(pa.z, pb.z));
-                if (LJ) {
-                    const float4 la = s_jl[e * 8 + jq];
-                    const float4 lb = cj == 8 ? s_jl[e * 8 + jq + 4] : make_float4(0.f, 0.f, 0.f, 0.f);
-                    dx = f2add(dx, f2sub(lxi2, f2p(la.x, lb.x)));
-                    dy = f2add(dy, f2sub(lyi2, f2p(la.y, lb.y)));
-                    dz = f2add(dz, f2sub(lzi2, f2p(la.z, lb.z)));
-                }
-                const f2 d2p = f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx)));
-                float d2a, d2b;
-                f2u(d2p, d2a, d2b);
-                const bool self_a = jl0 + int(jq) == i_local, self_b = jl0 + int(jq) + 4 == i_local;
-                bool in_a = d2a < lo && !self_a, in_b = d2b < lo && !self_b;
-                bool rare_a = !in_a && !(d2a > hi_t) && !self_a;
-                bool rare_b = !in_b && !(d2b > hi_t) && !self_b;
-                if (LJ) {
-                    rare_a = rare_a || (in_a && d2a < close2);
-                    rare_b = rare_b || (in_b && d2b < close2);
-                    in_a = in_a && !(d2a < close2);
-                    in_b = in_b && !(d2b < close2);
-                }
-                if (rare_a | rare_b) {
-                    double* side = &s_side[i_local][0];
-                    const uint64_t jb = uint64_t(s_idx[e]) * cj;
-                    if (rare_a) {
-                        const int rc = rare_slot<K>(A, i, jb + jq, r2, side);
-                        cnt += rc > 0, coincident |= rc < 0;
-                    }
-                    if (rare_b) {
-                        const int rc = rare_slot<K>(A, i, jb + jq + 4, r2, side);
-                        cnt += rc > 0, coincident |= rc < 0;
-                    }
-                }
-                cnt += uint32_t(in_a) + uint32_t(in_b);
-                const f2 ma = f2p(in_a ? 1.f : 0.f, in_b ? 1.f : 0.f);
-                if (K == SFCNL_KERNEL_DENSITY) {
-                    // W(q)/sigma_i: 1 + 6q^2(q-1) for q <= 1/2, 2(1-q)^3 otherwise
-                    float qa, qb;
-                    asm("sqrt.approx.f32 %0, %1;" : "=f"(qa) : "f"(d2a));
-                    asm("sqrt.approx.f32 %0, %1;" : "=f"(qb) : "f"(d2b));
-                    const f2 q = f2mul(f2p(qa, qb), invh2);
-                    const f2 q2 = f2mul(q, q);
-                    const f2 wa = f2fma(f2mul(f2p(6.f, 6.f), q2), f2sub(q, f2p(1.f, 1.f)), f2p(1.f, 1.f));
-                    float q0, q1;
-                    f2u(q, q0, q1);
-                    const f2 t = f2p(fmaxf(1.f - q0, 0.f), fmaxf(1.f - q1, 0.f));
-                    const f2 wb = f2mul(f2mul(f2p(2.f, 2.f), t), f2mul(t, t));
-                    float wa0, wa1, wb0, wb1;
-                    f2u(wa, wa0, wa1);
-                    f2u(wb, wb0, wb1);
-                    const f2 w = f2p(q0 <= 0.5f ? wa0 : wb0, q1 <= 0.5f ? wa1 : wb1);
-                    acc0 = f2fma(f2mul(f2p(pa.w, pb.w), ma), w, acc0);
-                } else if (LJ) {
-                    float ia, ib;
-                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ia) : "f"(d2a));
-                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ib) : "f"(d2b));
-                    const f2 inv2 = f2p(in_a ? ia : 0.f, in_b ? ib : 0.f);  // out/rare/self slots contribute 0
-                    const f2 s2 = f2mul(f2p(sig2, sig2), inv2);
-                    const f2 s6 = f2mul(f2mul(s2, s2), s2);
-                    const f2 coef = f2mul(f2mul(f2mul(f2p(eps24, eps24), inv2), s6),
-                                          f2fma(f2p(2.f, 2.f), s6, f2p(-1.f, -1.f)));
-                    const f2 en = f2mul(f2mul(f2p(eps4, eps4), s6), f2sub(s6, f2p(1.f, 1.f)));
-                    f2 cf = coef, ee = en;
-                    if (K == SFCNL_KERNEL_LJ_COULOMB) {
-                        const uint64_t jb = uint64_t(s_idx[e]) * cj;
-                        const float qi = float(A.ck * A.q[i]);
-                        const float qa = in_a ? qi * float(A.q[jb + jq]) : 0.f;
-                        const float qb = in_b && cj == 8 ? qi * float(A.q[jb + jq + 4]) : 0.f;
-                        float ra, rb;
-                        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(d2a));
-                        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rb) : "f"(d2b));
-                        const f2 qr = f2mul(f2p(qa, qb), f2p(ra, rb));
-                        ee = f2add(ee, qr);
-                        cf = f2fma(qr, inv2, cf);
-                    }
-                    acc0 = f2fma(cf, dx, acc0);
-                    acc1 = f2fma(cf, dy, acc1);
-                    acc2 = f2fma(cf, dz, acc2);
-                    acc3 = f2add(acc3, ee);
-                }
-            }
-        }
-        if (coincident) raise_error(A.err, sc, SFCNL_INPUT_ERROR, kMsgCoincident, 0);
-        __syncthreads();  // s_side complete
-        // combine: slot pair, then the 4 j-quarter lanes of each i, in fp64
-        double tot[4];
-        const f2 accs[4] = {acc0, acc1, acc2, acc3};
-#pragma unroll
-        for (int o = 0; o < 4; ++o) {
-            float a, b;
-            f2u(accs[o], a, b);
-            double v = double(a) + double(b);
-            v += __shfl_xor_sync(0xffffffffu, v, 1);
-            v += __shfl_xor_sync(0xffffffffu, v, 2);
-            tot[o] = v;
-        }
-        uint32_t c = cnt;
-        c += __shfl_xor_sync(0xffffffffu, c, 1);
-        c += __shfl_xor_sync(0xffffffffu, c, 2);
-        if (active && jq == 0) {
-            if (K == SFCNL_KERNEL_DENSITY) {
-                const double sg = 8.0 / (kPi * hi * hi * hi);
-                A.out[0][i] = sg * tot[0] + s_side[i_local][0];
-            } else if (K == SFCNL_KERNEL_COUNT) {
-                A.out[0][i] = double(c);
-            } else {
-#pragma unroll
-                for (int o = 0; o < 4; ++o) A.out[o][i] = tot[o] + s_side[i_local][o < NO ? o : 0];
-            }
-            A.cnt[i] = c;
-        }
+// Device-side block-offset index of an uploaded store: warp per SC walks the codec
+// block headers (first kBtab blocks) and records where each block starts.
+__global__ void k_block_table(PassArgs A, uint16_t* btab) {
+    __shared__ uint32_t scratch[8][64];
+    const uint64_t sc = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+    if (sc >= A.num_sc) return;
+    const uint32_t count = A.counts[sc];
+    if (!count) return;
+    const uint64_t begin = A.offsets[sc], end = A.offsets[sc + 1];
+    const uint64_t mb = uint64_t(count) * A.mask_bytes;
+    if (begin + mb > end) return;  // malformed: the pass reports it
+    const uint8_t* idata = A.blob + begin + mb;
+    const uint64_t ilen = end - begin - mb;
+    const uint32_t w = uint32_t(A.w);
+    uint64_t pos = 0, run = 0;
+    for (uint32_t b = 0; b * w < count && b < uint32_t(kBtab); ++b) {
+        if (lane_id() == 0) btab[sc * kBtab + b] = uint16_t(tmin<uint64_t>(pos, 0xffff));
+        uint64_t off;
+        int msg;
+        pos = warp_decode_block(idata, ilen, pos, tmin<uint32_t>(w, count - b * w), int(w), run,
+                                scratch[(threadIdx.x >> 5) & 7], &off, &msg);
+        if (pos == ~0ull) return;
     }
 }
 
 template <int K>
 void launch_pass(sfcnl_cu_ctx* c, const PassArgs& A, bool fast) {
     if (fast) {
-        const unsigned grid = unsigned(std::min<uint64_t>(A.num_sc, uint64_t(c->num_sms) * 8));
-        launch(c, k_pass_fast<K>, dim3(grid), dim3(kFastThreads), 0, A);
+        const unsigned grid = unsigned(std::min<uint64_t>(A.num_sc, uint64_t(c->num_sms) * 4));
+        if (A.cj == 8) {
+            const size_t smem = fast_smem<K, 8>();
+            cudaFuncSetAttribute(k_pass_fast<K, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            launch(c, k_pass_fast<K, 8>, dim3(grid), dim3(kFastThreads), smem, A);
+        } else {
+            const size_t smem = fast_smem<K, 4>();
+            cudaFuncSetAttribute(k_pass_fast<K, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            launch(c, k_pass_fast<K, 4>, dim3(grid), dim3(kFastThreads), smem, A);
+        }
     } else {
         const unsigned grid = unsigned(std::min<uint64_t>(A.num_sc, uint64_t(c->num_sms) * 32));
         launch(c, k_pass_exact<K>, dim3(grid), dim3(kExactThreads), 0, A);
@@ -680,6 +419,15 @@ int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p) {
     A.w = c->sp.w, A.compress = c->sp.compress, A.symmetric = symmetric;
     A.num_sc = c->num_sc, A.num_icl = (n + A.ci - 1) / A.ci;
     A.counts = c->counts.as<uint32_t>(), A.offsets = c->offsets.as<uint64_t>(), A.blob = c->blob.as<uint8_t>();
+    if (fast && A.compress) {
+        if (!c->btab_valid) {
+            SFCNL_CUDA_TRY(c->btab.reserve(c->num_sc * kBtab * 2));
+            launch(c, k_block_table, dim3(unsigned((c->num_sc * 32 + 255) / 256)), dim3(256), 0, A,
+                   c->btab.as<uint16_t>());
+            c->btab_valid = true;
+        }
+        A.btab = c->btab.as<uint16_t>();
+    }
     A.x = c->sorted.x.as<double>(), A.y = c->sorted.y.as<double>(), A.z = c->sorted.z.as<double>();
     A.h = c->sorted.h.as<double>();
     A.qs = p.query_scale, A.eps = p.epsilon, A.sigma = p.sigma, A.ck = p.coulomb_k;
