@@ -71,12 +71,8 @@ struct Workspace {
     unsigned long long* cmask;
     uint8_t* ebuf;
     uint32_t fcap, ccap, ecap;
-    float4* stage;    // [kCh * 8] staged j positions (fast masks); may alias fa/fb/ebuf
-    float* jab;       // [kCh * 6] staged j-cluster boxes
-    uint16_t* pairs;  // [kCh * 8] (candidate, i-cluster) pairs surviving the prefilter
+    bool fast;  // shared-memory workspace: the fast mask path may run
 };
-
-constexpr uint32_t kCh = 128;  // candidates per staging chunk
 
 __device__ __forceinline__ int nibble_count(uint64_t v) { return (64 - __clzll(v) + 3) / 4; }
 
@@ -119,192 +115,7 @@ __device__ __noinline__ bool exact_hit(const BuildArgs& A, double xi, double yi,
     return d2 <= dmul(rr, rr);
 }
 
-// Fast mask computation for gather stores with ci == 8 (cj in {4, 8}); returns false
-// (without touching cmask) for an SC that is not "safe" (see below), which then takes
-// the exact per-candidate loop.
-//
-// Coordinates are made relative to the SC's first particle in fp64, min-imaged per
-// particle and rounded to fp32. On periodic axes this is the true minimum image of
-// every in-range pair when max|rel_i| + scale*max h < L/2 ("safe"). Then:
-//  * an fp32 AABB gap between the i-cluster box and the staged j-cluster box that
-//    exceeds pre_r^2 + guard proves no pair of the two clusters is within r_i, so the
-//    bit is 0 whatever the reference's prefilter says;
-//  * a pair with d2_f32 < r2 - guard is within r_i in exact arithmetic, and then the
-//    reference prefilter (aabb_dist_sq <= pre_r^2, pre_r >= r_i) also passes: bit 1;
-//  * pairs inside the guard band are decided by the reference predicates in fp64.
-__device__ bool fast_masks(const BuildArgs& A, const Workspace& W, uint32_t nC, uint32_t nicl,
-                           uint64_t p0, uint32_t np, const double* s_x, const double* s_y,
-                           const double* s_z, const double* s_h, const Geo* s_igeo) {
-    __shared__ float s_ix[64], s_iy[64], s_iz[64], s_lo[64], s_hi[64];
-    __shared__ float s_iab[8][6];
-    __shared__ float s_pthr[8];
-    __shared__ float s_red[4][4];
-    __shared__ int s_unsafe;
-    __shared__ uint32_t s_npairs;
-    const unsigned tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
-    const unsigned nwarp = blockDim.x >> 5;
-    const double ox = s_x[0], oy = s_y[0], oz = s_z[0];
-    auto rel = [&](double v, double o, int d) {
-        double r = dsub(v, o);
-        if (A.box.per[d]) {
-            const double L = A.box.len[d];
-            if (r > 0.5 * L) r = dsub(r, L);
-            else if (r < -0.5 * L) r = dadd(r, L);
-        }
-        return r;
-    };
-    float ax = 0.f, ay = 0.f, az = 0.f, ar = 0.f;
-    for (uint32_t k = tid; k < 64; k += blockDim.x) {
-        float fx = 1e30f, fy = 1e30f, fz = 1e30f;
-        if (k < np) {
-            const double qx = rel(s_x[k], ox, 0), qy = rel(s_y[k], oy, 1), qz = rel(s_z[k], oz, 2);
-            fx = float(qx), fy = float(qy), fz = float(qz);
-            ax = fmaxf(ax, float(fabs(qx))), ay = fmaxf(ay, float(fabs(qy))), az = fmaxf(az, float(fabs(qz)));
-            ar = fmaxf(ar, float(dmul(A.scale, s_h[k])));
-        }
-        s_ix[k] = fx, s_iy[k] = fy, s_iz[k] = fz;
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        ax = fmaxf(ax, __shfl_xor_sync(0xffffffffu, ax, o));
-        ay = fmaxf(ay, __shfl_xor_sync(0xffffffffu, ay, o));
-        az = fmaxf(az, __shfl_xor_sync(0xffffffffu, az, o));
-        ar = fmaxf(ar, __shfl_xor_sync(0xffffffffu, ar, o));
-    }
-    if (lane == 0) s_red[warp][0] = ax, s_red[warp][1] = ay, s_red[warp][2] = az, s_red[warp][3] = ar;
-    __syncthreads();
-    if (tid == 0) {
-        float m[4] = {0.f, 0.f, 0.f, 0.f};
-        for (unsigned w = 0; w < nwarp; ++w)
-            for (int k = 0; k < 4; ++k) m[k] = fmaxf(m[k], s_red[w][k]);
-        int unsafe = 0;
-        for (int d = 0; d < 3; ++d)
-            if (A.box.per[d] && double(m[d]) + double(m[3]) >= 0.49 * A.box.len[d]) unsafe = 1;
-        s_unsafe = unsafe;
-        s_red[0][0] = fmaxf(m[0], fmaxf(m[1], m[2]));  // E_i
-    }
-    __syncthreads();
-    if (s_unsafe) return false;
-    const float Ei = s_red[0][0];
-    if (tid < nicl) {  // fp32 boxes of the i-clusters (relative frame)
-        float lo[3] = {1e30f, 1e30f, 1e30f}, hi[3] = {-1e30f, -1e30f, -1e30f};
-        for (uint32_t k = tid * 8; k < tmin<uint32_t>(tid * 8 + 8, np); ++k) {
-            lo[0] = fminf(lo[0], s_ix[k]), hi[0] = fmaxf(hi[0], s_ix[k]);
-            lo[1] = fminf(lo[1], s_iy[k]), hi[1] = fmaxf(hi[1], s_iy[k]);
-            lo[2] = fminf(lo[2], s_iz[k]), hi[2] = fmaxf(hi[2], s_iz[k]);
-        }
-        for (int d = 0; d < 3; ++d) s_iab[tid][d] = lo[d], s_iab[tid][3 + d] = hi[d];
-    }
-    for (uint32_t c = tid; c < nC; c += blockDim.x) W.cmask[c] = 0;
-    const uint32_t cj = A.cj;
-    for (uint32_t c0 = 0; c0 < nC; c0 += kCh) {
-        const uint32_t nc = tmin<uint32_t>(kCh, nC - c0);
-        __syncthreads();  // previous chunk's staging fully consumed
-        float emax = 0.f;
-        for (uint32_t t = tid; t < nc * cj; t += blockDim.x) {
-            const uint64_t j = uint64_t(W.cand[c0 + t / cj]) * cj + t % cj;
-            float4 v = make_float4(1e30f, 1e30f, 1e30f, 0.f);
-            if (j < A.n) {
-                v.x = float(rel(A.x[j], ox, 0)), v.y = float(rel(A.y[j], oy, 1)), v.z = float(rel(A.z[j], oz, 2));
-                emax = fmaxf(emax, fmaxf(fabsf(v.x), fmaxf(fabsf(v.y), fabsf(v.z))));
-            }
-            W.stage[t] = v;
-        }
-        for (int o = 16; o > 0; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-        if (lane == 0) s_red[warp][1] = emax;
-        if (tid == 0) s_npairs = 0;
-        __syncthreads();
-        float E = Ei;
-        for (unsigned w = 0; w < nwarp; ++w) E = fmaxf(E, s_red[w][1]);
-        for (uint32_t c = tid; c < nc; c += blockDim.x) {  // staged j-cluster boxes
-            float lo[3] = {1e30f, 1e30f, 1e30f}, hi[3] = {-1e30f, -1e30f, -1e30f};
-            for (uint32_t jj = 0; jj < cj; ++jj) {
-                const float4 v = W.stage[c * cj + jj];
-                if (v.x == 1e30f) continue;
-                lo[0] = fminf(lo[0], v.x), hi[0] = fmaxf(hi[0], v.x);
-                lo[1] = fminf(lo[1], v.y), hi[1] = fmaxf(hi[1], v.y);
-                lo[2] = fminf(lo[2], v.z), hi[2] = fmaxf(hi[2], v.z);
-            }
-            for (int d = 0; d < 3; ++d) W.jab[c * 6 + d] = lo[d], W.jab[c * 6 + 3 + d] = hi[d];
-        }
-        if (tid < 64) {  // per-i cutoff thresholds with the guard band
-            if (tid < np) {
-                const double r = dmul(A.scale, s_h[tid]);
-                const double r2 = dmul(r, r), g = d2_guard(r, r2, E);
-                s_lo[tid] = __double2float_rd(r2 - g);
-                s_hi[tid] = __double2float_ru(r2 + g);
-            } else {
-                s_lo[tid] = -1.f, s_hi[tid] = -1.f;
-            }
-        }
-        if (tid < nicl) {
-            const double pr = dmul(A.scale, s_igeo[tid].maxh);
-            const double pr2 = dmul(pr, pr);
-            s_pthr[tid] = __double2float_ru(pr2 + d2_guard(pr, pr2, E));
-        }
-        __syncthreads();
-        // conservative fp32 prefilter -> (candidate, i-cluster) pair list
-        for (uint32_t t0 = 0; t0 < nc * nicl; t0 += blockDim.x) {
-            const uint32_t t = t0 + tid;
-            bool keep = false;
-            uint32_t c = 0, b = 0;
-            if (t < nc * nicl) {
-                c = t / nicl, b = t % nicl;
-                float s = 0.f;
-#pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    const float g = fmaxf(fmaxf(s_iab[b][d], W.jab[c * 6 + d]) - fminf(s_iab[b][3 + d], W.jab[c * 6 + 3 + d]), 0.f);
-                    s = fmaf(g, g, s);
-                }
-                keep = !(s > s_pthr[b]);
-            }
-            const unsigned bal = __ballot_sync(0xffffffffu, keep);
-            uint32_t base = 0;
-            if (lane == 0 && bal) base = atomicAdd(&s_npairs, uint32_t(__popc(bal)));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (keep) W.pairs[base + __popc(bal & ((1u << lane) - 1u))] = uint16_t((c << 3) | b);
-        }
-        __syncthreads();
-        // warp per pair: lane = (i in cluster) x (j quarter), two slots per lane
-        const uint32_t il = lane >> 2, jq = lane & 3;
-        const uint32_t npairs = s_npairs;
-        for (uint32_t p = warp; p < npairs; p += nwarp) {
-            const uint32_t pc = W.pairs[p];
-            const uint32_t c = pc >> 3, b = pc & 7;
-            const uint32_t li = b * 8 + il;
-            const uint32_t jcl = W.cand[c0 + c];
-            const float4 pa = W.stage[c * cj + jq];
-            const float4 pb = cj == 8 ? W.stage[c * cj + jq + 4] : make_float4(1e30f, 1e30f, 1e30f, 0.f);
-            const f2 dx = f2sub(f2p(s_ix[li], s_ix[li]), f2p(pa.x, pb.x));
-            const f2 dy = f2sub(f2p(s_iy[li], s_iy[li]), f2p(pa.y, pb.y));
-            const f2 dz = f2sub(f2p(s_iz[li], s_iz[li]), f2p(pa.z, pb.z));
-            float d2a, d2b;
-            f2u(f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx))), d2a, d2b);
-            const int jl0 = int(int64_t(jcl) * cj - int64_t(p0));
-            const bool sa = jl0 + int(jq) == int(li), sb = cj != 8 || jl0 + int(jq) + 4 == int(li);
-            const float lo = s_lo[li], hi = s_hi[li];
-            const bool clear = (d2a < lo && !sa) || (d2b < lo && !sb);
-            bool hit = __any_sync(0xffffffffu, clear);
-            if (!hit) {
-                const bool band_a = !sa && !(d2a < lo) && !(d2a > hi);
-                const bool band_b = !sb && !(d2b < lo) && !(d2b > hi);
-                if (__any_sync(0xffffffffu, band_a || band_b)) {
-                    bool ex = false;
-                    const uint64_t jb = uint64_t(jcl) * cj;
-                    if (band_a) ex = exact_hit(A, s_x[li], s_y[li], s_z[li], s_h[li], jb + jq);
-                    if (band_b && !ex) ex = exact_hit(A, s_x[li], s_y[li], s_z[li], s_h[li], jb + jq + 4);
-                    if (__any_sync(0xffffffffu, ex)) {
-                        // the reference prefilter must pass too (neighbor_build.cpp:136-138)
-                        const double pr = dmul(A.scale, s_igeo[b].maxh);
-                        hit = !(aabb_dist_sq(s_igeo[b], A.jgeo[jcl], A.box) > dmul(pr, pr));
-                    }
-                }
-            }
-            if (hit && lane == 0) atomicOr(&W.cmask[c0 + c], 1ull << b);
-        }
-    }
-    __syncthreads();
-    return true;
-}
+#include "build_fast.cuh"
 
 // Returns false on capacity overflow (caller re-runs the SC in global-memory mode).
 __device__ bool build_sc(const BuildArgs& A, const Workspace& W, uint64_t sc) {
@@ -426,7 +237,7 @@ __device__ bool build_sc(const BuildArgs& A, const Workspace& W, uint64_t sc) {
     __syncthreads();
 
     // ---- interaction masks (neighbor_build.cpp:128-161)
-    const bool fast = W.stage && A.ci == 8 && (A.cj == 8 || A.cj == 4) && !A.symmetric &&
+    const bool fast = W.fast && A.ci == 8 && (A.cj == 8 || A.cj == 4) && !A.symmetric &&
                       fast_masks(A, W, nC, nicl, p0, np, s_x, s_y, s_z, s_h, s_igeo);
     for (uint32_t c = tid; c < nC && !fast; c += blockDim.x) {
         const uint32_t jcl = W.cand[c];
@@ -601,18 +412,14 @@ __device__ bool build_sc(const BuildArgs& A, const Workspace& W, uint64_t sc) {
     return true;
 }
 
-__global__ void __launch_bounds__(kBuildThreads) k_build_smem(BuildArgs A, uint64_t num_sc) {
-    // region0 is used in turn by the traversal frontier (fa|fb), the fast-mask
-    // staging buffer and the encoder's byte buffer.
-    static_assert(kCh * 8 * 16 >= 2 * kFCap * 4 && kCh * 8 * 16 >= kECap, "region0 size");
-    __shared__ __align__(16) float4 region0[kCh * 8];
+__global__ void __launch_bounds__(kBuildThreads, 5) k_build_smem(BuildArgs A, uint64_t num_sc) {
+    // region0 is used in turn by the traversal frontier (fa|fb) and the encoder's bytes.
+    static_assert(kECap <= 2 * kFCap * 4, "region0 size");
+    __shared__ __align__(16) uint32_t region0[2 * kFCap];
     __shared__ uint32_t cand[kCCap];
     __shared__ unsigned long long cmask[kCCap];
-    __shared__ float jab[kCh * 6];
-    __shared__ uint16_t pairs[kCh * 8];
-    uint32_t* fa = reinterpret_cast<uint32_t*>(region0);
-    const Workspace W{fa, fa + kFCap, cand, cmask, reinterpret_cast<uint8_t*>(region0), kFCap, kCCap, kECap,
-                      region0, jab, pairs};
+    const Workspace W{region0, region0 + kFCap, cand, cmask, reinterpret_cast<uint8_t*>(region0),
+                      kFCap, kCCap, kECap, true};
     for (uint64_t sc = blockIdx.x; sc < num_sc; sc += gridDim.x) {
         if (!build_sc(A, W, sc)) {
             if (threadIdx.x == 0) {
@@ -638,7 +445,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_global(BuildArgs A, con
         (reinterpret_cast<uintptr_t>(W.cand + ccap) + 15) & ~uintptr_t(15));
     W.ebuf = reinterpret_cast<uint8_t*>(W.cmask + ccap);
     W.fcap = fcap, W.ccap = ccap, W.ecap = ecap;
-    W.stage = nullptr, W.jab = nullptr, W.pairs = nullptr;  // exact mask loop
+    W.fast = false;  // exact mask loop
     for (uint64_t t = blockIdx.x; t < count; t += gridDim.x) {
         const uint64_t sc = list[t];
         if (!build_sc(A, W, sc)) {

@@ -335,6 +335,7 @@ __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& 
 }
 
 #include "pass_fast.cuh"
+#include "pass_ws.cuh"
 
 // Device-side block-offset index of an uploaded store: warp per SC walks the codec
 // block headers (first kBtab blocks) and records where each block starts.
@@ -364,15 +365,15 @@ __global__ void k_block_table(PassArgs A, uint16_t* btab) {
 template <int K>
 void launch_pass(sfcnl_cu_ctx* c, const PassArgs& A, bool fast) {
     if (fast) {
-        const unsigned grid = unsigned(std::min<uint64_t>(A.num_sc, uint64_t(c->num_sms) * 4));
+        const unsigned grid = unsigned(std::min<uint64_t>(A.num_sc, uint64_t(c->num_sms) * 2));
         if (A.cj == 8) {
-            const size_t smem = fast_smem<K, 8>();
-            cudaFuncSetAttribute(k_pass_fast<K, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            launch(c, k_pass_fast<K, 8>, dim3(grid), dim3(kFastThreads), smem, A);
+            const size_t smem = ws_smem<K, 8>();
+            cudaFuncSetAttribute(k_pass_ws<K, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            launch(c, k_pass_ws<K, 8>, dim3(grid), dim3(kWsThreads), smem, A);
         } else {
-            const size_t smem = fast_smem<K, 4>();
-            cudaFuncSetAttribute(k_pass_fast<K, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            launch(c, k_pass_fast<K, 4>, dim3(grid), dim3(kFastThreads), smem, A);
+            const size_t smem = ws_smem<K, 4>();
+            cudaFuncSetAttribute(k_pass_ws<K, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            launch(c, k_pass_ws<K, 4>, dim3(grid), dim3(kWsThreads), smem, A);
         }
     } else {
         const unsigned grid = unsigned(std::min<uint64_t>(A.num_sc, uint64_t(c->num_sms) * 32));

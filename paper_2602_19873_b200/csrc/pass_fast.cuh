@@ -62,6 +62,7 @@ __device__ __forceinline__ float rcp_ftz(float x) {
 template <int K>
 __device__ __noinline__ int rare_slot(const PassArgs& A, uint64_t i, uint64_t j, double r2,
                                       double* side) {
+    if (i == j) return 0;
     const double xi = A.x[i], yi = A.y[i], zi = A.z[i], hi = A.h[i];
     double dx, dy, dz;
     const double d2 = pair_d2_exact(xi, yi, zi, A.x[j], A.y[j], A.z[j], A.box, &dx, &dy, &dz);
@@ -154,13 +155,13 @@ __device__ bool decode_chunk(const PassArgs& A, uint64_t sc, const ScStream& st,
 }
 
 template <int K, int CJ>
-__global__ void __launch_bounds__(kFastThreads, 2) k_pass_fast(PassArgs A) {
+__global__ void __launch_bounds__(kFastThreads, 3) k_pass_fast(PassArgs A) {
     constexpr bool LJ = (K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB);
     constexpr int NO = nout<K>();
     extern __shared__ __align__(16) unsigned char dsm[];
     float4* s_j = reinterpret_cast<float4*>(dsm);                       // [kCap * CJ] hi + payload
-    float4* s_jl = s_j + kCap * CJ;                                      // [kCap * CJ] lo (LJ only)
-    uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_j + (LJ ? 2 : 1) * kCap * CJ);  // [kCap]
+    float4* s_jl = s_j + kCap * 8;                                       // [kCap * 8] lo (LJ only)
+    uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_j + (LJ ? 2 : 1) * kCap * 8);  // [kCap]
     uint8_t* s_msk = reinterpret_cast<uint8_t*>(s_idx + kCap);          // [kCap]
     __shared__ double s_side[kSC][NO];
     __shared__ float s_red[8][4];
@@ -247,22 +248,26 @@ __global__ void __launch_bounds__(kFastThreads, 2) k_pass_fast(PassArgs A) {
         for (uint32_t c0 = 0; c0 < st.count; c0 += kCap) {
             const uint32_t n = tmin<uint32_t>(kCap, st.count - c0);
             if (!decode_chunk(A, sc, st, c0, n, s_idx, s_msk, &s_seq_pos, &s_seq_run, &s_bad)) break;
-            // stage every j particle of the chunk: fp64 relative -> fp32 (hi [+ lo for LJ])
+            // stage every j particle of the chunk: fp64 relative -> fp32 (hi [+ lo for LJ]).
+            // Layout per (entry, j-quarter q): 8 floats {x_a, x_b, y_a, y_b, z_a, z_b, m_a, m_b}
+            // for slots a = q, b = q + 4, so a lane's two slots load as packed f32x2 pairs.
             float emax = 0.f;
-            for (uint32_t t = tid; t < n * CJ; t += kFastThreads) {
-                const uint32_t e = t / CJ, jj = t % CJ;
+            float* sj = reinterpret_cast<float*>(s_j);
+            float* sl = reinterpret_cast<float*>(s_jl);
+            for (uint32_t t = tid; t < n * 8; t += kFastThreads) {
+                const uint32_t e = t >> 3, jj = t & 7;
+                const uint32_t o = e * 32 + (jj & 3) * 8 + (jj >> 2);
+                float vx = kFar, vy = kFar, vz = kFar, vm = 0.f, lx = 0.f, ly = 0.f, lz = 0.f;
                 const uint64_t j = uint64_t(s_idx[e]) * CJ + jj;
-                float4 v = make_float4(kFar, kFar, kFar, 0.f);
-                float4 vl = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (j < A.n) {
+                if (jj < uint32_t(CJ) && j < A.n) {
                     const double qx = rel(A.x[j], ox, 0), qy = rel(A.y[j], oy, 1), qz = rel(A.z[j], oz, 2);
-                    v.x = float(qx), v.y = float(qy), v.z = float(qz);
-                    v.w = (K == SFCNL_KERNEL_DENSITY) ? float(A.m[j]) : 0.f;
-                    if (LJ) vl = make_float4(float(qx - double(v.x)), float(qy - double(v.y)), float(qz - double(v.z)), 0.f);
-                    emax = fmaxf(emax, fmaxf(fabsf(v.x), fmaxf(fabsf(v.y), fabsf(v.z))));
+                    vx = float(qx), vy = float(qy), vz = float(qz);
+                    vm = (K == SFCNL_KERNEL_DENSITY) ? float(A.m[j]) : 0.f;
+                    if (LJ) lx = float(qx - double(vx)), ly = float(qy - double(vy)), lz = float(qz - double(vz));
+                    emax = fmaxf(emax, fmaxf(fabsf(vx), fmaxf(fabsf(vy), fabsf(vz))));
                 }
-                s_j[t] = v;
-                if (LJ) s_jl[t] = vl;
+                sj[o] = vx, sj[o + 2] = vy, sj[o + 4] = vz, sj[o + 6] = vm;
+                if (LJ) sl[o] = lx, sl[o + 2] = ly, sl[o + 4] = lz;
             }
             for (int o = 16; o > 0; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
             if (lane == 0) s_red[warp][0] = emax;
@@ -281,24 +286,31 @@ __global__ void __launch_bounds__(kFastThreads, 2) k_pass_fast(PassArgs A) {
                 while (mine) {
                     const uint32_t e = g + __ffs(mine) - 1;
                     mine &= mine - 1;
-                    const int jl0 = int(int64_t(s_idx[e]) * CJ - int64_t(p0));
-                    // slots a = jq, b = jq + 4 (CJ == 8); CJ == 4 uses slot a only
-                    const float4 pa = s_j[e * CJ + jq];
-                    const float4 pb = CJ == 8 ? s_j[e * CJ + jq + 4] : make_float4(kFar, kFar, kFar, 0.f);
-                    f2 dx = f2sub(xi2, f2p(pa.x, pb.x));
-                    f2 dy = f2sub(yi2, f2p(pa.y, pb.y));
-                    f2 dz = f2sub(zi2, f2p(pa.z, pb.z));
+                    // slots a = jq, b = jq + 4 (CJ == 4: b is a far dummy), as f32x2 pairs
+                    const ulonglong2 P0 = reinterpret_cast<const ulonglong2*>(s_j)[e * 8 + jq * 2];
+                    const ulonglong2 P1 = reinterpret_cast<const ulonglong2*>(s_j)[e * 8 + jq * 2 + 1];
+                    f2 dx = f2sub(xi2, P0.x);
+                    f2 dy = f2sub(yi2, P0.y);
+                    f2 dz = f2sub(zi2, P1.x);
                     if (LJ) {
-                        const float4 la = s_jl[e * CJ + jq];
-                        const float4 lb = CJ == 8 ? s_jl[e * CJ + jq + 4] : make_float4(0.f, 0.f, 0.f, 0.f);
-                        dx = f2add(dx, f2sub(lxi2, f2p(la.x, lb.x)));
-                        dy = f2add(dy, f2sub(lyi2, f2p(la.y, lb.y)));
-                        dz = f2add(dz, f2sub(lzi2, f2p(la.z, lb.z)));
+                        const ulonglong2 L0 = reinterpret_cast<const ulonglong2*>(s_jl)[e * 8 + jq * 2];
+                        const ulonglong2 L1 = reinterpret_cast<const ulonglong2*>(s_jl)[e * 8 + jq * 2 + 1];
+                        dx = f2add(dx, f2sub(lxi2, L0.x));
+                        dy = f2add(dy, f2sub(lyi2, L0.y));
+                        dz = f2add(dz, f2sub(lzi2, L1.x));
                     }
+                    float pma, pmb;
+                    f2u(P1.y, pma, pmb);
                     const f2 d2p = f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx)));
                     float d2a, d2b;
                     f2u(d2p, d2a, d2b);
-                    const bool self_a = jl0 + int(jq) == i_local, self_b = CJ == 8 && jl0 + int(jq) + 4 == i_local;
+                    // i == j can only occur in the SC's own j-clusters (warp-uniform test)
+                    const int jl0 = int(s_idx[e]) * CJ - int(p0);
+                    bool self_a = false, self_b = false;
+                    if (jl0 >= -7 && jl0 < kSC) {
+                        self_a = jl0 + int(jq) == i_local;
+                        self_b = CJ == 8 && jl0 + int(jq) + 4 == i_local;
+                    }
                     bool in_a = d2a < lo && !self_a, in_b = d2b < lo && !self_b;
                     bool rare_a = !in_a && !(d2a > hi_t) && !self_a;
                     bool rare_b = !in_b && !(d2b > hi_t) && !self_b;
@@ -334,7 +346,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) k_pass_fast(PassArgs A) {
                         f2u(wa, wa0, wa1);
                         f2u(wb, wb0, wb1);
                         const f2 w = f2p(q0 <= 0.5f ? wa0 : wb0, q1 <= 0.5f ? wa1 : wb1);
-                        acc0 = f2fma(f2p(in_a ? pa.w : 0.f, in_b ? pb.w : 0.f), w, acc0);
+                        acc0 = f2fma(f2p(in_a ? pma : 0.f, in_b ? pmb : 0.f), w, acc0);
                     } else if (LJ) {
                         const f2 inv2 = f2p(in_a ? rcp_ftz(d2a) : 0.f, in_b ? rcp_ftz(d2b) : 0.f);  // out/rare/self -> 0
                         const f2 s2 = f2mul(f2p(sig2, sig2), inv2);
@@ -399,5 +411,5 @@ __global__ void __launch_bounds__(kFastThreads, 2) k_pass_fast(PassArgs A) {
 template <int K, int CJ>
 size_t fast_smem() {
     constexpr bool LJ = (K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB);
-    return size_t(kCap) * CJ * 16 * (LJ ? 2 : 1) + size_t(kCap) * 5;
+    return size_t(kCap) * 8 * 16 * (LJ ? 2 : 1) + size_t(kCap) * 5;
 }
