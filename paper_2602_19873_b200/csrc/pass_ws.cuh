@@ -15,7 +15,7 @@
 // for the fast path: the producer flags them and every slot of such an SC goes
 // through the exact fp64 reference predicate + kernel (rare_slot).
 
-constexpr int kWsConsumers = 256, kWsProducers = 64, kWsThreads = kWsConsumers + kWsProducers;
+constexpr int kWsConsumers = 256, kWsProducers = 128, kWsThreads = kWsConsumers + kWsProducers;
 constexpr int kWsCap = 128;  // entries per chunk (double-buffered)
 
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -50,10 +50,10 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_pass_ws(PassArgs A) {
     __shared__ WsMeta meta[2];
     __shared__ double s_side[kSC][NO];
     __shared__ uint32_t s_run[kBtab];
-    __shared__ float s_pred[2][4];
+    __shared__ float s_pred[kWsProducers / 32][4];
     __shared__ uint64_t s_seq_pos, s_seq_run;
     __shared__ int s_bad, s_unsafe_p;
-    __shared__ float s_ei_p, s_ax[2][3];
+    __shared__ float s_ei_p, s_ax[kWsProducers / 32][3];
     const unsigned tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
     const uint32_t w = uint32_t(A.w);
 
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_pass_ws(PassArgs A) {
                     const uint32_t nbt = (st.count + w - 1) / w;
                     const uint32_t b0 = c0 / w, b1 = (c0 + n + w - 1) / w;
                     if (nbt <= uint32_t(kBtab) && A.btab) {
-                        for (uint32_t b = b0 + pwarp; b < b1; b += 2) {
+                        for (uint32_t b = b0 + pwarp; b < b1; b += kWsProducers / 32) {
                             uint64_t off = 0, run = 0;
                             int msg = 0;
                             const uint64_t np2 = warp_decode_block(st.idata, st.ilen, A.btab[sc * kBtab + b],
@@ -199,17 +199,23 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_pass_ws(PassArgs A) {
                     M.bad = !ok || s_bad;
                     M.o[0] = ox, M.o[1] = oy, M.o[2] = oz;
                     if (ch == 0) {  // SC-wide: E_i and the periodic-image safety test
-                        const float er2 = fmaxf(s_pred[0][2], s_pred[1][2]);
+                        float er2 = 0.f, eim = 0.f, axm[3] = {0.f, 0.f, 0.f};
+                        for (int q = 0; q < kWsProducers / 32; ++q) {
+                            er2 = fmaxf(er2, s_pred[q][2]), eim = fmaxf(eim, s_pred[q][1]);
+                            for (int d = 0; d < 3; ++d) axm[d] = fmaxf(axm[d], s_ax[q][d]);
+                        }
                         int unsafe = 0;
                         for (int d = 0; d < 3; ++d)
                             if (A.box.per[d] &&
-                                double(fmaxf(s_ax[0][d], s_ax[1][d])) + double(er2) >= 0.49 * A.box.len[d])
+                                double(axm[d]) + double(er2) >= 0.49 * A.box.len[d])
                                 unsafe = 1;
-                        s_ei_p = fmaxf(s_pred[0][1], s_pred[1][1]);
+                        s_ei_p = eim;
                         s_unsafe_p = unsafe;
                     }
                     M.unsafe = s_unsafe_p;
-                    M.E = fmaxf(s_ei_p, fmaxf(s_pred[0][0], s_pred[1][0]));
+                    float em = 0.f;
+                    for (int q = 0; q < kWsProducers / 32; ++q) em = fmaxf(em, s_pred[q][0]);
+                    M.E = fmaxf(s_ei_p, em);
                 }
                 nbar_arrive(1 + buf, kWsThreads);  // FULL[buf]
                 buf ^= 1;
