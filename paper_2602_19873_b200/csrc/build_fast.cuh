@@ -25,7 +25,8 @@ __device__ bool fast_masks(const BuildArgs& A, const Workspace& W, uint32_t nC, 
     // for slots a = q, b = q + 4, so each lane loads its two slots as packed pairs
     __shared__ __align__(16) float s_st[kCh * 32];
     __shared__ float s_jab[kCh][6];
-    __shared__ uint16_t s_pairs[kCh * 8];
+    __shared__ unsigned s_pm[8][kCh / 32];  // prefilter survivors per i-cluster
+    __shared__ unsigned s_self[kCh / 32];
     __shared__ uint32_t s_cm[kCh];
     __shared__ uint32_t s_cand[kCh];
     __shared__ float s_ix[64], s_iy[64], s_iz[64], s_lo[64], s_hi[64];
@@ -140,13 +141,13 @@ __device__ bool fast_masks(const BuildArgs& A, const Workspace& W, uint32_t nC, 
             s_pthr[tid] = __double2float_ru(pr2 + d2_guard(pr, pr2, E));
         }
         __syncthreads();
-        // conservative fp32 prefilter -> (candidate, i-cluster) pair list
-        for (uint32_t t0 = 0; t0 < nc * nicl; t0 += blockDim.x) {
+        // conservative fp32 prefilter -> per i-cluster bitmask over the chunk's
+        // candidates (a warp covers 32 candidates of one i-cluster: one ballot)
+        for (uint32_t t0 = 0; t0 < 8 * kCh; t0 += blockDim.x) {
             const uint32_t t = t0 + tid;
+            const uint32_t b = t / kCh, c = t % kCh;
             bool keep = false;
-            uint32_t c = 0, b = 0;
-            if (t < nc * nicl) {
-                c = t / nicl, b = t - c * nicl;
+            if (b < nicl && c < nc) {
                 float s = 0.f;
 #pragma unroll
                 for (int d = 0; d < 3; ++d) {
@@ -156,48 +157,64 @@ __device__ bool fast_masks(const BuildArgs& A, const Workspace& W, uint32_t nC, 
                 keep = !(s > s_pthr[b]);
             }
             const unsigned bal = __ballot_sync(0xffffffffu, keep);
-            uint32_t base = 0;
-            if (lane == 0 && bal) base = atomicAdd(&s_npairs, uint32_t(__popc(bal)));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (keep) s_pairs[base + __popc(bal & ((1u << lane) - 1u))] = uint16_t((c << 3) | b);
+            if (lane == 0) s_pm[b][c >> 5] = bal;
+        }
+        // self candidates: j-clusters overlapping the SC's own particles (i == j possible)
+        if (tid < 2) {
+            unsigned m = 0;
+            for (uint32_t k = 0; k < 32; ++k) {
+                const uint32_t c = tid * 32 + k;
+                const int jl0 = c < nc ? int(s_cand[c]) * int(cj) - int(p0) : 1 << 20;
+                if (jl0 >= -7 && jl0 < kSC) m |= 1u << k;
+            }
+            s_self[tid] = m;
         }
         __syncthreads();
-        // warp per pair: lane = (i in cluster) x (j quarter), two slots per lane
-        const uint32_t npairs = s_npairs;
-        for (uint32_t p = warp; p < npairs; p += nwarp) {
-            const uint32_t pc = s_pairs[p];
-            const uint32_t c = pc >> 3, b = pc & 7;
+        // warp owns i-clusters b = warp, warp + nwarp, ...: its 8 particles stay in
+        // registers while it walks the candidates of its bitmask; lane = (i, j-quarter)
+        for (uint32_t b = warp; b < nicl; b += nwarp) {
             const uint32_t li = b * 8 + il;
-            const ulonglong2 P0 = reinterpret_cast<const ulonglong2*>(s_st)[c * 8 + jq * 2];
-            const f2 Pz = reinterpret_cast<const f2*>(s_st)[c * 16 + jq * 4 + 2];
             const float xi = s_ix[li], yi = s_iy[li], zi = s_iz[li];
-            const f2 dx = f2sub(f2p(xi, xi), P0.x);
-            const f2 dy = f2sub(f2p(yi, yi), P0.y);
-            const f2 dz = f2sub(f2p(zi, zi), Pz);
-            float d2a, d2b;
-            f2u(f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx))), d2a, d2b);
-            bool sa = false, sb = false;
-            const int jl0 = int(s_cand[c]) * int(cj) - int(p0);
-            if (jl0 >= -7 && jl0 < kSC) sa = jl0 + int(jq) == int(li), sb = jl0 + int(jq) + 4 == int(li);
+            const f2 xi2 = f2p(xi, xi), yi2 = f2p(yi, yi), zi2 = f2p(zi, zi);
             const float lo = s_lo[li], hi = s_hi[li];
-            const bool clear = (d2a < lo && !sa) || (d2b < lo && !sb);
-            bool hit = __any_sync(0xffffffffu, clear);
-            if (!hit) {
-                const bool band_a = !sa && !(d2a < lo) && !(d2a > hi);
-                const bool band_b = !sb && !(d2b < lo) && !(d2b > hi);
-                if (__any_sync(0xffffffffu, band_a || band_b)) {
-                    bool ex = false;
-                    const uint64_t jb = uint64_t(s_cand[c]) * cj;
-                    if (band_a) ex = exact_hit(A, s_x[li], s_y[li], s_z[li], s_h[li], jb + jq);
-                    if (band_b && !ex) ex = exact_hit(A, s_x[li], s_y[li], s_z[li], s_h[li], jb + jq + 4);
-                    if (__any_sync(0xffffffffu, ex)) {
-                        // the reference prefilter must pass too (neighbor_build.cpp:136-138)
-                        const double pr = dmul(A.scale, s_igeo[b].maxh);
-                        hit = !(aabb_dist_sq(s_igeo[b], A.jgeo[s_cand[c]], A.box) > dmul(pr, pr));
+            for (int half = 0; half < 2; ++half) {
+                unsigned todo = s_pm[b][half];
+                const unsigned self = s_self[half];
+                while (todo) {
+                    const uint32_t c = half * 32 + __ffs(todo) - 1;
+                    todo &= todo - 1;
+                    const ulonglong2 P0 = reinterpret_cast<const ulonglong2*>(s_st)[c * 8 + jq * 2];
+                    const f2 Pz = reinterpret_cast<const f2*>(s_st)[c * 16 + jq * 4 + 2];
+                    const f2 dx = f2sub(xi2, P0.x);
+                    const f2 dy = f2sub(yi2, P0.y);
+                    const f2 dz = f2sub(zi2, Pz);
+                    float d2a, d2b;
+                    f2u(f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx))), d2a, d2b);
+                    bool sa = false, sb = false;
+                    if ((self >> (c & 31)) & 1u) {
+                        const int jl0 = int(s_cand[c]) * int(cj) - int(p0);
+                        sa = jl0 + int(jq) == int(li), sb = jl0 + int(jq) + 4 == int(li);
                     }
+                    const bool clear = (d2a < lo && !sa) || (d2b < lo && !sb);
+                    bool hit = __any_sync(0xffffffffu, clear);
+                    if (!hit) {
+                        const bool band_a = !sa && !(d2a < lo) && !(d2a > hi);
+                        const bool band_b = !sb && !(d2b < lo) && !(d2b > hi);
+                        if (__any_sync(0xffffffffu, band_a || band_b)) {
+                            bool ex = false;
+                            const uint64_t jb = uint64_t(s_cand[c]) * cj;
+                            if (band_a) ex = exact_hit(A, s_x[li], s_y[li], s_z[li], s_h[li], jb + jq);
+                            if (band_b && !ex) ex = exact_hit(A, s_x[li], s_y[li], s_z[li], s_h[li], jb + jq + 4);
+                            if (__any_sync(0xffffffffu, ex)) {
+                                // the reference prefilter must pass too (neighbor_build.cpp:136-138)
+                                const double pr = dmul(A.scale, s_igeo[b].maxh);
+                                hit = !(aabb_dist_sq(s_igeo[b], A.jgeo[s_cand[c]], A.box) > dmul(pr, pr));
+                            }
+                        }
+                    }
+                    if (hit && lane == 0) atomicOr(&s_cm[c], 1u << b);
                 }
             }
-            if (hit && lane == 0) atomicOr(&s_cm[c], 1u << b);
         }
         __syncthreads();
         for (uint32_t c = tid; c < nc; c += blockDim.x) W.cmask[c0 + c] = s_cm[c];
