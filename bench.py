@@ -12,8 +12,13 @@ compressed; LJ sigma = 0.5 * N^-1/3 (bench.cpp:73-74); mixed-precision pass
 
   python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference] [--n N]
 
-Multi-GPU (torchrun): each rank owns its own 2^26-particle domain (weak scaling,
-no data-path collective); the step time is the max over ranks.
+Multi-GPU (torchrun, N > 1): SFC key-range domain decomposition
+(paper_2602_19873_b200/distributed.py). The global set is N x 2^26
+uniform particles in the periodic unit cube (h for 200 neighbours at the global
+density); every rank starts from its own 2^26 (spatially random) particles, and one
+step = exact distributed split + particle all-to-all + global octree + node-geometry
+all-reduce + halo exchange + range build + density + LJ on the rank's super-clusters
+(weak scaling; NCCL over NVLink). The step time is the max over ranks.
 """
 import argparse
 import json
@@ -54,7 +59,11 @@ def dist_init(args):
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("SFCNL_BENCH_BACKEND", "nccl")  # gloo: several ranks on one GPU (testing)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return ws, rank, local
 
 
@@ -63,7 +72,8 @@ def allreduce_max(x, ws):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -291,11 +301,102 @@ def run_b200(args, ws, rank, local):
         print(json.dumps(out), flush=True)
 
 
+def run_b200_distributed(args, ws, rank, local):
+    import torch
+    import paper_2602_19873_b200 as S
+    from paper_2602_19873_b200.distributed import Comm, CudaEngine, DomainDecomposition
+
+    n = args.n
+    ctx = S.Context(local)
+    # rank's share of a global uniform set of ws*n particles in the unit cube
+    ps, _ = S.make_uniform(S.UniformSpec(n=n, density=float(n), target_neighbors=args.target, seed=42 + rank))
+    ps.h[:] = S.uniform_h_for_target(args.target, float(n * ws))
+    box = S.SimulationBox((0.0, 0.0, 0.0), (1.0, 1.0, 1.0), (True, True, True))
+    pinned = {}
+    for name, v in (("x", ps.x), ("y", ps.y), ("z", ps.z), ("h", ps.h), ("m", ps.fields["m"])):
+        t = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        t.numpy()[:] = v
+        pinned[name] = t
+    pps = S.ParticleSet(pinned["x"].numpy(), pinned["y"].numpy(), pinned["z"].numpy(), pinned["h"].numpy(),
+                        {"m": pinned["m"].numpy()})
+    sigma = 0.5 * (1.0 / (n * ws)) ** (1.0 / 3.0)
+    kernels = [S.sph_density_kernel(), S.lj_kernel(1.0, sigma)]
+    bp = S.BuildParams(S.ClusterParams(8, 8, 32), S.GATHER, True, 1.0)
+    E = CudaEngine(ctx, box, ["m"])
+    E.upload(pps)
+    dd = DomainDecomposition(E, Comm(), bp, kernels, S.PassConfig(1.0, S.MIXED))
+    for _ in range(args.warmup):
+        res = dd.run(download=False)
+    ctx.synchronize()
+    barrier(ws)
+    launches0 = ctx.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(E.stream)
+        for _ in range(args.steps):
+            res = dd.run(download=False)
+        ev1.record(E.stream)
+        ev1.synchronize()
+    ctx.synchronize()
+    barrier(ws)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    launches = (ctx.launch_count() - launches0) // args.steps
+    ms_max = allreduce_max(ms, ws)
+    value_job = ms_max * 1e6 / (n * ws)
+    # end to end: pinned host inputs -> step -> store + outputs back to the host
+    e2e_ms, rr = [], None
+    for _ in range(args.e2e_steps):
+        ctx.synchronize()
+        barrier(ws)
+        t0 = time.perf_counter()
+        E.upload(pps)
+        rr = dd.run(download=True)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e = allreduce_max(float(np.median(e2e_ms)) if e2e_ms else float("nan"), ws)
+    nloc = res.p_end - res.p_begin
+    d2h = 0
+    if rr is not None:
+        d2h = rr.store.total_bytes() + sum(12 * nloc if len(k.names) == 1 else 36 * nloc for k in kernels)
+    halo = allreduce_max(float(res.halo_particles), ws)
+    # stage times of one instrumented step (build = dominant kernel), for the roofline
+    ctx.set_timing(True)
+    dd.run(download=False)
+    st = ctx.stage_times()
+    ctx.set_timing(False)
+    pk, pk_kind = peaks()
+    b_ms = st.get("build", float("nan"))
+    achieved = (32 + 8 + 3.77) * nloc / (b_ms * 1e-3) / 1e9 if b_ms > 0 else None
+    out = {
+        "metric": METRIC, "value": round(value_job, 4), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_max, 3), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "mixed f32/f64 (exact f64 cutoff decisions)",
+        "data": "synthetic (make_uniform per rank, seed 42+rank, global density)",
+        "config": {"workload": f"C2 weak-scaled: {ws} x 2^26 uniform periodic unit cube, 200 nbrs, "
+                               "ClusterParams(8,8,32) gather compressed, build + SPH density + LJ (mixed)",
+                   "n_per_gpu": n, "global_particles": n * ws, "l2": "inputs 2.7 GB/GPU > L2, no flush",
+                   "parallelism": f"sfc-domain x{ws} (NCCL all-to-all + halo)",
+                   "max_halo_particles_per_rank": int(halo)},
+        "e2e": {"value": round(e2e * 1e6 / (n * ws), 4) if e2e == e2e else None, "unit": UNIT,
+                "ms_per_step": round(e2e, 2), "h2d_bytes_per_step": 40 * n, "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "stages_ms_last_call": {k: round(v, 3) for k, v in st.items()},
+        "roofline": {"bound": "hbm", "kernel": "build", "achieved": round(achieved, 1) if achieved else None,
+                     "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": round(achieved / pk["hbm_gbs"], 4) if achieved else None, "traffic": None,
+                     "peak_kind": pk_kind},
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
 def main():
     args = parse()
     ws, rank, local = dist_init(args)
     if args.impl == "reference":
         run_reference(args, ws, rank)
+    elif ws > 1:
+        run_b200_distributed(args, ws, rank, local)
     else:
         run_b200(args, ws, rank, local)
     if ws > 1:

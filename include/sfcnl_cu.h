@@ -19,7 +19,9 @@
  * Memory model: a context owns one CUDA stream on one device and the device
  * copies of everything it computes. "set_*" calls copy host arrays in,
  * "get_*" calls copy results out; every call is synchronous at return unless
- * its comment says otherwise. All host pointers may be pageable or pinned.
+ * its comment says otherwise. All host pointers may be pageable or pinned; the
+ * array arguments of set_* / get_* may also be device pointers (copies use
+ * cudaMemcpyDefault), which keeps a multi-rank step device-resident.
  */
 #ifndef SFCNL_CU_H
 #define SFCNL_CU_H
@@ -167,6 +169,64 @@ int sfcnl_cu_set_store(sfcnl_cu_ctx* ctx, const sfcnl_build_params* params, uint
  * host arrays of n doubles (NULL = keep on device); count: n uint32 (nullable). */
 int sfcnl_cu_reduce(sfcnl_cu_ctx* ctx, const sfcnl_pass_params* params, double* const* outs,
                     uint32_t* neighbor_count);
+
+/* ---- (6) SFC domain decomposition -----------------------------
+ * The reference is single-process; these entry points let one process per GPU
+ * own a contiguous range of super-clusters of the GLOBAL sorted order while the
+ * store it builds is byte-identical to the corresponding slice of the
+ * single-domain store (neighbor_build.cpp:74-184 restricted to sc in
+ * [sc_begin, sc_end)). Particles outside the range but inside the halo must be
+ * present in the sorted slot at their global index.
+ *
+ * build_store_range: as build_store over super-clusters [sc_begin, sc_end)
+ * (clamped to the particle count). max_h > 0 overrides the local max(h) used by
+ * the traversal (pass the global all-reduced max so every rank prunes alike).
+ * The resulting store's counts/offsets/blob are local to the range; reduce then
+ * writes outputs for particles [64*sc_begin, min(n, 64*sc_end)) only. Gather
+ * mode only for ranges other than the whole set. */
+int sfcnl_cu_build_store_range(sfcnl_cu_ctx* ctx, const sfcnl_build_params* params, uint64_t sc_begin,
+                               uint64_t sc_end, double max_h, uint64_t* num_superclusters,
+                               uint64_t* blob_bytes);
+/* Allocate the sorted slot for n particles with the named extra fields (contents
+ * undefined) so ranks can fill it piecewise with write_sorted. Invalidates the
+ * store. */
+int sfcnl_cu_alloc_sorted(sfcnl_cu_ctx* ctx, uint64_t n, const sfcnl_box* box, const char* const* fields,
+                          int nfields);
+/* Copy count doubles into / out of sorted array `name` ("x","y","z","h" or a
+ * field) at element offset. *_on_device: the other pointer is device memory. */
+int sfcnl_cu_write_sorted(sfcnl_cu_ctx* ctx, const char* name, uint64_t offset, uint64_t count,
+                          const double* src, int src_on_device);
+int sfcnl_cu_read_sorted(sfcnl_cu_ctx* ctx, const char* name, uint64_t offset, uint64_t count, double* dst,
+                         int dst_on_device);
+/* Read a sub-range of the current SfcOrder (keys and/or perm, nullable). */
+int sfcnl_cu_read_order(sfcnl_cu_ctx* ctx, uint64_t offset, uint64_t count, uint64_t* keys, uint32_t* perm,
+                        int dst_on_device);
+/* Install globally sorted keys (e.g. all-gathered from the ranks) as the order
+ * build_octree consumes; perm is left undefined (apply_order must not follow). */
+int sfcnl_cu_set_keys(sfcnl_cu_ctx* ctx, uint64_t n, const uint64_t* keys, int src_on_device, int bits);
+/* apply_sfc_order (hilbert.cpp:28-44) into elements [offset, offset + n) of an
+ * allocated sorted slot (alloc_sorted) that holds every field of the input slot:
+ * a rank places its owned, locally sorted particles at their global positions. */
+int sfcnl_cu_apply_order_into(sfcnl_cu_ctx* ctx, uint64_t offset);
+/* compute_node_aabbs / compute_node_max_radius (octree.cpp:68-96) over particles
+ * [p_begin, p_end) only: every rank computes the partial geometry of the global
+ * octree from its own particles; an element-wise min (lo) / max (hi, maxh)
+ * all-reduce of the "node_geo" device array (8 doubles per node: lo[3], hi[3],
+ * maxh, pad) then yields the exact global geometry. Marks the array as
+ * caller-managed: halo_mark / build_store_range use it as is. */
+int sfcnl_cu_node_geometry_range(sfcnl_cu_ctx* ctx, uint64_t p_begin, uint64_t p_end);
+/* Flag (u8 per global j-cluster, device array "halo_flags") every j-cluster that
+ * build_store_range(sc_begin, sc_end) will read: the candidate clusters of
+ * collect_candidates (neighbor_build.cpp:43-65) for each super-cluster of the
+ * range. Needs positions/h of the range's own particles, the global octree and
+ * its (all-reduced) node geometry. A following build_store_range over the same
+ * range computes cluster geometry only for the range and the flagged halo. */
+int sfcnl_cu_halo_mark(sfcnl_cu_ctx* ctx, const sfcnl_build_params* params, uint64_t sc_begin,
+                       uint64_t sc_end, uint64_t* num_jclusters);
+/* Device pointer + byte length of an internal array for zero-copy collectives:
+ * "x","y","z","h", sorted fields by name, "keys","perm","nodes","node_geo",
+ * "halo_flags","out0".."out3","count". Valid until the next call that resizes it. */
+int sfcnl_cu_device_array(sfcnl_cu_ctx* ctx, const char* name, void** ptr, uint64_t* bytes);
 
 /* ---- host-side codec (no device work) ----------------------------------------
  * codec::encode / codec::decode_into (nibble_codec.hpp:54-60), used by the C++

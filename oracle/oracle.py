@@ -237,6 +237,74 @@ class Oracle:
         self._check(rc)
         return outs, cnt
 
+    # ---- domain-decomposition helpers (port only; SURVEY §8(e) parity checks)
+    def _store_from(self, h, n, ci, cj, w, mode, compress, scale):
+        try:
+            nsc, nb = C.c_uint64(), C.c_uint64()
+            self._f("store_info")(h, C.byref(nsc), C.byref(nb))
+            counts = np.empty(nsc.value, np.uint32)
+            offsets = np.empty(nsc.value + 1, np.uint64)
+            blob = np.empty(max(nb.value, 1), np.uint8)
+            self._f("store_copy")(h, _p(counts, U32), _p(offsets, U64), _p(blob, U8))
+            return Store(n, ci, cj, w, mode, compress, scale, counts, offsets, blob[: nb.value])
+        finally:
+            self._f("store_free")(h)
+
+    def node_geometry_range(self, tree: Tree, ps: Particles, p0, p1):
+        """Partial node geometry from particles [p0, p1): (lo (nn,3), hi (nn,3), maxh (nn,))."""
+        assert self.kind == "port"
+        nn = len(tree.pend)
+        lo, hi, mh = np.empty((nn, 3)), np.empty((nn, 3)), np.empty(nn)
+        self._check(self._f("node_geometry_range")(
+            U64(nn), _p(tree.pbegin, U32), _p(tree.pend, U32), _p(tree.first_child, I32), _p(ps.x, D),
+            _p(ps.y, D), _p(ps.z, D), _p(ps.h, D), U64(p0), U64(p1), _p(lo, D), _p(hi, D), _p(mh, D)))
+        return lo, hi, mh
+
+    def _range_common(self, ps, tree, geo):
+        lo, hi, mh = (np.ascontiguousarray(a, np.float64) for a in geo)
+        per = (C.c_int * 3)(*ps.periodic)
+        return (U64(ps.n), _p(ps.x, D), _p(ps.y, D), _p(ps.z, D), _p(ps.h, D), _p(ps.box6, D), per,
+                U64(len(tree.pend)), _p(tree.pbegin, U32), _p(tree.pend, U32), _p(tree.first_child, I32),
+                _p(lo, D), _p(hi, D), _p(mh, D)), (lo, hi, mh)
+
+    def halo_mark(self, ps: Particles, tree: Tree, geo, sc0, sc1, max_h, ci=8, cj=8, mode=0, scale=1.0):
+        assert self.kind == "port"
+        flags = np.zeros(max((ps.n + cj - 1) // cj, 1), np.uint8)
+        common, keep = self._range_common(ps, tree, geo)
+        self._check(self._f("halo_mark")(*common, U32(ci), U32(cj), C.c_int(mode), D(scale), U64(sc0),
+                                         U64(sc1), D(max_h), _p(flags, U8)))
+        return flags[: (ps.n + cj - 1) // cj]
+
+    def build_store_range(self, ps: Particles, tree: Tree, geo, sc0, sc1, max_h, ci=8, cj=8, w=32, mode=0,
+                          compress=1, scale=1.0) -> Store:
+        assert self.kind == "port"
+        h = C.c_void_p()
+        common, keep = self._range_common(ps, tree, geo)
+        self._check(self._f("build_store_range")(*common, U32(ci), U32(cj), C.c_int(w), C.c_int(mode),
+                                                 C.c_int(compress), D(scale), U64(sc0), U64(sc1), D(max_h),
+                                                 C.byref(h)))
+        return self._store_from(h, ps.n, ci, cj, w, mode, compress, scale)
+
+    def reduce_range(self, kernel, ps: Particles, store: Store, sc_base, query_scale=1.0, eps=1.0, sigma=1.0,
+                     ck=0.0):
+        """Gather-mode pass over a range store; outputs for particles [64*sc_base, ...)."""
+        assert self.kind == "port"
+        kid = KERNELS[kernel]
+        nout = 4 if kid >= 2 else 1
+        nsc = len(store.counts)
+        nloc = max(0, min(ps.n, 64 * (sc_base + nsc)) - 64 * sc_base)
+        outs = [np.zeros(max(nloc, 1)) for _ in range(nout)]
+        optr = (C.POINTER(C.c_double) * 4)(*[_p(o, D) for o in outs])
+        cnt = np.zeros(max(nloc, 1), np.uint32)
+        per = (C.c_int * 3)(*ps.periodic)
+        blob = store.blob if len(store.blob) else np.zeros(1, np.uint8)
+        self._check(self._f("reduce_range")(
+            C.c_int(kid), U64(ps.n), _p(ps.x, D), _p(ps.y, D), _p(ps.z, D), _p(ps.h, D), _p(ps.m, D),
+            _p(ps.q, D), _p(ps.box6, D), per, U32(store.ci), U32(store.cj), C.c_int(store.w),
+            C.c_int(store.compress), D(store.scale), U64(sc_base), U64(nsc), _p(store.counts, U32),
+            _p(store.offsets, U64), _p(blob, U8), D(query_scale), D(eps), D(sigma), D(ck), optr, _p(cnt, U32)))
+        return [o[:nloc] for o in outs], cnt[:nloc]
+
     # ---- codec
     def encode(self, idx, w=32):
         idx = np.ascontiguousarray(idx, np.uint32)

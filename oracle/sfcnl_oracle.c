@@ -405,6 +405,36 @@ int orc_node_geometry(const orc_tree* t, const double* x, const double* y, const
     return 0;
 }
 
+/* octree.cpp:68-96 restricted to particles [p0, p1) (a rank's partial geometry;
+ * element-wise min/max over ranks gives the global one). Arrays per node. */
+int orc_node_geometry_range(uint64_t num_nodes, const uint32_t* pbegin, const uint32_t* pend,
+                            const int32_t* first_child, const double* x, const double* y, const double* z,
+                            const double* h, uint64_t p0, uint64_t p1, double* lo, double* hi, double* maxh) {
+    for (uint64_t k = num_nodes; k-- > 0;) {
+        aabb_t b = aabb_empty();
+        double r = 0.0;
+        if (first_child[k] < 0) {
+            const uint64_t s0 = pbegin[k] > p0 ? pbegin[k] : p0, s1 = pend[k] < p1 ? pend[k] : p1;
+            for (uint64_t i = s0; i < s1; ++i) {
+                const double p[3] = {x[i], y[i], z[i]};
+                aabb_extend_pt(&b, p);
+                r = dmax(r, h[i]);
+            }
+        } else {
+            for (int c = 0; c < 8; ++c) {
+                const uint64_t ch = (uint64_t)(first_child[k] + c);
+                aabb_t cb;
+                for (int d = 0; d < 3; ++d) cb.lo[d] = lo[3 * ch + d], cb.hi[d] = hi[3 * ch + d];
+                aabb_extend(&b, &cb);
+                r = dmax(r, maxh[ch]);
+            }
+        }
+        for (int d = 0; d < 3; ++d) lo[3 * k + d] = b.lo[d], hi[3 * k + d] = b.hi[d];
+        maxh[k] = r;
+    }
+    return 0;
+}
+
 /* ---------------------------------------------------------------- predicates
  * core.hpp:77-85 periodic_delta, :132-135 interval_interval_gap, :152-165 aabb_dist_sq. */
 static double periodic_d2(const double a[3], const double b[3], const box_t* bx, double d[3]) {
@@ -586,13 +616,16 @@ static void u32push(u32vec* s, uint32_t v) {
     s->v[s->len++] = v;
 }
 
-int orc_build_store(uint64_t n, const double* x, const double* y, const double* z,
-                    const double* h, const double* box6, const int* per, int bits,
-                    uint64_t num_nodes, const uint64_t* key_first, const uint64_t* key_last,
-                    const uint32_t* pbegin, const uint32_t* pend, const int32_t* first_child,
-                    uint32_t ci, uint32_t cj, int w, int mode, int compress, double scale,
-                    orc_store** out) {
-    (void)bits, (void)key_first, (void)key_last;
+/* Shared body of orc_build_store (whole set) and the domain-decomposition helpers:
+ * super-clusters [sc0, sc1) only; node geometry from the caller when ext_lo is
+ * non-NULL; max_h_in > 0 replaces the set's max h in the periodic check; with
+ * jflags non-NULL only the candidate j-clusters are flagged (halo), no store. */
+static int build_impl(uint64_t n, const double* x, const double* y, const double* z, const double* h,
+                      const double* box6, const int* per, uint64_t num_nodes, const uint32_t* pbegin,
+                      const uint32_t* pend, const int32_t* first_child, const double* ext_lo,
+                      const double* ext_hi, const double* ext_maxh, uint32_t ci, uint32_t cj, int w,
+                      int mode, int compress, double scale, uint64_t sc0, uint64_t sc1, double max_h_in,
+                      uint8_t* jflags, orc_store** out) {
     /* ClusterParams (cluster.hpp:19-28), BuildParams (neighbor_store.hpp:25-28) */
     if (ci == 0 || cj == 0) return fail(1, "ClusterParams: cluster sizes must be positive", 0);
     if (64 % ci || 64 % cj) return fail(1, "ClusterParams: cluster sizes must divide the super-cluster size", 0);
@@ -600,8 +633,12 @@ int orc_build_store(uint64_t n, const double* x, const double* y, const double* 
     if (w != 32 && w != 64) return fail(1, "ClusterParams: block width must be 32 or 64", 0);
     if (!(scale >= 1.0)) return fail(1, "BuildParams: build_radius_scale must be >= 1", 0);
     const box_t bx = mkbox(box6, per);
-    /* validate (core.hpp:201-216) */
-    for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t total_sc = (n + 63) / 64;
+    if (sc1 > total_sc) sc1 = total_sc;
+    if (sc0 > sc1) return fail(1, "build_neighbor_store: bad super-cluster range", 0);
+    const uint64_t p_lo = sc0 * 64, p_hi = sc1 * 64 < n ? sc1 * 64 : n;
+    /* validate (core.hpp:201-216), over the range's own particles */
+    for (uint64_t i = p_lo; i < p_hi; ++i) {
         if (!(h[i] > 0)) return fail(1, "ParticleSet: h must be positive", 0);
         const double p[3] = {x[i], y[i], z[i]};
         for (int d = 0; d < 3; ++d) {
@@ -612,19 +649,20 @@ int orc_build_store(uint64_t n, const double* x, const double* y, const double* 
     if (num_nodes == 0 || pend[0] != (uint32_t)n) return fail(2, "build_neighbor_store: octree/particle-set mismatch", 0);
     const int symmetric = mode != 0;
     double max_h = 0;
-    for (uint64_t i = 0; i < n; ++i) max_h = dmax(max_h, h[i]);
+    for (uint64_t i = p_lo; i < p_hi; ++i) max_h = dmax(max_h, h[i]);
+    if (max_h_in > 0) max_h = max_h_in;
     for (int d = 0; d < 3; ++d)
         if (bx.per[d] && blen(&bx, d) < 2.0 * scale * max_h)
             return fail(2, "build_neighbor_store: periodic box must span twice the largest cutoff", 0);
 
-    const uint64_t num_sc = (n + 63) / 64, num_icl = (n + ci - 1) / ci, num_jcl = (n + cj - 1) / cj;
+    const uint64_t num_sc = sc1 - sc0, num_icl = (n + ci - 1) / ci, num_jcl = (n + cj - 1) / cj;
     const uint32_t icl_per_sc = 64 / ci, mask_bytes = (icl_per_sc + 7) / 8;
     struct orc_store* st = (struct orc_store*)calloc(1, sizeof(struct orc_store));
     st->num_sc = num_sc;
     st->counts = (uint32_t*)calloc(num_sc + 1, 4);
     st->offsets = (uint64_t*)calloc(num_sc + 1, 8);
     *out = st;
-    if (n == 0) return 0;
+    if (n == 0 || num_sc == 0) return 0;
 
     /* compute_cluster_geometry (neighbor_build.cpp:19-38) */
     aabb_t* iaabb = (aabb_t*)malloc(num_icl * sizeof(aabb_t));
@@ -657,7 +695,10 @@ int orc_build_store(uint64_t n, const double* x, const double* y, const double* 
     for (uint64_t k = num_nodes; k-- > 0;) {
         nbox[k] = aabb_empty();
         nmaxh[k] = 0;
-        if (first_child[k] < 0) {
+        if (ext_lo) {
+            for (int d = 0; d < 3; ++d) nbox[k].lo[d] = ext_lo[3 * k + d], nbox[k].hi[d] = ext_hi[3 * k + d];
+            nmaxh[k] = ext_maxh[k];
+        } else if (first_child[k] < 0) {
             for (uint32_t i = pbegin[k]; i < pend[k]; ++i) {
                 const double p[3] = {x[i], y[i], z[i]};
                 aabb_extend_pt(&nbox[k], p);
@@ -675,7 +716,7 @@ int orc_build_store(uint64_t n, const double* x, const double* y, const double* 
     uint64_t* masks = NULL;
     uint64_t mask_cap = 0;
     int32_t* stack = (int32_t*)malloc((num_nodes * 8 + 16) * 4);
-    for (uint64_t sc = 0; sc < num_sc; ++sc) {
+    for (uint64_t sc = sc0; sc < sc1; ++sc) {
         const uint64_t icl_base = sc * icl_per_sc;
         const uint64_t icl_end = icl_base + icl_per_sc < num_icl ? icl_base + icl_per_sc : num_icl;
         aabb_t sc_aabb = aabb_empty();
@@ -700,6 +741,10 @@ int orc_build_store(uint64_t n, const double* x, const double* y, const double* 
             } else {
                 for (int c = 7; c >= 0; --c) stack[sp++] = first_child[node] + c;
             }
+        }
+        if (jflags) {
+            for (uint64_t c = 0; c < cand.len; ++c) jflags[cand.v[c]] = 1;
+            continue;
         }
         /* mask loop (neighbor_build.cpp:128-161) */
         ent.len = 0;
@@ -740,8 +785,8 @@ int orc_build_store(uint64_t n, const double* x, const double* y, const double* 
             }
         }
         /* serialization (neighbor_build.cpp:164-182) */
-        st->counts[sc] = (uint32_t)ent.len;
-        st->offsets[sc] = st->blob.len;
+        st->counts[sc - sc0] = (uint32_t)ent.len;
+        st->offsets[sc - sc0] = st->blob.len;
         for (uint64_t e = 0; e < nmask; ++e)
             for (uint32_t b = 0; b < mask_bytes; ++b) bput(&st->blob, (uint8_t)((masks[e] >> (8 * b)) & 0xff));
         if (compress) {
@@ -756,6 +801,39 @@ int orc_build_store(uint64_t n, const double* x, const double* y, const double* 
     free(stack), free(masks), free(cand.v), free(ent.v);
     free(iaabb), free(jaabb), free(imaxh), free(jmaxh), free(nbox), free(nmaxh);
     return 0;
+}
+
+int orc_build_store(uint64_t n, const double* x, const double* y, const double* z,
+                    const double* h, const double* box6, const int* per, int bits,
+                    uint64_t num_nodes, const uint64_t* key_first, const uint64_t* key_last,
+                    const uint32_t* pbegin, const uint32_t* pend, const int32_t* first_child,
+                    uint32_t ci, uint32_t cj, int w, int mode, int compress, double scale,
+                    orc_store** out) {
+    (void)bits, (void)key_first, (void)key_last;
+    return build_impl(n, x, y, z, h, box6, per, num_nodes, pbegin, pend, first_child, NULL, NULL, NULL, ci,
+                      cj, w, mode, compress, scale, 0, (n + 63) / 64, 0.0, NULL, out);
+}
+
+int orc_build_store_range(uint64_t n, const double* x, const double* y, const double* z, const double* h,
+                          const double* box6, const int* per, uint64_t num_nodes, const uint32_t* pbegin,
+                          const uint32_t* pend, const int32_t* first_child, const double* node_lo,
+                          const double* node_hi, const double* node_maxh, uint32_t ci, uint32_t cj, int w,
+                          int mode, int compress, double scale, uint64_t sc0, uint64_t sc1, double max_h,
+                          orc_store** out) {
+    return build_impl(n, x, y, z, h, box6, per, num_nodes, pbegin, pend, first_child, node_lo, node_hi,
+                      node_maxh, ci, cj, w, mode, compress, scale, sc0, sc1, max_h, NULL, out);
+}
+
+int orc_halo_mark(uint64_t n, const double* x, const double* y, const double* z, const double* h,
+                  const double* box6, const int* per, uint64_t num_nodes, const uint32_t* pbegin,
+                  const uint32_t* pend, const int32_t* first_child, const double* node_lo,
+                  const double* node_hi, const double* node_maxh, uint32_t ci, uint32_t cj, int mode,
+                  double scale, uint64_t sc0, uint64_t sc1, double max_h, uint8_t* jflags) {
+    orc_store* st = NULL;
+    const int rc = build_impl(n, x, y, z, h, box6, per, num_nodes, pbegin, pend, first_child, node_lo, node_hi,
+                              node_maxh, ci, cj, 32, mode, 1, scale, sc0, sc1, max_h, jflags, &st);
+    orc_store_free(st);
+    return rc;
 }
 
 void orc_store_info(const orc_store* s, uint64_t* num_sc, uint64_t* blob_size) {
@@ -782,19 +860,31 @@ static double min_image(double d, double len) {
     return d;
 }
 
-int orc_reduce(int kernel, uint64_t n, const double* x, const double* y, const double* z,
-               const double* h, const double* m, const double* q, const double* box6,
-               const int* per, uint32_t ci, uint32_t cj, int w, int mode, int compress,
-               double scale, uint64_t num_sc, const uint32_t* counts, const uint64_t* offsets,
-               const uint8_t* blob, uint64_t blob_size, double query_scale, double eps,
-               double sigma, double ck, double** outs, uint32_t* ncount) {
-    (void)blob_size;
+/* sc_base: global index of the store's first super-cluster (range stores of a
+ * domain decomposition, gather mode); outs/ncount are indexed from particle
+ * 64 * sc_base. */
+static int reduce_impl(int kernel, uint64_t n, const double* x, const double* y, const double* z,
+                       const double* h, const double* m, const double* q, const double* box6,
+                       const int* per, uint32_t ci, uint32_t cj, int w, int mode, int compress,
+                       double scale, uint64_t sc_base, uint64_t num_sc, const uint32_t* counts,
+                       const uint64_t* offsets, const uint8_t* blob, double query_scale, double eps,
+                       double sigma, double ck, double** outs_g, uint32_t* ncount_g) {
     if (kernel < 0 || kernel > 3) return fail(1, "unknown kernel", 0);
     const int nout = (kernel >= 2) ? 4 : 1;
     if (query_scale > scale) return fail(1, "reduce: query_scale exceeds the store's build radius scale", 0);
-    for (int o = 0; o < nout; ++o) memset(outs[o], 0, n * 8);
-    memset(ncount, 0, n * 4);
-    if (n == 0) return 0;
+    if (mode != 0 && sc_base != 0) return fail(1, "reduce: symmetric stores cannot be restricted to a range", 0);
+    const uint64_t p_base = sc_base * 64;
+    const uint64_t p_end = (sc_base + num_sc) * 64 < n ? (sc_base + num_sc) * 64 : n;
+    const uint64_t nloc = p_end > p_base ? p_end - p_base : 0;
+    for (int o = 0; o < nout; ++o) memset(outs_g[o], 0, nloc * 8);
+    memset(ncount_g, 0, nloc * 4);
+    if (n == 0 || nloc == 0) return 0;
+    /* shift so that outs[o][i] addresses global particle i */
+    double* outs[4];
+    for (int o = 0; o < nout; ++o) outs[o] = outs_g[o] - p_base;
+    uint32_t* ncount = ncount_g - p_base;
+    counts -= sc_base;
+    offsets -= sc_base;
     const box_t bx = mkbox(box6, per);
     double blen3[3];
     for (int d = 0; d < 3; ++d) blen3[d] = bx.per[d] ? blen(&bx, d) : 0.0;
@@ -806,7 +896,7 @@ int orc_reduce(int kernel, uint64_t n, const double* x, const double* y, const d
     uint64_t idx_cap = 0;
     double* jacc = NULL;
     uint32_t* jcnt = NULL;
-    for (uint64_t sc = 0; sc < num_sc; ++sc) {
+    for (uint64_t sc = sc_base; sc < sc_base + num_sc; ++sc) {
         const uint32_t count = counts[sc];
         if (!count) continue;
         if (idx_cap < count) {
@@ -915,4 +1005,25 @@ int orc_reduce(int kernel, uint64_t n, const double* x, const double* y, const d
     }
     free(idx), free(jacc), free(jcnt);
     return 0;
+}
+
+int orc_reduce(int kernel, uint64_t n, const double* x, const double* y, const double* z,
+               const double* h, const double* m, const double* q, const double* box6,
+               const int* per, uint32_t ci, uint32_t cj, int w, int mode, int compress,
+               double scale, uint64_t num_sc, const uint32_t* counts, const uint64_t* offsets,
+               const uint8_t* blob, uint64_t blob_size, double query_scale, double eps,
+               double sigma, double ck, double** outs, uint32_t* ncount) {
+    (void)blob_size;
+    return reduce_impl(kernel, n, x, y, z, h, m, q, box6, per, ci, cj, w, mode, compress, scale, 0, num_sc,
+                       counts, offsets, blob, query_scale, eps, sigma, ck, outs, ncount);
+}
+
+int orc_reduce_range(int kernel, uint64_t n, const double* x, const double* y, const double* z,
+                     const double* h, const double* m, const double* q, const double* box6,
+                     const int* per, uint32_t ci, uint32_t cj, int w, int compress, double scale,
+                     uint64_t sc_base, uint64_t num_sc, const uint32_t* counts, const uint64_t* offsets,
+                     const uint8_t* blob, double query_scale, double eps, double sigma, double ck,
+                     double** outs, uint32_t* ncount) {
+    return reduce_impl(kernel, n, x, y, z, h, m, q, box6, per, ci, cj, w, 0, compress, scale, sc_base, num_sc,
+                       counts, offsets, blob, query_scale, eps, sigma, ck, outs, ncount);
 }

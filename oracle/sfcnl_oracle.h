@@ -67,6 +67,34 @@ int orc_reduce(int kernel, uint64_t n, const double* x, const double* y, const d
                const uint8_t* blob, uint64_t blob_size, double query_scale, double eps,
                double sigma, double ck, double** outs, uint32_t* ncount);
 
+/* ---- domain decomposition test helpers ----------------------
+ * Node geometry from particles [p0, p1) only (lo/hi 3 per node, maxh 1 per node). */
+int orc_node_geometry_range(uint64_t num_nodes, const uint32_t* pbegin, const uint32_t* pend,
+                            const int32_t* first_child, const double* x, const double* y, const double* z,
+                            const double* h, uint64_t p0, uint64_t p1, double* lo, double* hi, double* maxh);
+/* build_neighbor_store over super-clusters [sc0, sc1) with caller node geometry
+ * and global max h; the store's counts/offsets/blob are local to the range. */
+int orc_build_store_range(uint64_t n, const double* x, const double* y, const double* z, const double* h,
+                          const double* box6, const int* per, uint64_t num_nodes, const uint32_t* pbegin,
+                          const uint32_t* pend, const int32_t* first_child, const double* node_lo,
+                          const double* node_hi, const double* node_maxh, uint32_t ci, uint32_t cj, int w,
+                          int mode, int compress, double scale, uint64_t sc0, uint64_t sc1, double max_h,
+                          orc_store** out);
+/* Candidate j-clusters of super-clusters [sc0, sc1) (collect_candidates), as flags. */
+int orc_halo_mark(uint64_t n, const double* x, const double* y, const double* z, const double* h,
+                  const double* box6, const int* per, uint64_t num_nodes, const uint32_t* pbegin,
+                  const uint32_t* pend, const int32_t* first_child, const double* node_lo,
+                  const double* node_hi, const double* node_maxh, uint32_t ci, uint32_t cj, int mode,
+                  double scale, uint64_t sc0, uint64_t sc1, double max_h, uint8_t* jflags);
+/* gather-mode reduce over a range store starting at global super-cluster sc_base;
+ * outs/ncount hold the range's particles only. */
+int orc_reduce_range(int kernel, uint64_t n, const double* x, const double* y, const double* z,
+                     const double* h, const double* m, const double* q, const double* box6,
+                     const int* per, uint32_t ci, uint32_t cj, int w, int compress, double scale,
+                     uint64_t sc_base, uint64_t num_sc, const uint32_t* counts, const uint64_t* offsets,
+                     const uint8_t* blob, double query_scale, double eps, double sigma, double ck,
+                     double** outs, uint32_t* ncount);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,7 +78,9 @@ EXPORTS = [
     "sfcnl_cu_set_octree", "sfcnl_cu_node_geometry", "sfcnl_cu_build_store", "sfcnl_cu_get_store",
     "sfcnl_cu_set_store", "sfcnl_cu_reduce", "sfcnl_codec_encode", "sfcnl_codec_decode_into",
     "sfcnl_hilbert_encode", "sfcnl_hilbert_decode", "sfcnl_last_host_error", "sfcnl_make_uniform",
-    "sfcnl_make_evrard",
+    "sfcnl_make_evrard", "sfcnl_cu_build_store_range", "sfcnl_cu_alloc_sorted", "sfcnl_cu_write_sorted",
+    "sfcnl_cu_read_sorted", "sfcnl_cu_read_order", "sfcnl_cu_set_keys", "sfcnl_cu_apply_order_into",
+    "sfcnl_cu_node_geometry_range", "sfcnl_cu_halo_mark", "sfcnl_cu_device_array",
 ]
 
 _lib = None
@@ -128,6 +130,17 @@ def lib():
         "sfcnl_make_uniform": (C.c_int, [u64, C.c_double, C.c_double, C.POINTER(i32), C.c_double, u64,
                                          P, P, P, P, P, P, P]),
         "sfcnl_make_evrard": (C.c_int, [u64, C.c_double, i32, C.POINTER(i32), u64, P, P, P, P, P, P, P]),
+        "sfcnl_cu_build_store_range": (C.c_int, [P, C.POINTER(BuildParamsC), u64, u64, C.c_double,
+                                                 C.POINTER(u64), C.POINTER(u64)]),
+        "sfcnl_cu_alloc_sorted": (C.c_int, [P, u64, C.POINTER(Box), C.POINTER(C.c_char_p), C.c_int]),
+        "sfcnl_cu_write_sorted": (C.c_int, [P, C.c_char_p, u64, u64, P, C.c_int]),
+        "sfcnl_cu_read_sorted": (C.c_int, [P, C.c_char_p, u64, u64, P, C.c_int]),
+        "sfcnl_cu_read_order": (C.c_int, [P, u64, u64, P, P, C.c_int]),
+        "sfcnl_cu_set_keys": (C.c_int, [P, u64, P, C.c_int, C.c_int]),
+        "sfcnl_cu_apply_order_into": (C.c_int, [P, u64]),
+        "sfcnl_cu_node_geometry_range": (C.c_int, [P, u64, u64]),
+        "sfcnl_cu_halo_mark": (C.c_int, [P, C.POINTER(BuildParamsC), u64, u64, C.POINTER(u64)]),
+        "sfcnl_cu_device_array": (C.c_int, [P, C.c_char_p, C.POINTER(P), C.POINTER(u64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

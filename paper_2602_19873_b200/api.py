@@ -379,6 +379,61 @@ class Context:
         self.check(self.L.sfcnl_cu_reduce(self.h, C.byref(pp), arr, _ptr(cnt)))
         return ReduceResult(list(kernel.names), outs, cnt)
 
+    # domain decomposition (include/sfcnl_cu.h section (6)) ----------------
+    def set_particles_device(self, n, cols, names, box: SimulationBox):
+        """Orig slot from device arrays: cols = [x, y, z, h, *fields] (torch CUDA tensors)."""
+        b = box.c()
+        ptr = [int(c.data_ptr()) for c in cols]
+        self.check(self.L.sfcnl_cu_set_particles(self.h, int(n), *ptr[:4], C.byref(b)))
+        for name, p in zip(names, ptr[4:]):
+            self.check(self.L.sfcnl_cu_set_field(self.h, name.encode(), p))
+
+    def alloc_sorted(self, n, box: SimulationBox, fields):
+        b = box.c()
+        arr = (C.c_char_p * max(len(fields), 1))(*[f.encode() for f in fields])
+        self.check(self.L.sfcnl_cu_alloc_sorted(self.h, int(n), C.byref(b), arr, len(fields)))
+
+    def apply_order_into(self, offset):
+        self.check(self.L.sfcnl_cu_apply_order_into(self.h, int(offset)))
+
+    def set_keys_device(self, keys_tensor, bits=kDefaultSfcBits):
+        self.check(self.L.sfcnl_cu_set_keys(self.h, int(keys_tensor.numel()), int(keys_tensor.data_ptr()), 1,
+                                            int(bits)))
+
+    def node_geometry_range(self, p0, p1):
+        self.check(self.L.sfcnl_cu_node_geometry_range(self.h, int(p0), int(p1)))
+
+    def halo_mark(self, bp: BuildParams, sc0, sc1):
+        p = bp.c()
+        nj = C.c_uint64()
+        self.check(self.L.sfcnl_cu_halo_mark(self.h, C.byref(p), int(sc0), int(sc1), C.byref(nj)))
+        return nj.value
+
+    def build_store_range(self, bp: BuildParams, sc0, sc1, max_h=0.0):
+        nsc, nb = C.c_uint64(), C.c_uint64()
+        p = bp.c()
+        self.check(self.L.sfcnl_cu_build_store_range(self.h, C.byref(p), int(sc0), int(sc1), float(max_h),
+                                                     C.byref(nsc), C.byref(nb)))
+        return nsc.value, nb.value
+
+    def device_array(self, name, dtype, count=None):
+        """Zero-copy torch view of an internal device array (see sfcnl_cu_device_array)."""
+        import torch  # plumbing only: views for collectives
+        ptr, nbytes = C.c_void_p(), C.c_uint64()
+        self.check(self.L.sfcnl_cu_device_array(self.h, name.encode(), C.byref(ptr), C.byref(nbytes)))
+        item = torch.empty((), dtype=dtype).element_size()
+        n = nbytes.value // item if count is None else int(count)
+        if n * item > nbytes.value:
+            raise InputError(f"device_array {name}: {n} elements exceed {nbytes.value} bytes")
+        typestr = {torch.float64: "<f8", torch.int64: "<i8", torch.uint8: "|u1", torch.int32: "<i4",
+                   torch.uint32: "<u4", torch.float32: "<f4"}[dtype]
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr.value or 0, False),
+                                        "version": 3, "strides": None}
+
+        return torch.as_tensor(_View(), device=f"cuda:{self.device}")
+
     def stream(self):
         return self.L.sfcnl_cu_stream(self.h)
 

@@ -117,51 +117,19 @@ __device__ __noinline__ bool exact_hit(const BuildArgs& A, double xi, double yi,
 
 #include "build_fast.cuh"
 
-// Returns false on capacity overflow (caller re-runs the SC in global-memory mode).
-__device__ bool build_sc(const BuildArgs& A, const Workspace& W, uint64_t sc) {
-    __shared__ Geo s_igeo[64];
-    __shared__ double s_x[64], s_y[64], s_z[64], s_h[64];
-    __shared__ Geo s_sc;
-    __shared__ double s_r2;
-    __shared__ uint32_t scratch[33];
-    __shared__ int s_flag, s_over;
-    __shared__ uint32_t s_n[2];
+// Ordered-frontier BFS over the octree for one SC (collect_candidates,
+// neighbor_build.cpp:43-65). Leaves the accepted leaves (tagged, key order) in
+// *front and returns their number, or ~0u when the frontier exceeds W.fcap.
+__device__ __forceinline__ uint32_t sc_traverse(const BuildArgs& A, const Workspace& W, const Geo& scg,
+                                                double r2, uint32_t* scratch, int* s_flag, uint32_t** front) {
     const unsigned tid = threadIdx.x;
-    const uint64_t n = A.n;
-    const uint64_t icl_base = sc * A.icl_per_sc;
-    const uint64_t icl_end = tmin<uint64_t>(icl_base + A.icl_per_sc, A.num_icl);
-    const uint32_t nicl = uint32_t(icl_end - icl_base);
-    const uint64_t p0 = sc * kSC;
-    const uint32_t np = uint32_t(tmin<uint64_t>(p0 + kSC, n) - p0);
-    for (uint32_t b = tid; b < nicl; b += blockDim.x) s_igeo[b] = A.igeo[icl_base + b];
-    for (uint32_t k = tid; k < np; k += blockDim.x) {
-        s_x[k] = A.x[p0 + k], s_y[k] = A.y[p0 + k], s_z[k] = A.z[p0 + k], s_h[k] = A.h[p0 + k];
-    }
-    if (tid == 0) s_over = 0;
-    __syncthreads();
-    if (tid == 0) {
-        Geo g;
-        geo_init(g);
-        for (uint32_t b = 0; b < nicl; ++b) {
-            geo_extend(g, s_igeo[b]);
-            g.maxh = smax(g.maxh, s_igeo[b].maxh);
-        }
-        s_sc = g;
-        const double r = dmul(A.scale, g.maxh);
-        s_r2 = dmul(r, r);
-    }
-    __syncthreads();
-    const Geo scg = s_sc;
-    const double r2 = s_r2;
-
-    // ---- traversal (collect_candidates, neighbor_build.cpp:43-65)
     uint32_t* fa = W.fa;
     uint32_t* fb = W.fb;
     if (tid == 0) fa[0] = 0;
     uint32_t nA = 1;
     for (;;) {
         uint32_t nB = 0;
-        if (tid == 0) s_flag = 0;
+        if (tid == 0) *s_flag = 0;
         __syncthreads();
         for (uint32_t base = 0; base < nA; base += blockDim.x) {
             const uint32_t k = base + tid;
@@ -190,14 +158,13 @@ __device__ bool build_sc(const BuildArgs& A, const Workspace& W, uint64_t sc) {
             uint32_t tot;
             const uint32_t ex = block_excl_scan(emit, scratch, &tot);
             if (nB + tot > W.fcap) {
-                if (tid == 0) s_over = 1;
                 __syncthreads();
-                return false;
+                return ~0u;
             }
             if (emit == 1) fb[nB + ex] = (e & kTag) ? e : (e | kTag);
             if (emit == 8) {
                 for (int c = 0; c < 8; ++c) fb[nB + ex + c] = uint32_t(fc + c);
-                s_flag = 1;
+                *s_flag = 1;
             }
             nB += tot;
         }
@@ -205,9 +172,57 @@ __device__ bool build_sc(const BuildArgs& A, const Workspace& W, uint64_t sc) {
         uint32_t* t = fa;
         fa = fb, fb = t;
         nA = nB;
-        if (!s_flag) break;
+        if (!*s_flag) break;
         __syncthreads();
     }
+    *front = fa;
+    return nA;
+}
+
+// SC geometry = union of its i-clusters (neighbor_build.cpp:113-118); thread 0.
+__device__ __forceinline__ void sc_geometry(const BuildArgs& A, const Geo* s_igeo, uint32_t nicl, Geo* s_sc,
+                                            double* s_r2) {
+    Geo g;
+    geo_init(g);
+    for (uint32_t b = 0; b < nicl; ++b) {
+        geo_extend(g, s_igeo[b]);
+        g.maxh = smax(g.maxh, s_igeo[b].maxh);
+    }
+    *s_sc = g;
+    const double r = dmul(A.scale, g.maxh);
+    *s_r2 = dmul(r, r);
+}
+
+// Returns false on capacity overflow (caller re-runs the SC in global-memory mode).
+__device__ bool build_sc(const BuildArgs& A, const Workspace& W, uint64_t sc) {
+    __shared__ Geo s_igeo[64];
+    __shared__ double s_x[64], s_y[64], s_z[64], s_h[64];
+    __shared__ Geo s_sc;
+    __shared__ double s_r2;
+    __shared__ uint32_t scratch[33];
+    __shared__ int s_flag;
+    __shared__ uint32_t s_n[2];
+    const unsigned tid = threadIdx.x;
+    const uint64_t n = A.n;
+    const uint64_t icl_base = sc * A.icl_per_sc;
+    const uint64_t icl_end = tmin<uint64_t>(icl_base + A.icl_per_sc, A.num_icl);
+    const uint32_t nicl = uint32_t(icl_end - icl_base);
+    const uint64_t p0 = sc * kSC;
+    const uint32_t np = uint32_t(tmin<uint64_t>(p0 + kSC, n) - p0);
+    for (uint32_t b = tid; b < nicl; b += blockDim.x) s_igeo[b] = A.igeo[icl_base + b];
+    for (uint32_t k = tid; k < np; k += blockDim.x) {
+        s_x[k] = A.x[p0 + k], s_y[k] = A.y[p0 + k], s_z[k] = A.z[p0 + k], s_h[k] = A.h[p0 + k];
+    }
+    __syncthreads();
+    if (tid == 0) sc_geometry(A, s_igeo, nicl, &s_sc, &s_r2);
+    __syncthreads();
+    const Geo scg = s_sc;
+    const double r2 = s_r2;
+
+    // ---- traversal (collect_candidates, neighbor_build.cpp:43-65)
+    uint32_t* fa;
+    const uint32_t nA = sc_traverse(A, W, scg, r2, scratch, &s_flag, &fa);
+    if (nA == ~0u) return false;
 
     // ---- candidate j-clusters (union of accepted leaf ranges, in order)
     uint32_t nC = 0;
@@ -227,7 +242,6 @@ __device__ bool build_sc(const BuildArgs& A, const Workspace& W, uint64_t sc) {
         uint32_t tot;
         const uint32_t ex = block_excl_scan(cnt, scratch, &tot);
         if (nC + tot > W.ccap) {
-            if (tid == 0) s_over = 1;
             __syncthreads();
             return false;
         }
@@ -290,7 +304,6 @@ __device__ bool build_sc(const BuildArgs& A, const Workspace& W, uint64_t sc) {
     // ---- serialization (neighbor_build.cpp:164-182)
     const uint32_t mbytes = nE * A.mask_bytes;
     if (mbytes + 4 > W.ecap) {
-        if (tid == 0) s_over = 1;
         __syncthreads();
         return false;
     }
@@ -300,7 +313,6 @@ __device__ bool build_sc(const BuildArgs& A, const Workspace& W, uint64_t sc) {
     if (!A.compress) {
         size = mbytes + 4 * nE;
         if (size > W.ecap) {
-            if (tid == 0) s_over = 1;
             __syncthreads();
             return false;
         }
@@ -379,7 +391,6 @@ __device__ bool build_sc(const BuildArgs& A, const Workspace& W, uint64_t sc) {
     __syncthreads();
     if (A.compress) {
         if (s_n[1]) {
-            if (tid == 0) s_over = 1;
             __syncthreads();
             return false;
         }
@@ -412,7 +423,7 @@ __device__ bool build_sc(const BuildArgs& A, const Workspace& W, uint64_t sc) {
     return true;
 }
 
-__global__ void __launch_bounds__(kBuildThreads, 5) k_build_smem(BuildArgs A, uint64_t num_sc) {
+__global__ void __launch_bounds__(kBuildThreads, 5) k_build_smem(BuildArgs A, uint64_t sc_begin, uint64_t sc_end) {
     // region0 is used in turn by the traversal frontier (fa|fb) and the encoder's bytes.
     static_assert(kECap <= 2 * kFCap * 4, "region0 size");
     __shared__ __align__(16) uint32_t region0[2 * kFCap];
@@ -420,7 +431,7 @@ __global__ void __launch_bounds__(kBuildThreads, 5) k_build_smem(BuildArgs A, ui
     __shared__ unsigned long long cmask[kCCap];
     const Workspace W{region0, region0 + kFCap, cand, cmask, reinterpret_cast<uint8_t*>(region0),
                       kFCap, kCCap, kECap, true};
-    for (uint64_t sc = blockIdx.x; sc < num_sc; sc += gridDim.x) {
+    for (uint64_t sc = sc_begin + blockIdx.x; sc < sc_end; sc += gridDim.x) {
         if (!build_sc(A, W, sc)) {
             if (threadIdx.x == 0) {
                 const unsigned long long slot = atomicAdd(&A.ctl[1], 1ull);
@@ -453,6 +464,55 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_global(BuildArgs A, con
             __syncthreads();
         }
     }
+}
+
+// ---- halo marking (domain decomposition) -------------------------
+// The particles a rank's build and pass read outside its own range are exactly the
+// candidate j-clusters of its SCs (accepted leaves' cluster ranges). One CTA per SC
+// runs the build's traversal and flags those clusters.
+__device__ bool halo_sc(const BuildArgs& A, const Workspace& W, uint64_t sc, uint8_t* jflags) {
+    __shared__ Geo s_igeo[64];
+    __shared__ Geo s_sc;
+    __shared__ double s_r2;
+    __shared__ uint32_t scratch[33];
+    __shared__ int s_flag;
+    const unsigned tid = threadIdx.x;
+    const uint64_t icl_base = sc * A.icl_per_sc;
+    const uint64_t icl_end = tmin<uint64_t>(icl_base + A.icl_per_sc, A.num_icl);
+    const uint32_t nicl = uint32_t(icl_end - icl_base);
+    for (uint32_t b = tid; b < nicl; b += blockDim.x) s_igeo[b] = A.igeo[icl_base + b];
+    __syncthreads();
+    if (tid == 0) sc_geometry(A, s_igeo, nicl, &s_sc, &s_r2);
+    __syncthreads();
+    uint32_t* fa;
+    const uint32_t nA = sc_traverse(A, W, s_sc, s_r2, scratch, &s_flag, &fa);
+    if (nA == ~0u) return false;
+    for (uint32_t k = tid; k < nA; k += blockDim.x) {
+        const Node nd = A.nodes[fa[k] & ~kTag];
+        for (uint32_t j = nd.pbegin / A.cj; j <= (nd.pend - 1) / A.cj; ++j) jflags[j] = 1;
+    }
+    __syncthreads();
+    return true;
+}
+
+__global__ void __launch_bounds__(kBuildThreads) k_halo_smem(BuildArgs A, uint64_t sc_begin, uint64_t sc_end,
+                                                             uint8_t* jflags) {
+    __shared__ uint32_t front[2 * kFCap];
+    const Workspace W{front, front + kFCap, nullptr, nullptr, nullptr, kFCap, 0, 0, false};
+    for (uint64_t sc = sc_begin + blockIdx.x; sc < sc_end; sc += gridDim.x) {
+        if (!halo_sc(A, W, sc, jflags) && threadIdx.x == 0) {
+            const unsigned long long slot = atomicAdd(&A.ctl[1], 1ull);
+            A.overflow_list[slot] = uint32_t(sc);
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kBuildThreads) k_halo_global(BuildArgs A, const uint32_t* list, uint64_t count,
+                                                               uint32_t* ws, uint32_t fcap, uint8_t* jflags) {
+    uint32_t* base = ws + uint64_t(blockIdx.x) * 2 * fcap;
+    const Workspace W{base, base + fcap, nullptr, nullptr, nullptr, fcap, 0, 0, false};
+    for (uint64_t t = blockIdx.x; t < count; t += gridDim.x) halo_sc(A, W, list[t], jflags);
 }
 
 __global__ void k_compact(uint64_t num_sc, const uint32_t* __restrict__ sizes,
@@ -497,7 +557,7 @@ __global__ void k_validate(uint64_t n, const double* __restrict__ x, const doubl
 
 }  // namespace
 
-int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p) {
+int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, uint64_t sc1, double max_h_in) {
     // ClusterParams / BuildParams validation (cluster.hpp:19-28, neighbor_store.hpp:25-28)
     if (p.ci == 0 || p.cj == 0) return set_error(c, 1, "ClusterParams: cluster sizes must be positive");
     if (64 % p.ci || 64 % p.cj)
@@ -508,15 +568,22 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p) {
     if (!c->sorted.valid) return set_error(c, 1, "build_neighbor_store: no particles");
     const uint64_t n = c->sorted.n;
     const Box& box = c->sorted.box;
+    // super-cluster range [sc0, sc1) of the sorted slot (the whole set by default;
+    // a rank of a domain decomposition builds its own range over global arrays)
+    const uint64_t total_sc = (n + 63) / 64;
+    if (sc1 > total_sc) sc1 = total_sc;
+    if (sc0 > sc1) return set_error(c, 1, "build_neighbor_store: bad super-cluster range");
+    const uint64_t p_lo = sc0 * 64, p_hi = tmin<uint64_t>(sc1 * 64, n);
 
     SFCNL_CUDA_TRY(c->build_ctl.reserve(8 * 8));
     SFCNL_CUDA_TRY(cudaMemsetAsync(c->build_ctl.p, 0, 8 * 8, c->stream));
     SFCNL_CUDA_TRY(cudaMemsetAsync(c->derr.p, 0xff, sizeof(DevError), c->stream));
-    if (n) {
-        const int grid = int(std::min<uint64_t>((n + 255) / 256, uint64_t(c->num_sms) * 8));
-        launch(c, k_validate, dim3(grid), dim3(256), 0, n, c->sorted.x.as<const double>(),
-               c->sorted.y.as<const double>(), c->sorted.z.as<const double>(),
-               c->sorted.h.as<const double>(), box, c->build_ctl.as<unsigned long long>() + 3,
+    if (p_hi > p_lo) {
+        const uint64_t m = p_hi - p_lo;
+        const int grid = int(std::min<uint64_t>((m + 255) / 256, uint64_t(c->num_sms) * 8));
+        launch(c, k_validate, dim3(grid), dim3(256), 0, m, c->sorted.x.as<const double>() + p_lo,
+               c->sorted.y.as<const double>() + p_lo, c->sorted.z.as<const double>() + p_lo,
+               c->sorted.h.as<const double>() + p_lo, box, c->build_ctl.as<unsigned long long>() + 3,
                c->derr.as<DevError>());
     }
     static const char* const kValMsgs[] = {"", "ParticleSet: h must be positive",
@@ -529,35 +596,43 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p) {
     if (!c->has_tree || c->tree_n != n)
         return set_error(c, 2, "build_neighbor_store: octree/particle-set mismatch");
     unsigned long long maxh_bits = 0;
-    SFCNL_CUDA_TRY(cudaMemcpy(&maxh_bits, c->build_ctl.as<unsigned long long>() + 3, 8, cudaMemcpyDeviceToHost));
+    SFCNL_CUDA_TRY(cudaMemcpyAsync(&maxh_bits, c->build_ctl.as<unsigned long long>() + 3, 8, cudaMemcpyDeviceToHost, c->stream));
+    SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
     double max_h;
     memcpy(&max_h, &maxh_bits, 8);
+    if (max_h_in > 0) max_h = max_h_in;  // global max h supplied by the caller (domain decomposition)
     for (int d = 0; d < 3; ++d)
         if (box.per[d] && box.len[d] < 2.0 * p.build_radius_scale * max_h)
             return set_error(c, 2, "build_neighbor_store: periodic box must span twice the largest cutoff");
 
-    const uint64_t num_sc = (n + 63) / 64;
+    const uint64_t num_sc = sc1 - sc0;
+    c->sc_base = sc0;
     c->sp = p;
     c->store_n = n;
     c->num_sc = num_sc;
     c->has_store = false;
     SFCNL_CUDA_TRY(c->counts.reserve(std::max<uint64_t>(num_sc, 1) * 4));
     SFCNL_CUDA_TRY(c->offsets.reserve((num_sc + 1) * 8));
-    if (n == 0) {
+    if (num_sc == 0) {
         SFCNL_CUDA_TRY(cudaMemsetAsync(c->offsets.p, 0, 8, c->stream));
         c->blob_bytes = 0;
         c->has_store = true;
         return 0;
     }
     {
-        int rc = run_cluster_geometry(c, p.ci, p.cj);
-        if (!rc) rc = run_node_geometry(c);
+        // geometry of the clusters this range reads: all of them, or (domain
+        // decomposition) the range plus the halo flagged by run_halo_mark
+        const bool whole = sc0 == 0 && sc1 == total_sc;
+        const bool halo = !whole && c->jflags_valid && c->jflags_sc0 == sc0 && c->jflags_sc1 == sc1;
+        int rc = halo ? run_cluster_geometry(c, p.ci, p.cj, p_lo, p_hi, c->jflags.as<uint8_t>())
+                      : run_cluster_geometry(c, p.ci, p.cj);
+        if (!rc && !c->node_geo_external) rc = run_node_geometry(c);
         if (rc) return rc;
     }
     SFCNL_CUDA_TRY(c->sc_size.reserve(num_sc * 4));
     SFCNL_CUDA_TRY(c->sc_scratch_off.reserve(num_sc * 8));
     SFCNL_CUDA_TRY(c->overflow_list.reserve(num_sc * 4));
-    uint64_t scratch_cap = std::max<uint64_t>(c->scratch.bytes, n * 16 + (1 << 20));
+    uint64_t scratch_cap = std::max<uint64_t>(c->scratch.bytes, (p_hi - p_lo) * 16 + (1 << 20));
 
     BuildArgs A;
     A.n = n;
@@ -572,16 +647,17 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p) {
     A.ngeo = c->node_geo.as<Geo>();
     A.igeo = c->igeo.as<Geo>();
     A.jgeo = p.cj == p.ci ? c->igeo.as<Geo>() : c->jgeo.as<Geo>();
-    A.counts = c->counts.as<uint32_t>();
-    A.sizes = c->sc_size.as<uint32_t>();
-    A.soff = c->sc_scratch_off.as<uint64_t>();
+    // per-SC outputs are indexed by the global SC index: offset the bases by sc0
+    A.counts = c->counts.as<uint32_t>() - sc0;
+    A.sizes = c->sc_size.as<uint32_t>() - sc0;
+    A.soff = c->sc_scratch_off.as<uint64_t>() - sc0;
     A.ctl = c->build_ctl.as<unsigned long long>();
     A.overflow_list = c->overflow_list.as<uint32_t>();
     A.err = c->derr.as<DevError>();
     A.btab = nullptr;
     if (p.compress) {
-        SFCNL_CUDA_TRY(c->btab.reserve(num_sc * 16 * 2));
-        A.btab = c->btab.as<uint16_t>();
+        SFCNL_CUDA_TRY(c->btab.reserve(std::max<uint64_t>(num_sc, 1) * 16 * 2));
+        A.btab = c->btab.as<uint16_t>() - sc0 * 16;
     }
 
     unsigned long long ctl[3];
@@ -591,8 +667,8 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p) {
         A.scratch_cap = c->scratch.bytes;
         SFCNL_CUDA_TRY(cudaMemsetAsync(c->build_ctl.p, 0, 3 * 8, c->stream));
         stage_begin(c, kBuild);
-        const unsigned grid = unsigned(std::min<uint64_t>(num_sc, uint64_t(c->num_sms) * 64));
-        launch(c, k_build_smem, dim3(grid), dim3(kBuildThreads), 0, A, num_sc);
+        const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(num_sc, uint64_t(c->num_sms) * 64)));
+        launch(c, k_build_smem, dim3(grid), dim3(kBuildThreads), 0, A, sc0, sc1);
         SFCNL_CUDA_TRY(cudaGetLastError());
         SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 3 * 8, cudaMemcpyDeviceToHost, c->stream));
         SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -643,4 +719,61 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p) {
     return 0;
 }
 
+int run_halo_mark(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, uint64_t sc1) {
+    if (p.ci == 0 || p.cj == 0 || 64 % p.ci || 64 % p.cj || p.ci % p.cj)
+        return set_error(c, 1, "ClusterParams: invalid cluster parameters");
+    if (!(p.build_radius_scale >= 1.0)) return set_error(c, 1, "BuildParams: build_radius_scale must be >= 1");
+    if (!c->sorted.valid) return set_error(c, 1, "halo_mark: no particles");
+    const uint64_t n = c->sorted.n;
+    if (!c->has_tree || c->tree_n != n) return set_error(c, 2, "halo_mark: octree/particle-set mismatch");
+    const uint64_t total_sc = (n + 63) / 64;
+    if (sc1 > total_sc) sc1 = total_sc;
+    if (sc0 > sc1) return set_error(c, 1, "halo_mark: bad super-cluster range");
+    const uint64_t nj = (n + p.cj - 1) / p.cj;
+    SFCNL_CUDA_TRY(c->jflags.reserve(std::max<uint64_t>(nj, 1)));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(c->jflags.p, 0, std::max<uint64_t>(nj, 1), c->stream));
+    c->jflags_valid = false;
+    if (sc1 > sc0) {
+        const uint64_t p_lo = sc0 * 64, p_hi = tmin<uint64_t>(sc1 * 64, n);
+        int rc = run_cluster_geometry(c, p.ci, p.ci, p_lo, p_hi);  // i-clusters of the range
+        if (!rc && !c->node_geo_external) rc = run_node_geometry(c);
+        if (rc) return rc;
+        SFCNL_CUDA_TRY(c->build_ctl.reserve(8 * 8));
+        SFCNL_CUDA_TRY(cudaMemsetAsync(c->build_ctl.p, 0, 8 * 8, c->stream));
+        SFCNL_CUDA_TRY(c->overflow_list.reserve((sc1 - sc0) * 4));
+        BuildArgs A{};
+        A.n = n;
+        A.box = c->sorted.box;
+        A.scale = p.build_radius_scale;
+        A.ci = p.ci, A.cj = p.cj, A.icl_per_sc = 64 / p.ci, A.mask_bytes = (A.icl_per_sc + 7) / 8;
+        A.symmetric = p.mode != 0;
+        A.num_icl = (n + p.ci - 1) / p.ci;
+        A.nodes = c->nodes.as<Node>();
+        A.ngeo = c->node_geo.as<Geo>();
+        A.igeo = c->igeo.as<Geo>();
+        A.ctl = c->build_ctl.as<unsigned long long>();
+        A.overflow_list = c->overflow_list.as<uint32_t>();
+        A.err = c->derr.as<DevError>();
+        const unsigned grid = unsigned(std::min<uint64_t>(sc1 - sc0, uint64_t(c->num_sms) * 16));
+        launch(c, k_halo_smem, dim3(grid), dim3(kBuildThreads), 0, A, sc0, sc1, c->jflags.as<uint8_t>());
+        SFCNL_CUDA_TRY(cudaGetLastError());
+        unsigned long long ctl[2];
+        SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 2 * 8, cudaMemcpyDeviceToHost, c->stream));
+        SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        if (ctl[1]) {
+            const uint32_t fcap = uint32_t(std::min<uint64_t>(c->num_nodes + 8, 0x7fffffffull));
+            const uint64_t nblk = std::min<uint64_t>(ctl[1], 8);
+            SFCNL_CUDA_TRY(c->fallback_ws.reserve(nblk * 2 * uint64_t(fcap) * 4));
+            launch(c, k_halo_global, dim3(unsigned(nblk)), dim3(kBuildThreads), 0, A,
+                   (const uint32_t*)A.overflow_list, uint64_t(ctl[1]), c->fallback_ws.as<uint32_t>(), fcap,
+                   c->jflags.as<uint8_t>());
+            SFCNL_CUDA_TRY(cudaGetLastError());
+        }
+    }
+    c->jflags_valid = true;
+    c->jflags_sc0 = sc0, c->jflags_sc1 = sc1;
+    return 0;
+}
+
 }  // namespace sfcnl_cu
+

@@ -34,7 +34,6 @@ __device__ bool fast_masks(const BuildArgs& A, const Workspace& W, uint32_t nC, 
     __shared__ float s_pthr[8];
     __shared__ float s_red[4][4];
     __shared__ int s_unsafe;
-    __shared__ uint32_t s_npairs;
     const unsigned tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
     const unsigned nwarp = blockDim.x >> 5;
     const double ox = s_x[0], oy = s_y[0], oz = s_z[0];
@@ -94,7 +93,6 @@ __device__ bool fast_masks(const BuildArgs& A, const Workspace& W, uint32_t nC, 
         const uint32_t nc = tmin<uint32_t>(kCh, nC - c0);
         __syncthreads();  // previous chunk fully consumed
         for (uint32_t c = tid; c < nc; c += blockDim.x) s_cand[c] = W.cand[c0 + c], s_cm[c] = 0;
-        if (tid == 0) s_npairs = 0;
         __syncthreads();
         float emax = 0.f;
         for (uint32_t t = tid; t < nc * 8; t += blockDim.x) {

@@ -93,7 +93,8 @@ int check_box(sfcnl_cu_ctx* c, const sfcnl_box* b) {
 
 int upload(sfcnl_cu_ctx* c, DBuf& dst, const void* src, size_t bytes) {
     SFCNL_CUDA_TRY(dst.reserve(bytes));
-    if (bytes) SFCNL_CUDA_TRY(cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    // cudaMemcpyDefault: the source may be host (pageable/pinned) or device memory (UVA)
+    if (bytes) SFCNL_CUDA_TRY(cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyDefault, c->stream));
     return 0;
 }
 
@@ -105,6 +106,7 @@ int set_slot(sfcnl_cu_ctx* c, Slot& s, uint64_t n, const double* x, const double
     s.n = n;
     s.box = make_box(box);
     s.fields.clear();
+    drop_external(c);
     if (int rc = upload(c, s.x, x, n * 8)) return rc;
     if (int rc = upload(c, s.y, y, n * 8)) return rc;
     if (int rc = upload(c, s.z, z, n * 8)) return rc;
@@ -126,7 +128,7 @@ int set_slot_field(sfcnl_cu_ctx* c, Slot& s, const char* name, const double* v) 
 }
 
 int download(sfcnl_cu_ctx* c, void* dst, const void* src, size_t bytes) {
-    if (bytes && dst) SFCNL_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+    if (bytes && dst) SFCNL_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream));
     return 0;
 }
 
@@ -329,6 +331,7 @@ int sfcnl_cu_set_octree(sfcnl_cu_ctx* c, uint64_t num_nodes, const sfcnl_node* n
     c->tree_bits = bits;
     c->tree_n = n;
     c->has_tree = true;
+    drop_external(c);
     if (int rc = run_tree_levels_from_nodes(c, depth)) return rc;
     return finish(c);
 }
@@ -353,7 +356,7 @@ int sfcnl_cu_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params* p, uint64_t*
                          uint64_t* blob_bytes) {
     CallScope scope(c);
     if (!p) return set_error(c, SFCNL_INPUT_ERROR, "null build params");
-    if (int rc = run_build_store(c, *p)) return rc;
+    if (int rc = run_build_store(c, *p, 0, ~0ull, 0.0)) return rc;
     if (num_sc) *num_sc = c->num_sc;
     if (blob_bytes) *blob_bytes = c->blob_bytes;
     return finish(c);
@@ -388,6 +391,7 @@ int sfcnl_cu_set_store(sfcnl_cu_ctx* c, const sfcnl_build_params* p, uint64_t n,
     c->blob_bytes = blob_bytes;
     c->has_store = true;
     c->btab_valid = false;  // rebuilt on demand by the pass
+    c->sc_base = 0;
     return finish(c);
 }
 
@@ -396,12 +400,152 @@ int sfcnl_cu_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params* p, double* const* 
     if (!p) return set_error(c, SFCNL_INPUT_ERROR, "null pass params");
     if (int rc = run_reduce(c, *p)) return rc;
     const int no = p->kernel >= 2 ? 4 : 1;
-    const uint64_t n = c->sorted.n;
+    const uint64_t n = pass_out_count(c);
     if (outs)
         for (int o = 0; o < no; ++o)
             if (int rc = download(c, outs[o], c->outs[o].p, n * 8)) return rc;
     if (int rc = download(c, count, c->ncount.p, n * 4)) return rc;
     return finish(c);
+}
+
+int sfcnl_cu_build_store_range(sfcnl_cu_ctx* c, const sfcnl_build_params* p, uint64_t sc_begin, uint64_t sc_end,
+                               double max_h, uint64_t* num_sc, uint64_t* blob_bytes) {
+    CallScope scope(c);
+    if (!p) return set_error(c, SFCNL_INPUT_ERROR, "null build params");
+    if (int rc = run_build_store(c, *p, sc_begin, sc_end, max_h)) return rc;
+    if (num_sc) *num_sc = c->num_sc;
+    if (blob_bytes) *blob_bytes = c->blob_bytes;
+    return finish(c);
+}
+
+int sfcnl_cu_alloc_sorted(sfcnl_cu_ctx* c, uint64_t n, const sfcnl_box* box, const char* const* fields,
+                          int nfields) {
+    CallScope scope(c);
+    if (int rc = check_box(c, box)) return rc;
+    Slot& s = c->sorted;
+    s.valid = false;
+    s.n = n;
+    s.box = make_box(box);
+    c->has_store = false;
+    c->btab_valid = false;
+    drop_external(c);
+    for (DBuf* b : {&s.x, &s.y, &s.z, &s.h}) SFCNL_CUDA_TRY(b->reserve(std::max<uint64_t>(n, 1) * 8));
+    // keep the allocations of fields that survive (steps re-allocate the same set)
+    std::vector<Field> next(nfields > 0 ? nfields : 0);
+    for (int k = 0; k < nfields; ++k) {
+        if (!fields[k]) return set_error(c, SFCNL_INPUT_ERROR, "alloc_sorted: null field name");
+        next[k].name = fields[k];
+        if (Field* old = s.find(fields[k])) next[k].data = std::move(old->data);
+        SFCNL_CUDA_TRY(next[k].data.reserve(std::max<uint64_t>(n, 1) * 8));
+    }
+    s.fields = std::move(next);
+    s.valid = true;
+    return finish(c);
+}
+
+static DBuf* sorted_array(sfcnl_cu_ctx* c, const char* name) {
+    Slot& s = c->sorted;
+    const std::string nm = name ? name : "";
+    if (nm == "x") return &s.x;
+    if (nm == "y") return &s.y;
+    if (nm == "z") return &s.z;
+    if (nm == "h") return &s.h;
+    Field* f = s.find(nm);
+    return f ? &f->data : nullptr;
+}
+
+int sfcnl_cu_write_sorted(sfcnl_cu_ctx* c, const char* name, uint64_t offset, uint64_t count, const double* src,
+                          int src_on_device) {
+    CallScope scope(c);
+    DBuf* b = sorted_array(c, name);
+    if (!c->sorted.valid || !b) return set_error(c, SFCNL_INPUT_ERROR, "write_sorted: no such sorted array");
+    if (offset + count > c->sorted.n) return set_error(c, SFCNL_INPUT_ERROR, "write_sorted: range out of bounds");
+    if (count)
+        SFCNL_CUDA_TRY(cudaMemcpyAsync(b->as<double>() + offset, src, count * 8,
+                                       src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+    return finish(c);
+}
+
+int sfcnl_cu_read_sorted(sfcnl_cu_ctx* c, const char* name, uint64_t offset, uint64_t count, double* dst,
+                         int dst_on_device) {
+    CallScope scope(c);
+    DBuf* b = sorted_array(c, name);
+    if (!c->sorted.valid || !b) return set_error(c, SFCNL_INPUT_ERROR, "read_sorted: no such sorted array");
+    if (offset + count > c->sorted.n) return set_error(c, SFCNL_INPUT_ERROR, "read_sorted: range out of bounds");
+    if (count)
+        SFCNL_CUDA_TRY(cudaMemcpyAsync(dst, b->as<double>() + offset, count * 8,
+                                       dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+    return finish(c);
+}
+
+int sfcnl_cu_read_order(sfcnl_cu_ctx* c, uint64_t offset, uint64_t count, uint64_t* keys, uint32_t* perm,
+                        int dst_on_device) {
+    CallScope scope(c);
+    if (!c->has_order || offset + count > c->order_n) return set_error(c, SFCNL_INPUT_ERROR, "read_order: bad range");
+    const cudaMemcpyKind k = dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (count && keys) SFCNL_CUDA_TRY(cudaMemcpyAsync(keys, c->keys.as<uint64_t>() + offset, count * 8, k, c->stream));
+    if (count && perm) SFCNL_CUDA_TRY(cudaMemcpyAsync(perm, c->perm.as<uint32_t>() + offset, count * 4, k, c->stream));
+    return finish(c);
+}
+
+int sfcnl_cu_set_keys(sfcnl_cu_ctx* c, uint64_t n, const uint64_t* keys, int src_on_device, int bits) {
+    CallScope scope(c);
+    if (bits < 1 || bits > 21) return set_error(c, SFCNL_INPUT_ERROR, "bits per dimension must be in [1, 21]");
+    SFCNL_CUDA_TRY(c->keys.reserve(std::max<uint64_t>(n, 1) * 8));
+    SFCNL_CUDA_TRY(c->perm.reserve(std::max<uint64_t>(n, 1) * 4));
+    if (n)
+        SFCNL_CUDA_TRY(cudaMemcpyAsync(c->keys.p, keys, n * 8,
+                                       src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+    c->order_n = n;
+    c->bits = bits;
+    c->has_order = true;
+    c->has_tree = false;
+    drop_external(c);
+    return finish(c);
+}
+
+int sfcnl_cu_apply_order_into(sfcnl_cu_ctx* c, uint64_t offset) {
+    CallScope scope(c);
+    if (offset > (uint64_t(1) << 62)) return set_error(c, SFCNL_INPUT_ERROR, "apply_order_into: bad offset");
+    if (int rc = run_apply_order(c, int64_t(offset))) return rc;
+    return finish(c);
+}
+
+int sfcnl_cu_node_geometry_range(sfcnl_cu_ctx* c, uint64_t p_begin, uint64_t p_end) {
+    CallScope scope(c);
+    if (int rc = run_node_geometry(c, p_begin, p_end)) return rc;
+    c->node_geo_external = true;
+    return finish(c);
+}
+
+int sfcnl_cu_halo_mark(sfcnl_cu_ctx* c, const sfcnl_build_params* p, uint64_t sc_begin, uint64_t sc_end,
+                       uint64_t* num_jclusters) {
+    CallScope scope(c);
+    if (!p) return set_error(c, SFCNL_INPUT_ERROR, "null build params");
+    if (int rc = run_halo_mark(c, *p, sc_begin, sc_end)) return rc;
+    if (num_jclusters) *num_jclusters = (c->sorted.n + p->cj - 1) / p->cj;
+    return finish(c);
+}
+
+int sfcnl_cu_device_array(sfcnl_cu_ctx* c, const char* name, void** ptr, uint64_t* bytes) {
+    CallScope scope(c);
+    if (!name || !ptr) return set_error(c, SFCNL_INPUT_ERROR, "device_array: null argument");
+    const std::string nm = name;
+    DBuf* b = nullptr;
+    uint64_t len = 0;
+    if (nm == "keys" && c->has_order) b = &c->keys, len = c->order_n * 8;
+    else if (nm == "perm" && c->has_order) b = &c->perm, len = c->order_n * 4;
+    else if (nm == "node_geo" && c->has_tree) b = &c->node_geo, len = c->num_nodes * sizeof(Geo);
+    else if (nm == "nodes" && c->has_tree) b = &c->nodes, len = c->num_nodes * sizeof(Node);
+    else if (nm == "halo_flags" && c->jflags_valid) b = &c->jflags, len = (c->sorted.n + c->sp.cj - 1) / c->sp.cj;
+    else if (nm.rfind("out", 0) == 0 && nm.size() == 4 && nm[3] >= '0' && nm[3] <= '3')
+        b = &c->outs[nm[3] - '0'], len = pass_out_count(c) * 8;
+    else if (nm == "count") b = &c->ncount, len = pass_out_count(c) * 4;
+    else if (c->sorted.valid && (b = sorted_array(c, name))) len = c->sorted.n * 8;
+    if (!b || (len && len > b->bytes)) return set_error(c, SFCNL_INPUT_ERROR, "device_array: no such array: " + nm);
+    *ptr = b->p;
+    if (bytes) *bytes = len;
+    return 0;
 }
 
 }  // extern "C"

@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <string>
 #include <utility>
 #include <vector>
@@ -95,6 +96,7 @@ struct sfcnl_cu_ctx {
     sfcnl_cu::DBuf level_nodes;  // node indices grouped by depth (deepest processed first)
     std::vector<uint64_t> level_off;  // host: level d occupies [level_off[d], level_off[d+1])
     sfcnl_cu::DBuf node_geo;   // Geo[num_nodes]
+    bool node_geo_external = false;  // node_geo supplied by the caller (domain decomposition)
     sfcnl_cu::DBuf tree_scratch;
     // level-synchronous construction scratch, one entry per depth
     struct Level {
@@ -114,6 +116,10 @@ struct sfcnl_cu_ctx {
     sfcnl_cu::DBuf counts, offsets, blob;
     sfcnl_cu::DBuf btab;  // device-side codec block offsets per SC (u16 x 16), not part of the store
     bool btab_valid = false;
+    uint64_t sc_base = 0;  // first (global) super-cluster of the current store
+    sfcnl_cu::DBuf jflags;  // halo: u8 per global j-cluster, set by run_halo_mark
+    bool jflags_valid = false;
+    uint64_t jflags_sc0 = 0, jflags_sc1 = 0;
     sfcnl_cu::DBuf sc_size, sc_scratch_off, scratch, build_ctl, overflow_list, fallback_ws;
 
     // (5) pass
@@ -143,17 +149,33 @@ void stage_end(sfcnl_cu_ctx* c, Stage s);
 
 // Kernel drivers (each in its own .cu).
 int run_sort_by_sfc(sfcnl_cu_ctx* c, int bits);
-int run_apply_order(sfcnl_cu_ctx* c);
+int run_apply_order(sfcnl_cu_ctx* c, int64_t into = -1);  // into >= 0: gather into sorted[into..]
 int run_build_octree(sfcnl_cu_ctx* c, uint32_t bucket);
 int run_tree_levels_from_nodes(sfcnl_cu_ctx* c, const std::vector<uint8_t>& depth);
-int run_node_geometry(sfcnl_cu_ctx* c);
-int run_cluster_geometry(sfcnl_cu_ctx* c, uint32_t ci, uint32_t cj);
-int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p);
+int run_node_geometry(sfcnl_cu_ctx* c, uint64_t p0 = 0, uint64_t p1 = ~0ull);  // leaves clip to [p0, p1)
+// clusters overlapping particles [p0, p1), plus j-clusters flagged in jflags (if non-null)
+int run_cluster_geometry(sfcnl_cu_ctx* c, uint32_t ci, uint32_t cj, uint64_t p0 = 0, uint64_t p1 = ~0ull,
+                         const uint8_t* jflags = nullptr);
+int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, uint64_t sc1, double max_h);
 int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p);
+int run_halo_mark(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, uint64_t sc1);
 
 // Host helpers shared with the C++ drop-in.
 void hilbert_table(uint16_t* table);  // 48 states x 8 octants: out | next << 3
 int host_set_error(int code, const std::string& msg, uint64_t off = 0);
+
+// Caller-supplied node geometry and halo flags describe one tree + particle set.
+inline void drop_external(sfcnl_cu_ctx* c) {
+    c->node_geo_external = false;
+    c->jflags_valid = false;
+}
+
+// Particles covered by the current store's super-cluster range (outputs of a pass).
+inline uint64_t pass_out_count(const sfcnl_cu_ctx* c) {
+    const uint64_t lo = c->sc_base * 64;
+    const uint64_t hi = std::min<uint64_t>(c->sorted.n, (c->sc_base + c->num_sc) * 64);
+    return hi > lo ? hi - lo : 0;
+}
 
 template <class K, class... A>
 inline void launch(sfcnl_cu_ctx* c, K kernel, dim3 grid, dim3 block, size_t smem, A... args) {

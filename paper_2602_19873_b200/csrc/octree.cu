@@ -127,7 +127,7 @@ __global__ void k_write_nodes(int d, int bits, uint64_t m, const uint64_t* __res
 __global__ void k_node_geo(const uint32_t* __restrict__ list, uint64_t m, const Node* __restrict__ nodes,
                            const double* __restrict__ x, const double* __restrict__ y,
                            const double* __restrict__ z, const double* __restrict__ h,
-                           Geo* __restrict__ geo) {
+                           Geo* __restrict__ geo, uint64_t p0, uint64_t p1) {
     const uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (k >= m) return;
     const uint32_t idx = list[k];
@@ -135,7 +135,10 @@ __global__ void k_node_geo(const uint32_t* __restrict__ list, uint64_t m, const 
     Geo g;
     geo_init(g);
     if (nd.first_child < 0) {
-        for (uint32_t i = nd.pbegin; i < nd.pend; ++i) {
+        // leaves see only particles [p0, p1) (a rank's partial geometry; min/max
+        // combine exactly across ranks)
+        const uint64_t b = nd.pbegin > p0 ? nd.pbegin : p0, e = nd.pend < p1 ? nd.pend : p1;
+        for (uint64_t i = b; i < e; ++i) {
             geo_extend_pt(g, x[i], y[i], z[i]);
             g.maxh = smax(g.maxh, h[i]);
         }
@@ -151,9 +154,11 @@ __global__ void k_node_geo(const uint32_t* __restrict__ list, uint64_t m, const 
 
 __global__ void k_cluster_geo(uint64_t n, uint32_t width, uint64_t ncl, const double* __restrict__ x,
                               const double* __restrict__ y, const double* __restrict__ z,
-                              const double* __restrict__ h, Geo* __restrict__ geo) {
+                              const double* __restrict__ h, Geo* __restrict__ geo, uint64_t k0, uint64_t k1,
+                              const uint8_t* __restrict__ flags) {
     const uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     if (k >= ncl) return;
+    if ((k < k0 || k >= k1) && !(flags && flags[k])) return;  // not read by this rank
     const uint64_t b = k * width, e = tmin<uint64_t>(b + width, n);
     Geo g;
     geo_init(g);
@@ -249,6 +254,7 @@ int run_build_octree(sfcnl_cu_ctx* c, uint32_t bucket) {
     c->tree_bits = bits;
     c->tree_n = n;
     c->has_tree = true;
+    drop_external(c);
     return 0;
 }
 
@@ -268,7 +274,7 @@ int run_tree_levels_from_nodes(sfcnl_cu_ctx* c, const std::vector<uint8_t>& dept
     return 0;
 }
 
-int run_node_geometry(sfcnl_cu_ctx* c) {
+int run_node_geometry(sfcnl_cu_ctx* c, uint64_t p0, uint64_t p1) {
     if (!c->has_tree) return set_error(c, 1, "node geometry: no octree");
     if (!c->sorted.valid || c->sorted.n != c->tree_n)
         return set_error(c, 2, "build_neighbor_store: octree/particle-set mismatch");
@@ -282,27 +288,30 @@ int run_node_geometry(sfcnl_cu_ctx* c) {
                (const uint32_t*)(c->level_nodes.as<uint32_t>() + c->level_off[d]), m,
                (const Node*)c->nodes.as<Node>(), c->sorted.x.as<const double>(),
                c->sorted.y.as<const double>(), c->sorted.z.as<const double>(),
-               c->sorted.h.as<const double>(), c->node_geo.as<Geo>());
+               c->sorted.h.as<const double>(), c->node_geo.as<Geo>(), p0, p1);
     }
     SFCNL_CUDA_TRY(cudaGetLastError());
     stage_end(c, kNodeGeo);
     return 0;
 }
 
-int run_cluster_geometry(sfcnl_cu_ctx* c, uint32_t ci, uint32_t cj) {
+int run_cluster_geometry(sfcnl_cu_ctx* c, uint32_t ci, uint32_t cj, uint64_t p0, uint64_t p1,
+                         const uint8_t* jflags) {
     const uint64_t n = c->sorted.n;
     const uint64_t ni = (n + ci - 1) / ci, nj = (n + cj - 1) / cj;
     SFCNL_CUDA_TRY(c->igeo.reserve(std::max<uint64_t>(ni, 1) * sizeof(Geo)));
     SFCNL_CUDA_TRY(c->jgeo.reserve(std::max<uint64_t>(nj, 1) * sizeof(Geo)));
     if (!n) return 0;
+    if (p1 > n) p1 = n;
     stage_begin(c, kClusterGeo);
+    // i-clusters: the range (plus the flagged halo when the array doubles as jgeo)
     launch(c, k_cluster_geo, dim3(blocks_for(ni)), dim3(256), 0, n, ci, ni, c->sorted.x.as<const double>(),
            c->sorted.y.as<const double>(), c->sorted.z.as<const double>(), c->sorted.h.as<const double>(),
-           c->igeo.as<Geo>());
+           c->igeo.as<Geo>(), p0 / ci, (p1 + ci - 1) / ci, cj == ci ? jflags : (const uint8_t*)nullptr);
     if (cj != ci)
         launch(c, k_cluster_geo, dim3(blocks_for(nj)), dim3(256), 0, n, cj, nj, c->sorted.x.as<const double>(),
                c->sorted.y.as<const double>(), c->sorted.z.as<const double>(),
-               c->sorted.h.as<const double>(), c->jgeo.as<Geo>());
+               c->sorted.h.as<const double>(), c->jgeo.as<Geo>(), p0 / cj, (p1 + cj - 1) / cj, jflags);
     SFCNL_CUDA_TRY(cudaGetLastError());
     stage_end(c, kClusterGeo);
     return 0;

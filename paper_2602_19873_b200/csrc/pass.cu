@@ -40,7 +40,7 @@ struct PassArgs {
     Box box;
     uint32_t ci, cj, icl_per_sc, mask_bytes;
     int w, compress, symmetric;
-    uint64_t num_sc, num_icl;
+    uint64_t sc_begin, num_sc, num_icl;  // super-clusters [sc_begin, num_sc) (global numbering)
     const uint32_t* counts;
     const uint64_t* offsets;
     const uint8_t* blob;
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(kExactThreads) k_pass_exact(PassArgs A) {
     __shared__ uint32_t s_idx[64];
     __shared__ unsigned long long s_msk[64];
     __shared__ int s_len;
-    for (uint64_t sc = blockIdx.x; sc < A.num_sc; sc += gridDim.x) {
+    for (uint64_t sc = A.sc_begin + blockIdx.x; sc < A.num_sc; sc += gridDim.x) {
         ScStream st;
         if (!open_sc(A, sc, st)) continue;
         sc_exact<K>(A, sc, st, s_idx, s_msk, &s_len);
@@ -341,7 +341,7 @@ __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& 
 // block headers (first kBtab blocks) and records where each block starts.
 __global__ void k_block_table(PassArgs A, uint16_t* btab) {
     __shared__ uint32_t scratch[8][64];
-    const uint64_t sc = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+    const uint64_t sc = A.sc_begin + ((blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5);
     if (sc >= A.num_sc) return;
     const uint32_t count = A.counts[sc];
     if (!count) return;
@@ -365,7 +365,7 @@ __global__ void k_block_table(PassArgs A, uint16_t* btab) {
 template <int K>
 void launch_pass(sfcnl_cu_ctx* c, const PassArgs& A, bool fast) {
     if (fast) {
-        const unsigned grid = unsigned(std::min<uint64_t>(A.num_sc, uint64_t(c->num_sms) * 2));
+        const unsigned grid = unsigned(std::min<uint64_t>(A.num_sc - A.sc_begin, uint64_t(c->num_sms) * 2));
         if (A.cj == 8) {
             const size_t smem = ws_smem<K, 8>();
             cudaFuncSetAttribute(k_pass_ws<K, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -376,7 +376,7 @@ void launch_pass(sfcnl_cu_ctx* c, const PassArgs& A, bool fast) {
             launch(c, k_pass_ws<K, 4>, dim3(grid), dim3(kWsThreads), smem, A);
         }
     } else {
-        const unsigned grid = unsigned(std::min<uint64_t>(A.num_sc, uint64_t(c->num_sms) * 32));
+        const unsigned grid = unsigned(std::min<uint64_t>(A.num_sc - A.sc_begin, uint64_t(c->num_sms) * 32));
         launch(c, k_pass_exact<K>, dim3(grid), dim3(kExactThreads), 0, A);
     }
 }
@@ -404,36 +404,44 @@ int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p) {
         A.q = f->data.as<double>();
     }
     const int no = p.kernel >= 2 ? 4 : 1;
-    for (int o = 0; o < no; ++o) SFCNL_CUDA_TRY(c->outs[o].reserve(std::max<uint64_t>(n, 1) * 8));
-    SFCNL_CUDA_TRY(c->ncount.reserve(std::max<uint64_t>(n, 1) * 4));
-    if (n == 0) return 0;
+    // A range store (sc_base > 0 or a partial range) covers particles
+    // [sc_base*64, sc_base*64 + nout); outputs are indexed locally.
+    const uint64_t nout = pass_out_count(c);
+    const uint64_t p0 = c->sc_base * 64;
+    for (int o = 0; o < no; ++o) SFCNL_CUDA_TRY(c->outs[o].reserve(std::max<uint64_t>(nout, 1) * 8));
+    SFCNL_CUDA_TRY(c->ncount.reserve(std::max<uint64_t>(nout, 1) * 4));
+    if (nout == 0) return 0;
     const bool symmetric = c->sp.mode != 0;
+    if (symmetric && (c->sc_base != 0 || nout != n))
+        return set_error(c, 1, "reduce: symmetric stores cannot be restricted to a super-cluster range");
     const bool fast = p.precision == 1 && !symmetric && c->sp.ci == 8 && (c->sp.cj == 8 || c->sp.cj == 4);
     if (symmetric || !fast) {
-        for (int o = 0; o < no; ++o) SFCNL_CUDA_TRY(cudaMemsetAsync(c->outs[o].p, 0, n * 8, c->stream));
-        SFCNL_CUDA_TRY(cudaMemsetAsync(c->ncount.p, 0, n * 4, c->stream));
+        for (int o = 0; o < no; ++o) SFCNL_CUDA_TRY(cudaMemsetAsync(c->outs[o].p, 0, nout * 8, c->stream));
+        SFCNL_CUDA_TRY(cudaMemsetAsync(c->ncount.p, 0, nout * 4, c->stream));
     }
     SFCNL_CUDA_TRY(cudaMemsetAsync(c->derr.p, 0xff, sizeof(DevError), c->stream));
     A.n = n;
     A.box = c->sorted.box;
     A.ci = c->sp.ci, A.cj = c->sp.cj, A.icl_per_sc = 64 / c->sp.ci, A.mask_bytes = (A.icl_per_sc + 7) / 8;
     A.w = c->sp.w, A.compress = c->sp.compress, A.symmetric = symmetric;
-    A.num_sc = c->num_sc, A.num_icl = (n + A.ci - 1) / A.ci;
-    A.counts = c->counts.as<uint32_t>(), A.offsets = c->offsets.as<uint64_t>(), A.blob = c->blob.as<uint8_t>();
+    A.sc_begin = c->sc_base, A.num_sc = c->sc_base + c->num_sc, A.num_icl = (n + A.ci - 1) / A.ci;
+    // store arrays are local to the range: shift them so kernels index by global SC
+    A.counts = c->counts.as<uint32_t>() - c->sc_base, A.offsets = c->offsets.as<uint64_t>() - c->sc_base;
+    A.blob = c->blob.as<uint8_t>();
     if (fast && A.compress) {
         if (!c->btab_valid) {
             SFCNL_CUDA_TRY(c->btab.reserve(c->num_sc * kBtab * 2));
             launch(c, k_block_table, dim3(unsigned((c->num_sc * 32 + 255) / 256)), dim3(256), 0, A,
-                   c->btab.as<uint16_t>());
+                   c->btab.as<uint16_t>() - c->sc_base * kBtab);
             c->btab_valid = true;
         }
-        A.btab = c->btab.as<uint16_t>();
+        A.btab = c->btab.as<uint16_t>() - c->sc_base * kBtab;
     }
     A.x = c->sorted.x.as<double>(), A.y = c->sorted.y.as<double>(), A.z = c->sorted.z.as<double>();
     A.h = c->sorted.h.as<double>();
     A.qs = p.query_scale, A.eps = p.epsilon, A.sigma = p.sigma, A.ck = p.coulomb_k;
-    for (int o = 0; o < 4; ++o) A.out[o] = c->outs[o].as<double>();
-    A.cnt = c->ncount.as<uint32_t>();
+    for (int o = 0; o < 4; ++o) A.out[o] = c->outs[o].as<double>() - p0;
+    A.cnt = c->ncount.as<uint32_t>() - p0;
     A.err = c->derr.as<DevError>();
     stage_begin(c, kPass);
     switch (p.kernel) {

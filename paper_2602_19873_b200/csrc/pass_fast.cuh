@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kFastThreads, 3) k_pass_fast(PassArgs A) {
     const float sig2 = float(A.sigma * A.sigma);
     const float eps24 = float(24.0 * A.eps), eps4 = float(4.0 * A.eps);
     const float close2 = 1.5f * sig2;  // (1.22 sigma)^2: LJ pairs this close go to fp64
-    for (uint64_t sc = blockIdx.x; sc < A.num_sc; sc += gridDim.x) {
+    for (uint64_t sc = A.sc_begin + blockIdx.x; sc < A.num_sc; sc += gridDim.x) {
         ScStream st;
         if (!open_sc(A, sc, st)) continue;
         const uint64_t p0 = sc * kSC;

@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_pass_ws(PassArgs A) {
         const unsigned ptid = tid - kWsConsumers, pwarp = warp - 8;
         int buf = 0;
         int uses[2] = {0, 0};
-        for (uint64_t sc = blockIdx.x; sc < A.num_sc; sc += gridDim.x) {
+        for (uint64_t sc = A.sc_begin + blockIdx.x; sc < A.num_sc; sc += gridDim.x) {
             ScStream st;
             const bool ok = open_sc(A, sc, st);
             const uint32_t nchunks = (ok && st.count) ? (st.count + kWsCap - 1) / kWsCap : 1;

@@ -332,33 +332,49 @@ int run_sort_by_sfc(sfcnl_cu_ctx* c, int bits) {
     return 0;
 }
 
-int run_apply_order(sfcnl_cu_ctx* c) {
+int run_apply_order(sfcnl_cu_ctx* c, int64_t into) {
     if (!c->has_order || !c->orig.valid || c->order_n != c->orig.n)
         return set_error(c, 1, "apply_sfc_order: permutation size mismatch");
     const uint64_t n = c->orig.n;
     Slot& s = c->sorted;
-    s.n = n;
-    s.box = c->orig.box;
     std::vector<const double*> src{c->orig.x.as<double>(), c->orig.y.as<double>(),
                                    c->orig.z.as<double>(), c->orig.h.as<double>()};
-    SFCNL_CUDA_TRY(s.x.reserve(n * 8));
-    SFCNL_CUDA_TRY(s.y.reserve(n * 8));
-    SFCNL_CUDA_TRY(s.z.reserve(n * 8));
-    SFCNL_CUDA_TRY(s.h.reserve(n * 8));
-    std::vector<double*> dst{s.x.as<double>(), s.y.as<double>(), s.z.as<double>(), s.h.as<double>()};
-    std::vector<Field> newf;
-    for (auto& f : c->orig.fields) {
-        Field* existing = s.find(f.name);
-        Field g;
-        g.name = f.name;
-        if (existing) g.data = std::move(existing->data);
-        SFCNL_CUDA_TRY(g.data.reserve(n * 8));
-        src.push_back(f.data.as<double>());
-        dst.push_back(g.data.as<double>());
-        newf.push_back(std::move(g));
+    std::vector<double*> dst;
+    if (into >= 0) {
+        // gather into elements [into, into + n) of an allocated (larger) sorted slot
+        if (!s.valid || uint64_t(into) + n > s.n)
+            return set_error(c, 1, "apply_order_into: sorted slot too small");
+        const uint64_t o = uint64_t(into);
+        dst = {s.x.as<double>() + o, s.y.as<double>() + o, s.z.as<double>() + o, s.h.as<double>() + o};
+        for (auto& f : c->orig.fields) {
+            Field* g = s.find(f.name);
+            if (!g) return set_error(c, 1, "apply_order_into: sorted slot lacks field " + f.name);
+            src.push_back(f.data.as<double>());
+            dst.push_back(g->data.as<double>() + o);
+        }
+    } else {
+        s.n = n;
+        s.box = c->orig.box;
+        SFCNL_CUDA_TRY(s.x.reserve(n * 8));
+        SFCNL_CUDA_TRY(s.y.reserve(n * 8));
+        SFCNL_CUDA_TRY(s.z.reserve(n * 8));
+        SFCNL_CUDA_TRY(s.h.reserve(n * 8));
+        dst = {s.x.as<double>(), s.y.as<double>(), s.z.as<double>(), s.h.as<double>()};
+        std::vector<Field> newf;
+        for (auto& f : c->orig.fields) {
+            Field* existing = s.find(f.name);
+            Field g;
+            g.name = f.name;
+            if (existing) g.data = std::move(existing->data);
+            SFCNL_CUDA_TRY(g.data.reserve(n * 8));
+            src.push_back(f.data.as<double>());
+            dst.push_back(g.data.as<double>());
+            newf.push_back(std::move(g));
+        }
+        s.fields = std::move(newf);
+        s.valid = true;
+        drop_external(c);
     }
-    s.fields = std::move(newf);
-    s.valid = true;
     if (n == 0) return 0;
     const int narr = int(src.size());
     SFCNL_CUDA_TRY(c->ptrs.reserve(2 * narr * sizeof(void*)));

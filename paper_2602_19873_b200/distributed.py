@@ -1,0 +1,331 @@
+"""SFC key-range domain decomposition over ranks.
+
+The reference is single-process (``parallel_for`` over super-clusters,
+neighbor_build.cpp:109 / reduce.hpp:217-220). Super-clusters are independent, so the
+path shards: rank r owns a contiguous range of the GLOBAL SFC order, snapped to
+super-cluster (64-particle) boundaries, and builds + queries only its super-clusters.
+The union of the per-rank stores is byte-identical to the single-domain store and the
+union of the per-rank pass outputs is identical to the single-domain outputs.
+
+One step (``DomainDecomposition.run``), one process per GPU:
+
+1. local SFC sort of the rank's input particles (K1-K3, own kernels);
+2. exact global split of the (key, global id) order at the super-cluster bounds:
+   a 64-round binary search on the key value (one all-reduce of P-1 counts per round,
+   no host sync), then ties split in rank order (= global id order);
+3. all-to-all of the particle payload (x, y, z, h, fields) to the owners;
+4. owner: local SFC sort of what it received (stable => (key, global id) order) and
+   a gather straight into its slice of global-index arrays (apply_order_into);
+5. all-gather of the owned keys -> every rank builds the identical global octree
+   (reference numbering);
+6. node geometry from owned particles only, combined exactly by one MIN all-reduce
+   (hi and max h negated): min/max are order-independent, so the result equals
+   compute_node_aabbs / compute_node_max_radius of the whole set;
+7. halo: the rank's build traversal marks the candidate j-clusters it will read
+   (exactly collect_candidates, neighbor_build.cpp:43-65); the missing ones are
+   requested from their owners and their particles exchanged by two all-to-alls;
+8. range build (build_store_range) and range pass (reduce) over owned super-clusters.
+
+Collectives go through ``Comm`` (torch.distributed: NCCL on device tensors; other
+backends, e.g. gloo for CPU tests or several ranks sharing one GPU, are staged through
+host memory). The engine does the per-rank work: ``CudaEngine`` (this module) drives
+the C-ABI context; the parity tests plug in a CPU engine over the oracle.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from .api import (BuildParams, Context, Kernel, NeighborStore, ParticleSet, PassConfig, ReduceResult,
+                  SimulationBox, kDefaultSfcBits)
+
+SC = 64  # super-cluster size (cluster.hpp:9)
+KEY_SPAN = 1 << 63  # keys are < 2^(3*21)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def sc_partition(n_total: int, world: int):
+    """Super-cluster bounds and particle bounds of each rank (balanced SC counts)."""
+    total_sc = (n_total + SC - 1) // SC
+    scb = [(q * total_sc) // world for q in range(world + 1)]
+    pb = [min(SC * s, n_total) for s in scb]
+    return scb, pb
+
+
+class Comm:
+    """Collectives over a torch.distributed process group on the engine's tensors."""
+
+    def __init__(self, group=None):
+        dist = _torch().distributed
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.staged = dist.get_backend(group) != "nccl"
+
+    def _in(self, t):
+        return t.cpu() if (self.staged and t.is_cuda) else t
+
+    def allreduce_(self, t, op="sum"):
+        dist = _torch().distributed
+        o = {"sum": dist.ReduceOp.SUM, "min": dist.ReduceOp.MIN, "max": dist.ReduceOp.MAX}[op]
+        if self.world == 1:
+            return t
+        c = self._in(t)
+        dist.all_reduce(c, op=o, group=self.group)
+        if c is not t:
+            t.copy_(c)
+        return t
+
+    def all_gather(self, t):
+        """Equal-size all-gather along dim 0 -> [world, *t.shape]."""
+        torch = _torch()
+        if self.world == 1:
+            return t.unsqueeze(0).clone()
+        c = self._in(t.contiguous())
+        out = torch.empty((self.world * c.shape[0],) + tuple(c.shape[1:]), dtype=c.dtype, device=c.device)
+        torch.distributed.all_gather_into_tensor(out, c, group=self.group)
+        return out.view((self.world,) + tuple(c.shape)).to(t.device)
+
+    def all_gather_v(self, t, counts: Sequence[int]):
+        """Concatenation over ranks of t (dim 0), rank q contributing counts[q] rows."""
+        torch = _torch()
+        if self.world == 1:
+            return t.clone()
+        m = max(max(counts), 1)
+        pad = torch.zeros((m,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[: t.shape[0]] = t
+        g = self.all_gather(pad)
+        return torch.cat([g[q, : counts[q]] for q in range(self.world)])
+
+    def all_to_all_v(self, t, send: Sequence[int], recv: Sequence[int]):
+        torch = _torch()
+        if self.world == 1:
+            return t.clone()
+        c = self._in(t.contiguous())
+        out = torch.empty((int(sum(recv)),) + tuple(c.shape[1:]), dtype=c.dtype, device=c.device)
+        torch.distributed.all_to_all_single(out, c, output_split_sizes=[int(v) for v in recv],
+                                            input_split_sizes=[int(v) for v in send], group=self.group)
+        return out.to(t.device)
+
+
+@dataclass
+class RankResult:
+    rank: int
+    n_total: int
+    p_begin: int
+    p_end: int
+    sc_begin: int
+    sc_end: int
+    num_nodes: int
+    halo_particles: int
+    store: Optional[NeighborStore]
+    results: List[Optional[ReduceResult]]
+
+
+class CudaEngine:
+    """Per-rank work on one GPU through the C-ABI context (device-resident)."""
+
+    def __init__(self, ctx: Context, box: SimulationBox, field_names: Sequence[str], bits=kDefaultSfcBits):
+        self.ctx, self.box, self.fields = ctx, box, list(field_names)
+        self.bits = bits
+        torch = _torch()
+        self.device = torch.device(f"cuda:{ctx.device}")
+        self.stream = torch.cuda.ExternalStream(ctx.stream(), device=self.device)
+        self.n_total = 0
+        self.num_nodes = 0
+
+    # -- inputs: the rank's particles stay resident (device copies) across steps
+    def upload(self, ps: ParticleSet):
+        torch = _torch()
+        cols = [ps.x, ps.y, ps.z, ps.h] + [ps.field(k) for k in self.fields]
+        with torch.cuda.stream(self.stream):
+            self.inp = [torch.from_numpy(np.ascontiguousarray(c)).to(self.device, non_blocking=True) for c in cols]
+        self.n_local = ps.size()
+
+    def _cols(self, n):
+        torch = _torch()
+        return [self.ctx.device_array(a, torch.float64, n) for a in ["x", "y", "z", "h"] + self.fields]
+
+    # -- (1) local sort; returns sorted keys (int64)
+    def local_sort(self):
+        torch = _torch()
+        self.ctx.set_particles_device(self.n_local, self.inp, self.fields, self.box)
+        self.ctx.sort(self.bits)
+        self.ctx.apply_order()
+        return self.ctx.device_array("keys", torch.int64, self.n_local)
+
+    def payload(self):
+        torch = _torch()
+        return torch.stack(self._cols(self.n_local), dim=1)
+
+    # -- (4) owner placement; returns the owned sorted keys
+    def own(self, recv, n_total, p0):
+        torch = _torch()
+        n = recv.shape[0]
+        cols = [recv[:, f].contiguous() for f in range(recv.shape[1])]
+        self.ctx.set_particles_device(n, cols, self.fields, self.box)
+        self.ctx.sort(self.bits)
+        self.ctx.alloc_sorted(n_total, self.box, self.fields)
+        self.ctx.apply_order_into(p0)
+        self.n_total = n_total
+        return self.ctx.device_array("keys", torch.int64, n).clone()
+
+    # -- (5) global octree
+    def octree(self, gkeys, bucket):
+        self.ctx.set_keys_device(gkeys, self.bits)
+        self.num_nodes = self.ctx.octree(bucket)
+        return self.num_nodes
+
+    # -- (6) partial node geometry: [num_nodes, 8] view (lo3, hi3, maxh, pad), combined in place
+    def node_geometry_partial(self, p0, p1):
+        torch = _torch()
+        self.ctx.node_geometry_range(p0, p1)
+        return self.ctx.device_array("node_geo", torch.float64, self.num_nodes * 8).view(self.num_nodes, 8)
+
+    def set_node_geometry(self, geo):
+        pass  # combined in place in the context's array
+
+    # -- (7) halo
+    def halo_flags(self, bp: BuildParams, sc0, sc1, max_h):
+        torch = _torch()
+        nj = self.ctx.halo_mark(bp, sc0, sc1)
+        return self.ctx.device_array("halo_flags", torch.uint8, nj)
+
+    def gather_rows(self, idx):
+        torch = _torch()
+        return torch.stack([c[idx] for c in self._cols(self.n_total)], dim=1)
+
+    def scatter_rows(self, idx, rows):
+        for f, c in enumerate(self._cols(self.n_total)):
+            c[idx] = rows[:, f]
+
+    # -- (8) build + pass
+    def build_range(self, bp: BuildParams, sc0, sc1, max_h, download):
+        nsc, nb = self.ctx.build_store_range(bp, sc0, sc1, max_h)
+        if not download:
+            return None
+        return self.ctx.get_store(bp, self.n_total, nsc, nb)
+
+    def reduce(self, kernel: Kernel, cfg: PassConfig, nloc, download):
+        return self.ctx.reduce(kernel, cfg, nloc, download=download)
+
+
+class DomainDecomposition:
+    """The distributed build-and-query step (module docstring)."""
+
+    def __init__(self, engine, comm: Comm, bp: BuildParams, kernels: Sequence[Kernel], cfg: PassConfig,
+                 bucket=64):
+        self.E, self.comm, self.bp = engine, comm, bp
+        self.kernels = list(kernels)
+        self.cfg = cfg
+        self.bucket = bucket
+
+    def _ctx_stream(self):
+        s = getattr(self.E, "stream", None)
+        if s is None:
+            import contextlib
+            return contextlib.nullcontext()
+        return _torch().cuda.stream(s)
+
+    def run(self, download=True) -> RankResult:
+        with self._ctx_stream():
+            return self._run(download)
+
+    def _run(self, download):
+        torch = _torch()
+        E, comm = self.E, self.comm
+        P, r = comm.world, comm.rank
+        dev = E.device
+        # (1) local keys
+        keys = E.local_sort()
+        n_l = int(keys.numel())
+        counts = comm.all_gather(torch.tensor([n_l], dtype=torch.int64, device=dev)).view(-1).tolist()
+        N = int(sum(counts))
+        scb, pb = sc_partition(N, P)
+        # (2) exact split at the interior bounds
+        cut = torch.zeros((P, P + 1), dtype=torch.int64, device=dev)
+        if P > 1:
+            tgt = torch.tensor(pb[1:-1], dtype=torch.int64, device=dev)
+            lo = torch.zeros(P - 1, dtype=torch.int64, device=dev)
+            hi = torch.full((P - 1,), KEY_SPAN - 1, dtype=torch.int64, device=dev)
+            for _ in range(64):  # smallest K with #(key <= K) > t, fixed trip count (no host sync)
+                mid = lo + (hi - lo) // 2
+                c = torch.searchsorted(keys, mid, right=True)
+                comm.allreduce_(c, "sum")
+                ok = c > tgt
+                hi = torch.where(ok, mid, hi)
+                lo = torch.where(ok, lo, mid + 1)
+            less = torch.searchsorted(keys, lo, right=False)
+            eq = torch.searchsorted(keys, lo, right=True) - less
+            less_all = comm.all_gather(less)  # [P, P-1]
+            eq_all = comm.all_gather(eq)
+            need = tgt - less_all.sum(0)
+            eq_before = torch.cumsum(eq_all, 0) - eq_all
+            take = torch.minimum(torch.clamp(need.unsqueeze(0) - eq_before, min=0), eq_all)
+            cut[:, 1:P] = less_all + take
+        cut[:, P] = torch.tensor(counts, dtype=torch.int64, device=dev)
+        cut_h = cut.cpu().numpy()
+        send = np.diff(cut_h[r]).tolist()
+        recv = [int(cut_h[s, r + 1] - cut_h[s, r]) for s in range(P)]
+        # (3) payload to owners
+        moved = comm.all_to_all_v(E.payload(), send, recv)
+        # (4) owners place their particles at global positions [p0, p1)
+        p0, p1 = pb[r], pb[r + 1]
+        assert moved.shape[0] == p1 - p0, "distributed split lost particles"
+        own_keys = E.own(moved, N, p0)
+        # (5) global keys -> global octree
+        gkeys = comm.all_gather_v(own_keys, [pb[q + 1] - pb[q] for q in range(P)])
+        nn = E.octree(gkeys, self.bucket)
+        # (6) node geometry: partial over owned particles, exact MIN all-reduce
+        geo = E.node_geometry_partial(p0, p1)
+        geo[:, 3:7].neg_()
+        comm.allreduce_(geo, "min")
+        geo[:, 3:7].neg_()
+        E.set_node_geometry(geo)
+        max_h = float(geo[0, 6]) if nn else 0.0  # root max h = max over all particles
+        # (7) halo exchange
+        sc0, sc1 = scb[r], scb[r + 1]
+        halo = 0
+        if P > 1:
+            cj = self.bp.params.cj
+            flags = E.halo_flags(self.bp, sc0, sc1, max_h)
+            jc = torch.nonzero(flags).view(-1).to(torch.int64)
+            first = jc * cj
+            jc = jc[(first < p0) | (first >= p1)]
+            bounds = torch.tensor(pb[1:], dtype=torch.int64, device=dev)
+            owner = torch.searchsorted(bounds, jc * cj, right=True)
+            req = torch.bincount(owner, minlength=P)
+            req_all = comm.all_gather(req).cpu().numpy()  # [P, P]: req_all[s, q] = s asks q
+            send_req = req_all[r].tolist()
+            recv_req = req_all[:, r].tolist()
+            asked = comm.all_to_all_v(jc, send_req, recv_req)
+            lane = torch.arange(cj, dtype=torch.int64, device=dev)
+            aidx = (asked.unsqueeze(1) * cj + lane).view(-1).clamp_(max=N - 1)
+            rows = E.gather_rows(aidx)
+            back = comm.all_to_all_v(rows, [v * cj for v in recv_req], [v * cj for v in send_req])
+            widx = (jc.unsqueeze(1) * cj + lane).view(-1)
+            keep = widx < N
+            E.scatter_rows(widx[keep], back[keep])
+            halo = int(keep.sum())
+        # (8) range build + pass
+        store = E.build_range(self.bp, sc0, sc1, max_h, download)
+        results = [E.reduce(k, self.cfg, p1 - p0, download) for k in self.kernels]
+        return RankResult(r, N, p0, p1, sc0, sc1, nn, halo, store, results)
+
+
+def merge_stores(parts: Sequence[NeighborStore]) -> NeighborStore:
+    """Concatenate per-rank range stores (rank order) into the single-domain layout."""
+    counts = np.concatenate([p.counts for p in parts])
+    blobs, offs, base = [], [], 0
+    for p in parts:
+        offs.append(np.asarray(p.offsets[:-1], np.uint64) + np.uint64(base))
+        blobs.append(np.asarray(p.blob, np.uint8))
+        base += len(p.blob)
+    offs.append(np.array([base], np.uint64))
+    return NeighborStore(parts[0].build, parts[0].n, counts, np.concatenate(offs), np.concatenate(blobs))
