@@ -43,7 +43,7 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--n", type=int, default=1 << 26)
+    p.add_argument("--particles", "--n", dest="n", type=int, default=1 << 26)  # per GPU
     p.add_argument("--target", type=float, default=200.0)
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--cpu-sample", type=int, default=1 << 20)
@@ -58,8 +58,10 @@ def dist_init(args):
     if ws > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
         backend = os.environ.get("SFCNL_BENCH_BACKEND", "nccl")  # gloo: several ranks on one GPU (testing)
+        if backend != "nccl":
+            local = local % torch.cuda.device_count()
+        torch.cuda.set_device(local)
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:

@@ -771,7 +771,7 @@ int run_halo_mark(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, ui
         }
     }
     c->jflags_valid = true;
-    c->jflags_sc0 = sc0, c->jflags_sc1 = sc1;
+    c->jflags_sc0 = sc0, c->jflags_sc1 = sc1, c->jflags_len = nj;
     return 0;
 }
 

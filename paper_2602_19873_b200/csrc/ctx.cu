@@ -537,7 +537,7 @@ int sfcnl_cu_device_array(sfcnl_cu_ctx* c, const char* name, void** ptr, uint64_
     else if (nm == "perm" && c->has_order) b = &c->perm, len = c->order_n * 4;
     else if (nm == "node_geo" && c->has_tree) b = &c->node_geo, len = c->num_nodes * sizeof(Geo);
     else if (nm == "nodes" && c->has_tree) b = &c->nodes, len = c->num_nodes * sizeof(Node);
-    else if (nm == "halo_flags" && c->jflags_valid) b = &c->jflags, len = (c->sorted.n + c->sp.cj - 1) / c->sp.cj;
+    else if (nm == "halo_flags" && c->jflags_valid) b = &c->jflags, len = c->jflags_len;
     else if (nm.rfind("out", 0) == 0 && nm.size() == 4 && nm[3] >= '0' && nm[3] <= '3')
         b = &c->outs[nm[3] - '0'], len = pass_out_count(c) * 8;
     else if (nm == "count") b = &c->ncount, len = pass_out_count(c) * 4;

@@ -119,7 +119,7 @@ struct sfcnl_cu_ctx {
     uint64_t sc_base = 0;  // first (global) super-cluster of the current store
     sfcnl_cu::DBuf jflags;  // halo: u8 per global j-cluster, set by run_halo_mark
     bool jflags_valid = false;
-    uint64_t jflags_sc0 = 0, jflags_sc1 = 0;
+    uint64_t jflags_sc0 = 0, jflags_sc1 = 0, jflags_len = 0;
     sfcnl_cu::DBuf sc_size, sc_scratch_off, scratch, build_ctl, overflow_list, fallback_ws;
 
     // (5) pass

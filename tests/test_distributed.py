@@ -153,7 +153,7 @@ def test_range_build_and_pass_slices_single_gpu():
         assert np.array_equal(st.counts, full.counts[sc0:sc1])
         assert np.array_equal(st.blob, full.blob[b0:b1])
         assert np.array_equal(st.offsets, full.offsets[sc0:sc1 + 1] - full.offsets[sc0])
-        p0, p1 = 64 * sc0, min(64 * sc1, sps.size())
+        p0, p1 = min(64 * sc0, sps.size()), min(64 * sc1, sps.size())
         for c, r in zip(cfgs, ref):
             got = ctx.reduce(sfcnl.sph_density_kernel(), c, p1 - p0)
             assert np.array_equal(got.neighbor_count, r.neighbor_count[p0:p1])
