@@ -423,7 +423,7 @@ __device__ bool build_sc(const BuildArgs& A, const Workspace& W, uint64_t sc) {
     return true;
 }
 
-__global__ void __launch_bounds__(kBuildThreads, 5) k_build_smem(BuildArgs A, uint64_t sc_begin, uint64_t sc_end) {
+__global__ void __launch_bounds__(kBuildThreads, 5) k_build_smem(const __grid_constant__ BuildArgs A, uint64_t sc_begin, uint64_t sc_end) {
     // region0 is used in turn by the traversal frontier (fa|fb) and the encoder's bytes.
     static_assert(kECap <= 2 * kFCap * 4, "region0 size");
     __shared__ __align__(16) uint32_t region0[2 * kFCap];
@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(kBuildThreads, 5) k_build_smem(BuildArgs A, ui
     }
 }
 
-__global__ void __launch_bounds__(kBuildThreads) k_build_global(BuildArgs A, const uint32_t* list,
+__global__ void __launch_bounds__(kBuildThreads) k_build_global(const __grid_constant__ BuildArgs A, const uint32_t* list,
                                                                  uint64_t count, uint8_t* ws,
                                                                  uint64_t ws_stride, uint32_t fcap,
                                                                  uint32_t ccap, uint32_t ecap) {
@@ -495,7 +495,7 @@ __device__ bool halo_sc(const BuildArgs& A, const Workspace& W, uint64_t sc, uin
     return true;
 }
 
-__global__ void __launch_bounds__(kBuildThreads) k_halo_smem(BuildArgs A, uint64_t sc_begin, uint64_t sc_end,
+__global__ void __launch_bounds__(kBuildThreads) k_halo_smem(const __grid_constant__ BuildArgs A, uint64_t sc_begin, uint64_t sc_end,
                                                              uint8_t* jflags) {
     __shared__ uint32_t front[2 * kFCap];
     const Workspace W{front, front + kFCap, nullptr, nullptr, nullptr, kFCap, 0, 0, false};
@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_halo_smem(BuildArgs A, uint64
     }
 }
 
-__global__ void __launch_bounds__(kBuildThreads) k_halo_global(BuildArgs A, const uint32_t* list, uint64_t count,
+__global__ void __launch_bounds__(kBuildThreads) k_halo_global(const __grid_constant__ BuildArgs A, const uint32_t* list, uint64_t count,
                                                                uint32_t* ws, uint32_t fcap, uint8_t* jflags) {
     uint32_t* base = ws + uint64_t(blockIdx.x) * 2 * fcap;
     const Workspace W{base, base + fcap, nullptr, nullptr, nullptr, fcap, 0, 0, false};

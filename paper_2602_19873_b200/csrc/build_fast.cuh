@@ -27,7 +27,7 @@ __device__ bool fast_masks(const BuildArgs& A, const Workspace& W, uint32_t nC, 
     __shared__ float s_jab[kCh][6];
     __shared__ unsigned s_pm[8][kCh / 32];  // prefilter survivors per i-cluster
     __shared__ unsigned s_self[kCh / 32];
-    __shared__ uint32_t s_cm[kCh];
+    __shared__ unsigned s_hit[8][kCh / 32];  // pair-test hits per i-cluster
     __shared__ uint32_t s_cand[kCh];
     __shared__ float s_ix[64], s_iy[64], s_iz[64], s_lo[64], s_hi[64];
     __shared__ float s_iab[8][6];
@@ -92,7 +92,7 @@ __device__ bool fast_masks(const BuildArgs& A, const Workspace& W, uint32_t nC, 
     for (uint32_t c0 = 0; c0 < nC; c0 += kCh) {
         const uint32_t nc = tmin<uint32_t>(kCh, nC - c0);
         __syncthreads();  // previous chunk fully consumed
-        for (uint32_t c = tid; c < nc; c += blockDim.x) s_cand[c] = W.cand[c0 + c], s_cm[c] = 0;
+        for (uint32_t c = tid; c < nc; c += blockDim.x) s_cand[c] = W.cand[c0 + c];
         __syncthreads();
         float emax = 0.f;
         for (uint32_t t = tid; t < nc * 8; t += blockDim.x) {
@@ -169,53 +169,80 @@ __device__ bool fast_masks(const BuildArgs& A, const Workspace& W, uint32_t nC, 
         }
         __syncthreads();
         // warp owns i-clusters b = warp, warp + nwarp, ...: its 8 particles stay in
-        // registers while it walks the candidates of its bitmask; lane = (i, j-quarter)
+        // registers while it walks the candidates of its bitmask; lane = (i, j-quarter).
+        // Hits collect in a register bitmask per 32 candidates (no smem atomics);
+        // candidates that overlap the SC's own particles (i == j possible) take a
+        // separate loop so the main loop carries no self test.
         for (uint32_t b = warp; b < nicl; b += nwarp) {
             const uint32_t li = b * 8 + il;
             const float xi = s_ix[li], yi = s_iy[li], zi = s_iz[li];
             const f2 xi2 = f2p(xi, xi), yi2 = f2p(yi, yi), zi2 = f2p(zi, zi);
             const float lo = s_lo[li], hi = s_hi[li];
             for (int half = 0; half < 2; ++half) {
-                unsigned todo = s_pm[b][half];
                 const unsigned self = s_self[half];
-                while (todo) {
-                    const uint32_t c = half * 32 + __ffs(todo) - 1;
-                    todo &= todo - 1;
+                unsigned todo = s_pm[b][half] & ~self;
+                unsigned hits = 0;
+                auto d2pair = [&](uint32_t c, float& d2a, float& d2b) {
                     const ulonglong2 P0 = reinterpret_cast<const ulonglong2*>(s_st)[c * 8 + jq * 2];
                     const f2 Pz = reinterpret_cast<const f2*>(s_st)[c * 16 + jq * 4 + 2];
                     const f2 dx = f2sub(xi2, P0.x);
                     const f2 dy = f2sub(yi2, P0.y);
                     const f2 dz = f2sub(zi2, Pz);
-                    float d2a, d2b;
                     f2u(f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx))), d2a, d2b);
-                    bool sa = false, sb = false;
-                    if ((self >> (c & 31)) & 1u) {
-                        const int jl0 = int(s_cand[c]) * int(cj) - int(p0);
-                        sa = jl0 + int(jq) == int(li), sb = jl0 + int(jq) + 4 == int(li);
+                };
+                // guard-band pairs: the reference's fp64 predicates decide
+                auto band = [&](uint32_t c, float d2a, float d2b, bool sa, bool sb) {
+                    const bool band_a = !sa && !(d2a > hi), band_b = !sb && !(d2b > hi);
+                    if (!__any_sync(0xffffffffu, band_a || band_b)) return false;
+                    bool ex = false;
+                    const uint64_t jb = uint64_t(s_cand[c]) * cj;
+                    if (band_a) ex = exact_hit(A, s_x[li], s_y[li], s_z[li], s_h[li], jb + jq);
+                    if (band_b && !ex) ex = exact_hit(A, s_x[li], s_y[li], s_z[li], s_h[li], jb + jq + 4);
+                    if (!__any_sync(0xffffffffu, ex)) return false;
+                    // the reference prefilter must pass too (neighbor_build.cpp:136-138)
+                    const double pr = dmul(A.scale, s_igeo[b].maxh);
+                    return !(aabb_dist_sq(s_igeo[b], A.jgeo[s_cand[c]], A.box) > dmul(pr, pr));
+                };
+                while (todo) {
+                    const uint32_t ca = __ffs(todo) - 1;
+                    todo &= todo - 1;
+                    float a0, a1;
+                    d2pair(half * 32 + ca, a0, a1);
+                    if (todo) {  // two candidates in flight
+                        const uint32_t cb = __ffs(todo) - 1;
+                        todo &= todo - 1;
+                        float b0, b1;
+                        d2pair(half * 32 + cb, b0, b1);
+                        const unsigned va = __ballot_sync(0xffffffffu, fminf(a0, a1) < lo);
+                        const unsigned vb = __ballot_sync(0xffffffffu, fminf(b0, b1) < lo);
+                        if (va || band(half * 32 + ca, a0, a1, false, false)) hits |= 1u << ca;
+                        if (vb || band(half * 32 + cb, b0, b1, false, false)) hits |= 1u << cb;
+                    } else {
+                        if (__any_sync(0xffffffffu, fminf(a0, a1) < lo) || band(half * 32 + ca, a0, a1, false, false))
+                            hits |= 1u << ca;
                     }
-                    const bool clear = (d2a < lo && !sa) || (d2b < lo && !sb);
-                    bool hit = __any_sync(0xffffffffu, clear);
-                    if (!hit) {
-                        const bool band_a = !sa && !(d2a < lo) && !(d2a > hi);
-                        const bool band_b = !sb && !(d2b < lo) && !(d2b > hi);
-                        if (__any_sync(0xffffffffu, band_a || band_b)) {
-                            bool ex = false;
-                            const uint64_t jb = uint64_t(s_cand[c]) * cj;
-                            if (band_a) ex = exact_hit(A, s_x[li], s_y[li], s_z[li], s_h[li], jb + jq);
-                            if (band_b && !ex) ex = exact_hit(A, s_x[li], s_y[li], s_z[li], s_h[li], jb + jq + 4);
-                            if (__any_sync(0xffffffffu, ex)) {
-                                // the reference prefilter must pass too (neighbor_build.cpp:136-138)
-                                const double pr = dmul(A.scale, s_igeo[b].maxh);
-                                hit = !(aabb_dist_sq(s_igeo[b], A.jgeo[s_cand[c]], A.box) > dmul(pr, pr));
-                            }
-                        }
-                    }
-                    if (hit && lane == 0) atomicOr(&s_cm[c], 1u << b);
                 }
+                unsigned todo_self = s_pm[b][half] & self;
+                while (todo_self) {
+                    const uint32_t cs = __ffs(todo_self) - 1;
+                    todo_self &= todo_self - 1;
+                    const uint32_t c = half * 32 + cs;
+                    float d2a, d2b;
+                    d2pair(c, d2a, d2b);
+                    const int jl0 = int(s_cand[c]) * int(cj) - int(p0);
+                    const bool sa = jl0 + int(jq) == int(li), sb = jl0 + int(jq) + 4 == int(li);
+                    const bool clear = (d2a < lo && !sa) || (d2b < lo && !sb);
+                    if (__any_sync(0xffffffffu, clear) || band(c, d2a, d2b, sa, sb)) hits |= 1u << cs;
+                }
+                if (lane == 0) s_hit[b][half] = hits;
             }
         }
         __syncthreads();
-        for (uint32_t c = tid; c < nc; c += blockDim.x) W.cmask[c0 + c] = s_cm[c];
+        for (uint32_t c = tid; c < nc; c += blockDim.x) {
+            uint32_t m = 0;
+            for (uint32_t b = 0; b < nicl; ++b) m |= ((s_hit[b][c >> 5] >> (c & 31)) & 1u) << b;
+            W.cmask[c0 + c] = m;
+        }
     }
     __syncthreads();
     return true;

@@ -259,7 +259,7 @@ __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& 
                          unsigned long long* s_msk, int* s_len);
 
 template <int K>
-__global__ void __launch_bounds__(kExactThreads) k_pass_exact(PassArgs A) {
+__global__ void __launch_bounds__(kExactThreads) k_pass_exact(const __grid_constant__ PassArgs A) {
     __shared__ uint32_t s_idx[64];
     __shared__ unsigned long long s_msk[64];
     __shared__ int s_len;
@@ -339,7 +339,7 @@ __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& 
 
 // Device-side block-offset index of an uploaded store: warp per SC walks the codec
 // block headers (first kBtab blocks) and records where each block starts.
-__global__ void k_block_table(PassArgs A, uint16_t* btab) {
+__global__ void k_block_table(const __grid_constant__ PassArgs A, uint16_t* btab) {
     __shared__ uint32_t scratch[8][64];
     const uint64_t sc = A.sc_begin + ((blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5);
     if (sc >= A.num_sc) return;

@@ -155,7 +155,7 @@ __device__ bool decode_chunk(const PassArgs& A, uint64_t sc, const ScStream& st,
 }
 
 template <int K, int CJ>
-__global__ void __launch_bounds__(kFastThreads, 3) k_pass_fast(PassArgs A) {
+__global__ void __launch_bounds__(kFastThreads, 3) k_pass_fast(const __grid_constant__ PassArgs A) {
     constexpr bool LJ = (K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB);
     constexpr int NO = nout<K>();
     extern __shared__ __align__(16) unsigned char dsm[];

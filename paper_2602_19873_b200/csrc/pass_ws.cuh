@@ -18,6 +18,11 @@
 constexpr int kWsConsumers = 256, kWsProducers = 128, kWsThreads = kWsConsumers + kWsProducers;
 constexpr int kWsCap = 128;  // entries per chunk (double-buffered)
 
+template <bool B>
+struct BoolC {
+    static constexpr bool value = B;
+};
+
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
@@ -42,7 +47,7 @@ struct WsStage {
 };
 
 template <int K, int CJ>
-__global__ void __launch_bounds__(kWsThreads, 2) k_pass_ws(PassArgs A) {
+__global__ void __launch_bounds__(kWsThreads, 2) k_pass_ws(const __grid_constant__ PassArgs A) {
     constexpr bool LJ = (K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB);
     constexpr int NO = nout<K>();
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -267,8 +272,9 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_pass_ws(PassArgs A) {
             acc0 = acc1 = acc2 = acc3 = 0;
             cnt = 0;
             coincident = false;
-            for (uint32_t k = tid; k < kSC * NO; k += kWsConsumers) (&s_side[0][0])[k] = 0.0;
-            nbar_sync(5, kWsConsumers);
+            // s_side rows of this warp's i-cluster are private to the warp
+            for (uint32_t k = lane; k < 8 * NO; k += 32) (&s_side[warp * 8][0])[k] = 0.0;
+            __syncwarp();
         }
         bad |= bool(M.bad);
         const uint32_t n = M.n;
@@ -282,106 +288,147 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_pass_ws(PassArgs A) {
             }
         }
         if (!bad) {
-            for (uint32_t g = 0; g < n; g += 32) {
-                const bool mb = g + lane < n && ((S.msk[g + lane] >> warp) & 1u);
-                unsigned mine = __ballot_sync(0xffffffffu, mb);
-                while (mine) {
-                    const uint32_t e = g + __ffs(mine) - 1;
-                    mine &= mine - 1;
-                    const ulonglong2 P0 = reinterpret_cast<const ulonglong2*>(S.sj)[e * 8 + jq * 2];
-                    const ulonglong2 P1 = reinterpret_cast<const ulonglong2*>(S.sj)[e * 8 + jq * 2 + 1];
-                    f2 dx = f2sub(xi2, P0.x);
-                    f2 dy = f2sub(yi2, P0.y);
-                    f2 dz = f2sub(zi2, P1.x);
-                    if (LJ) {
-                        const ulonglong2 L0 = reinterpret_cast<const ulonglong2*>(S.sl)[e * 8 + jq * 2];
-                        const ulonglong2 L1 = reinterpret_cast<const ulonglong2*>(S.sl)[e * 8 + jq * 2 + 1];
-                        dx = f2add(dx, f2sub(lxi2, L0.x));
-                        dy = f2add(dy, f2sub(lyi2, L0.y));
-                        dz = f2add(dz, f2sub(lzi2, L1.x));
-                    }
-                    float pma, pmb;
-                    f2u(P1.y, pma, pmb);
-                    float d2a, d2b;
-                    f2u(f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx))), d2a, d2b);
+            // one entry = 8 i x 8 j slots of this warp's i-cluster; lane (i, jq) owns
+            // slots a = jq, b = jq + 4 as packed f32x2
+            struct Ld {
+                f2 dx, dy, dz;
+                float pma, pmb, d2a, d2b;
+            };
+            auto load = [&](uint32_t e) {
+                Ld L;
+                const ulonglong2 P0 = reinterpret_cast<const ulonglong2*>(S.sj)[e * 8 + jq * 2];
+                const ulonglong2 P1 = reinterpret_cast<const ulonglong2*>(S.sj)[e * 8 + jq * 2 + 1];
+                L.dx = f2sub(xi2, P0.x);
+                L.dy = f2sub(yi2, P0.y);
+                L.dz = f2sub(zi2, P1.x);
+                if (LJ) {
+                    const ulonglong2 L0 = reinterpret_cast<const ulonglong2*>(S.sl)[e * 8 + jq * 2];
+                    const ulonglong2 L1 = reinterpret_cast<const ulonglong2*>(S.sl)[e * 8 + jq * 2 + 1];
+                    L.dx = f2add(L.dx, f2sub(lxi2, L0.x));
+                    L.dy = f2add(L.dy, f2sub(lyi2, L0.y));
+                    L.dz = f2add(L.dz, f2sub(lzi2, L1.x));
+                }
+                f2u(P1.y, L.pma, L.pmb);
+                f2u(f2fma(L.dz, L.dz, f2fma(L.dy, L.dy, f2mul(L.dx, L.dx))), L.d2a, L.d2b);
+                return L;
+            };
+            // kSelf: the entry's j-cluster overlaps the SC's own particles (i == j
+            // possible); kUnsafe: periodic images ambiguous, every slot exact
+            auto compute = [&](uint32_t e, const Ld& L, auto SELF, auto UNSAFE) {
+                constexpr bool kSelf = decltype(SELF)::value, kUnsafe = decltype(UNSAFE)::value;
+                bool self_a = false, self_b = false;
+                if (kSelf) {
                     const int jl0 = int(S.idx[e]) * CJ - int(p0);
-                    bool self_a = false, self_b = false;
-                    if (jl0 >= -7 && jl0 < kSC) {
-                        self_a = jl0 + int(jq) == i_local;
-                        self_b = CJ == 8 && jl0 + int(jq) + 4 == i_local;
+                    self_a = jl0 + int(jq) == i_local;
+                    self_b = CJ == 8 && jl0 + int(jq) + 4 == i_local;
+                }
+                bool in_a, in_b, rare_a, rare_b;
+                if (kUnsafe) {
+                    in_a = in_b = false;
+                    rare_a = !self_a;
+                    rare_b = CJ == 8 && !self_b;
+                } else {
+                    in_a = L.d2a < lo && !self_a, in_b = L.d2b < lo && !self_b;
+                    rare_a = !in_a && !(L.d2a > hi_t) && !self_a;
+                    rare_b = !in_b && !(L.d2b > hi_t) && !self_b;
+                }
+                if (LJ) {
+                    rare_a = rare_a || (in_a && L.d2a < close2);
+                    rare_b = rare_b || (in_b && L.d2b < close2);
+                    in_a = in_a && !(L.d2a < close2);
+                    in_b = in_b && !(L.d2b < close2);
+                }
+                if (rare_a | rare_b) {
+                    double* side = &s_side[i_local][0];
+                    const uint64_t jb = uint64_t(S.idx[e]) * CJ;
+                    if (rare_a && jb + jq < A.n) {
+                        const int rc = rare_slot<K>(A, i, jb + jq, r2, side);
+                        cnt += rc > 0, coincident |= rc < 0;
                     }
-                    bool in_a = d2a < lo && !self_a, in_b = d2b < lo && !self_b;
-                    bool rare_a = !in_a && !(d2a > hi_t) && !self_a;
-                    bool rare_b = !in_b && !(d2b > hi_t) && !self_b;
-                    if (unsafe) {  // staged images may be wrong: every slot takes the exact path
-                        in_a = in_b = false;
-                        rare_a = !self_a;
-                        rare_b = CJ == 8 && !self_b;
+                    if (rare_b && jb + jq + 4 < A.n) {
+                        const int rc = rare_slot<K>(A, i, jb + jq + 4, r2, side);
+                        cnt += rc > 0, coincident |= rc < 0;
                     }
-                    if (LJ) {
-                        rare_a = rare_a || (in_a && d2a < close2);
-                        rare_b = rare_b || (in_b && d2b < close2);
-                        in_a = in_a && !(d2a < close2);
-                        in_b = in_b && !(d2b < close2);
-                    }
-                    if (rare_a | rare_b) {
-                        double* side = &s_side[i_local][0];
+                }
+                cnt += uint32_t(in_a) + uint32_t(in_b);
+                if (K == SFCNL_KERNEL_DENSITY) {
+                    // cubic spline W(q)/sigma = 2 max(1-q,0)^3 - 8 max(1/2-q,0)^3
+                    // (= 1 + 6q^2(q-1) for q <= 1/2, 2(1-q)^3 for 1/2 < q <= 1)
+                    const f2 q = f2mul(f2p(sqrt_ftz(L.d2a), sqrt_ftz(L.d2b)), invh2);
+                    float q0, q1;
+                    f2u(q, q0, q1);
+                    const f2 t = f2p(fmaxf(1.f - q0, 0.f), fmaxf(1.f - q1, 0.f));
+                    const f2 u = f2p(fmaxf(0.5f - q0, 0.f), fmaxf(0.5f - q1, 0.f));
+                    const f2 t3 = f2mul(f2mul(t, t), t), u3 = f2mul(f2mul(u, u), u);
+                    const f2 wv = f2fma(f2p(-8.f, -8.f), u3, f2mul(f2p(2.f, 2.f), t3));
+                    acc0 = f2fma(f2p(in_a ? L.pma : 0.f, in_b ? L.pmb : 0.f), wv, acc0);
+                } else if (LJ) {
+                    const f2 inv2 = f2p(in_a ? rcp_ftz(L.d2a) : 0.f, in_b ? rcp_ftz(L.d2b) : 0.f);
+                    const f2 s2 = f2mul(f2p(sig2, sig2), inv2);
+                    const f2 s6 = f2mul(f2mul(s2, s2), s2);
+                    const f2 coef = f2mul(f2mul(f2mul(f2p(eps24, eps24), inv2), s6),
+                                          f2fma(f2p(2.f, 2.f), s6, f2p(-1.f, -1.f)));
+                    f2 ee = f2mul(f2mul(f2p(eps4, eps4), s6), f2sub(s6, f2p(1.f, 1.f)));
+                    f2 cf = coef;
+                    if (K == SFCNL_KERNEL_LJ_COULOMB) {
                         const uint64_t jb = uint64_t(S.idx[e]) * CJ;
-                        if (rare_a && jb + jq < A.n) {
-                            const int rc = rare_slot<K>(A, i, jb + jq, r2, side);
-                            cnt += rc > 0, coincident |= rc < 0;
-                        }
-                        if (rare_b && jb + jq + 4 < A.n) {
-                            const int rc = rare_slot<K>(A, i, jb + jq + 4, r2, side);
-                            cnt += rc > 0, coincident |= rc < 0;
-                        }
+                        const float qi = float(A.ck * A.q[i]);
+                        const float qa = in_a ? qi * float(A.q[jb + jq]) : 0.f;
+                        const float qb = (CJ == 8 && in_b) ? qi * float(A.q[jb + jq + 4]) : 0.f;
+                        float ra, rb;
+                        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(L.d2a));
+                        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rb) : "f"(L.d2b));
+                        const f2 qr = f2mul(f2p(qa, qb), f2p(ra, rb));
+                        ee = f2add(ee, qr);
+                        cf = f2fma(qr, inv2, cf);
                     }
-                    cnt += uint32_t(in_a) + uint32_t(in_b);
-                    if (K == SFCNL_KERNEL_DENSITY) {
-                        const f2 q = f2mul(f2p(sqrt_ftz(d2a), sqrt_ftz(d2b)), invh2);
-                        const f2 q2 = f2mul(q, q);
-                        const f2 wa = f2fma(f2mul(f2p(6.f, 6.f), q2), f2sub(q, f2p(1.f, 1.f)), f2p(1.f, 1.f));
-                        float q0, q1;
-                        f2u(q, q0, q1);
-                        const f2 t = f2p(fmaxf(1.f - q0, 0.f), fmaxf(1.f - q1, 0.f));
-                        const f2 wb = f2mul(f2mul(f2p(2.f, 2.f), t), f2mul(t, t));
-                        float wa0, wa1, wb0, wb1;
-                        f2u(wa, wa0, wa1);
-                        f2u(wb, wb0, wb1);
-                        const f2 wv = f2p(q0 <= 0.5f ? wa0 : wb0, q1 <= 0.5f ? wa1 : wb1);
-                        acc0 = f2fma(f2p(in_a ? pma : 0.f, in_b ? pmb : 0.f), wv, acc0);
-                    } else if (LJ) {
-                        const f2 inv2 = f2p(in_a ? rcp_ftz(d2a) : 0.f, in_b ? rcp_ftz(d2b) : 0.f);
-                        const f2 s2 = f2mul(f2p(sig2, sig2), inv2);
-                        const f2 s6 = f2mul(f2mul(s2, s2), s2);
-                        const f2 coef = f2mul(f2mul(f2mul(f2p(eps24, eps24), inv2), s6),
-                                              f2fma(f2p(2.f, 2.f), s6, f2p(-1.f, -1.f)));
-                        f2 ee = f2mul(f2mul(f2p(eps4, eps4), s6), f2sub(s6, f2p(1.f, 1.f)));
-                        f2 cf = coef;
-                        if (K == SFCNL_KERNEL_LJ_COULOMB) {
-                            const uint64_t jb = uint64_t(S.idx[e]) * CJ;
-                            const float qi = float(A.ck * A.q[i]);
-                            const float qa = in_a ? qi * float(A.q[jb + jq]) : 0.f;
-                            const float qb = (CJ == 8 && in_b) ? qi * float(A.q[jb + jq + 4]) : 0.f;
-                            float ra, rb;
-                            asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(d2a));
-                            asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rb) : "f"(d2b));
-                            const f2 qr = f2mul(f2p(qa, qb), f2p(ra, rb));
-                            ee = f2add(ee, qr);
-                            cf = f2fma(qr, inv2, cf);
-                        }
-                        acc0 = f2fma(cf, dx, acc0);
-                        acc1 = f2fma(cf, dy, acc1);
-                        acc2 = f2fma(cf, dz, acc2);
-                        acc3 = f2add(acc3, ee);
+                    acc0 = f2fma(cf, L.dx, acc0);
+                    acc1 = f2fma(cf, L.dy, acc1);
+                    acc2 = f2fma(cf, L.dz, acc2);
+                    acc3 = f2add(acc3, ee);
+                }
+            };
+            const int self_lo = int(p0) - (CJ - 1);  // j-clusters overlapping [p0, p0 + 64)
+            for (uint32_t g = 0; g < n; g += 32) {
+                const bool have = g + lane < n;
+                const bool mb = have && ((S.msk[g + lane] >> warp) & 1u);
+                const int jf = have ? int(S.idx[g + lane]) * CJ - self_lo : -1;
+                const unsigned selfm = __ballot_sync(0xffffffffu, jf >= 0 && jf < kSC + CJ - 1);
+                unsigned mine = __ballot_sync(0xffffffffu, mb);
+                if (unsafe) {
+                    while (mine) {
+                        const uint32_t e = g + __ffs(mine) - 1;
+                        mine &= mine - 1;
+                        compute(e, load(e), BoolC<true>(), BoolC<true>());
                     }
+                    continue;
+                }
+                unsigned ms = mine & selfm;
+                mine &= ~selfm;
+                while (mine) {
+                    const uint32_t e1 = g + __ffs(mine) - 1;
+                    mine &= mine - 1;
+                    if (!LJ && mine) {  // two entries in flight (register budget allows it for density)
+                        const uint32_t e2 = g + __ffs(mine) - 1;
+                        mine &= mine - 1;
+                        const Ld L1 = load(e1), L2 = load(e2);
+                        compute(e1, L1, BoolC<false>(), BoolC<false>());
+                        compute(e2, L2, BoolC<false>(), BoolC<false>());
+                    } else {
+                        compute(e1, load(e1), BoolC<false>(), BoolC<false>());
+                    }
+                }
+                while (ms) {
+                    const uint32_t e = g + __ffs(ms) - 1;
+                    ms &= ms - 1;
+                    compute(e, load(e), BoolC<true>(), BoolC<false>());
                 }
             }
         }
         const bool last = M.last;
         const uint64_t sc = M.sc;
         if (last) {
-            nbar_sync(5, kWsConsumers);  // s_side complete
+            __syncwarp();  // this warp's s_side rows complete
             if (coincident) raise_error(A.err, sc, SFCNL_INPUT_ERROR, kMsgCoincident, 0);
             double tot[4];
             const f2 accs[4] = {acc0, acc1, acc2, acc3};
