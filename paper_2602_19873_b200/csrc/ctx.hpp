@@ -124,6 +124,7 @@ struct sfcnl_cu_ctx {
 
     // (5) pass
     sfcnl_cu::DBuf outs[4], ncount, jstage;
+    sfcnl_cu::DBuf work_ctr;  // dynamic work counter of the warp-per-SC kernels
 
     // errors
     sfcnl_cu::DBuf derr;  // DevError

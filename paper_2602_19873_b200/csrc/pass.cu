@@ -28,6 +28,7 @@
 //   neighbor_count (the pair set) is exact. Contributions accumulate in fp32 per
 //   lane and are combined in fp64.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "ctx.hpp"
@@ -52,6 +53,7 @@ struct PassArgs {
     const double* m;
     const double* q;
     double qs, eps, sigma, ck;
+    float lj_close2;  // LJ pairs with d2 < lj_close2 * sigma^2 take the fp64 path
     double* out[4];
     uint32_t* cnt;
     DevError* err;
@@ -336,6 +338,7 @@ __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& 
 
 #include "pass_fast.cuh"
 #include "pass_ws.cuh"
+#include "pass_warp.cuh"
 
 // Device-side block-offset index of an uploaded store: warp per SC walks the codec
 // block headers (first kBtab blocks) and records where each block starts.
@@ -362,19 +365,29 @@ __global__ void k_block_table(const __grid_constant__ PassArgs A, uint16_t* btab
     }
 }
 
+template <int K, int CJ>
+void launch_pass_warp(sfcnl_cu_ctx* c, const PassArgs& A) {
+    const size_t smem = pw_smem<K>();
+    cudaFuncSetAttribute(k_pass_warp<K, CJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass_warp<K, CJ>, kPwWarps * 32, smem);
+    const uint64_t warps = A.num_sc - A.sc_begin;
+    const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((warps + kPwWarps - 1) / kPwWarps,
+                                                                            uint64_t(c->num_sms) * std::max(per_sm, 1))));
+    cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream);
+    launch(c, k_pass_warp<K, CJ>, dim3(grid), dim3(kPwWarps * 32), smem, A, c->work_ctr.as<unsigned long long>());
+}
+
 template <int K>
 void launch_pass(sfcnl_cu_ctx* c, const PassArgs& A, bool fast) {
-    if (fast) {
+    if (fast && getenv("SFCNL_PASS_WS")) {
         const unsigned grid = unsigned(std::min<uint64_t>(A.num_sc - A.sc_begin, uint64_t(c->num_sms) * 2));
-        if (A.cj == 8) {
-            const size_t smem = ws_smem<K, 8>();
-            cudaFuncSetAttribute(k_pass_ws<K, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            launch(c, k_pass_ws<K, 8>, dim3(grid), dim3(kWsThreads), smem, A);
-        } else {
-            const size_t smem = ws_smem<K, 4>();
-            cudaFuncSetAttribute(k_pass_ws<K, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            launch(c, k_pass_ws<K, 4>, dim3(grid), dim3(kWsThreads), smem, A);
-        }
+        const size_t smem = ws_smem<K, 8>();
+        cudaFuncSetAttribute(k_pass_ws<K, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        launch(c, k_pass_ws<K, 8>, dim3(grid), dim3(kWsThreads), smem, A);
+    } else if (fast) {
+        if (A.cj == 8) launch_pass_warp<K, 8>(c, A);
+        else launch_pass_warp<K, 4>(c, A);
     } else {
         const unsigned grid = unsigned(std::min<uint64_t>(A.num_sc - A.sc_begin, uint64_t(c->num_sms) * 32));
         launch(c, k_pass_exact<K>, dim3(grid), dim3(kExactThreads), 0, A);
@@ -420,6 +433,7 @@ int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p) {
         SFCNL_CUDA_TRY(cudaMemsetAsync(c->ncount.p, 0, nout * 4, c->stream));
     }
     SFCNL_CUDA_TRY(cudaMemsetAsync(c->derr.p, 0xff, sizeof(DevError), c->stream));
+    SFCNL_CUDA_TRY(c->work_ctr.reserve(8));
     A.n = n;
     A.box = c->sorted.box;
     A.ci = c->sp.ci, A.cj = c->sp.cj, A.icl_per_sc = 64 / c->sp.ci, A.mask_bytes = (A.icl_per_sc + 7) / 8;
@@ -440,6 +454,8 @@ int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p) {
     A.x = c->sorted.x.as<double>(), A.y = c->sorted.y.as<double>(), A.z = c->sorted.z.as<double>();
     A.h = c->sorted.h.as<double>();
     A.qs = p.query_scale, A.eps = p.epsilon, A.sigma = p.sigma, A.ck = p.coulomb_k;
+    A.lj_close2 = kLjClose2;
+    if (const char* e = getenv("SFCNL_LJ_CLOSE2")) A.lj_close2 = float(atof(e));
     for (int o = 0; o < 4; ++o) A.out[o] = c->outs[o].as<double>() - p0;
     A.cnt = c->ncount.as<uint32_t>() - p0;
     A.err = c->derr.as<DevError>();

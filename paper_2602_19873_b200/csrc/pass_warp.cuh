@@ -1,0 +1,483 @@
+// Warp-per-super-cluster mixed-precision pass (precision 1, gather, ci == 8,
+// cj in {4, 8}); included by pass.cu after pass_fast.cuh (shares its helpers).
+//
+// Replaces the per-SC entry loop of reduce<Real,K> (reduce.hpp:94-197) for the
+// built-in kernels. Every warp is independent: it takes the next super-cluster
+// (SC) from a global counter and runs the whole SC alone, so the kernel has no
+// block barriers and no producer/consumer hand-over; the warps of an SM hide
+// each other's load latency.
+//
+// Per SC (64 particles, 8 i-clusters b):
+//  * i side: the 64 particles are made relative to the SC's first particle in
+//    fp64 (per-particle minimum image), rounded to fp32 (hi, + lo for LJ) and
+//    kept in the warp's shared-memory slice with r_i and the kernel constants.
+//  * per codec block (w entries, decoded by the warp in order: block mask ballot,
+//    nibble-count scans, difference scan -- codec::decode_into,
+//    nibble_codec.cpp:136-178) and per 32 entries of it:
+//      stage: every j particle once, SC-relative fp32 in the packed-pair layout
+//             {x_a,x_b,y_a,y_b,z_a,z_b,p_a,p_b} per (entry, j-quarter), slots
+//             a = q, b = q + 4, so a lane's two slots load as f32x2 pairs;
+//      compute: for each i-cluster b, the entries whose mask has bit b
+//             (ballot + ffs); lane = (i in cluster b) x (j quarter), two slots
+//             per lane in FFMA2/FADD2/FMUL2; partial sums are reduced over the
+//             four j-quarter lanes and added into per-i fp64 sums in shared
+//             memory once per (block, b).
+//  * cutoff decisions: fp32 with the guard band of pass.cu; band slots (and LJ
+//    pairs closer than kLjClose * sigma, where fp32 could overflow) go through
+//    the reference's fp64 predicate and kernel (rare_slot), so neighbor_count is
+//    exact. SCs whose periodic images are ambiguous in the SC frame ("unsafe")
+//    evaluate every slot that way.
+constexpr int kPwWarps = 8;    // independent warps per CTA
+constexpr int kPwChunk = 32;   // entries staged at a time
+// LJ pairs with d2 < kLjClose2 * sigma^2 are evaluated in fp64 from the staged
+// hi/lo coordinates (in registers): the energy (s6 - 1) and force (2 s6 - 1)
+// factors cross zero at d = sigma and 2^(1/6) sigma, where an fp32 term keeps an
+// absolute error of ~1e-6 * 4 s6 that the 1e-5 * sum_j |E_ij| bar cannot absorb,
+// and fp32 (sigma/d)^12 overflows for d -> 0. Pairs closer than kLjTiny2 * sigma^2
+// (coincidence range) take the reference's fp64 path (rare_slot).
+constexpr float kLjClose2 = 1.5f;
+constexpr float kLjTiny2 = 1e-6f;
+constexpr bool kTwo = false;
+
+template <int K>
+struct PwSmem {
+    static constexpr bool LJ = (K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB);
+    static constexpr int NO = nout<K>();
+    static constexpr int kMinBlocks = LJ ? 2 : 3;  // CTAs per SM (registers: 128 / 85)
+    float sj[kPwChunk * 32];              // hi x,y,z + payload
+    float sl[LJ ? kPwChunk * 32 : 4];     // lo x,y,z (LJ)
+    uint32_t idx[64];                     // decoded block
+    float ix[64], iy[64], iz[64];
+    float ilx[LJ ? 64 : 1], ily[LJ ? 64 : 1], ilz[LJ ? 64 : 1];
+    double ir[64];     // r_i = query_scale * h_i (< 0: inactive)
+    double iscale[64]; // density: 8/(pi h^3) * 2 (the spline's factor 2 folded in)
+    float iinvh[64];   // density: 1 / h_i
+    double acc[64][NO];
+    uint32_t cnt[64];
+};
+
+template <int K>
+constexpr size_t pw_smem() {
+    return size_t(kPwWarps) * sizeof(PwSmem<K>);
+}
+
+__device__ __forceinline__ float warp_fmax(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+template <int K, int CJ>
+__global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_warp(const __grid_constant__ PassArgs A,
+                                                             unsigned long long* __restrict__ work) {
+    constexpr bool LJ = PwSmem<K>::LJ;
+    constexpr int NO = nout<K>();
+    extern __shared__ __align__(16) unsigned char dsm[];
+    PwSmem<K>& S = reinterpret_cast<PwSmem<K>*>(dsm)[threadIdx.x >> 5];
+    const unsigned lane = lane_id();
+    const uint32_t il = lane >> 2, jq = lane & 3;
+    const uint32_t w = uint32_t(A.w);
+    const float sig2 = float(A.sigma * A.sigma);
+    const float eps24 = float(24.0 * A.eps), eps4 = float(4.0 * A.eps);
+    const float close2 = A.lj_close2 * sig2, tiny2 = kLjTiny2 * sig2;
+    const double sig2d = A.sigma * A.sigma, eps24d = 24.0 * A.eps, eps4d = 4.0 * A.eps;
+
+    for (;;) {
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(work, 1ull);
+        const uint64_t sc = A.sc_begin + __shfl_sync(0xffffffffu, t, 0);
+        if (sc >= A.num_sc) break;
+
+        // ---- open the SC's slice (decode_entry_indices, neighbor_store.cpp:18-42)
+        const uint32_t count = A.counts[sc];
+        const uint8_t* rec = nullptr;
+        const uint8_t* idata = nullptr;
+        uint64_t ilen = 0;
+        bool bad = false;
+        if (count) {
+            const uint64_t begin = A.offsets[sc], end = A.offsets[sc + 1];
+            const uint64_t mb = uint64_t(count) * A.mask_bytes;
+            if (begin + mb > end) {
+                if (lane == 0) raise_error(A.err, sc, SFCNL_DECODE_ERROR, kMsgMaskSlice, begin);
+                bad = true;
+            } else {
+                rec = A.blob + begin;
+                idata = rec + mb;
+                ilen = end - begin - mb;
+                if (!A.compress && ilen != uint64_t(count) * 4) {
+                    if (lane == 0) raise_error(A.err, sc, SFCNL_DECODE_ERROR, kMsgRawLen, ilen);
+                    bad = true;
+                }
+            }
+        }
+
+        // ---- i side
+        const uint64_t p0 = sc * kSC;
+        const uint32_t np = uint32_t(tmin<uint64_t>(p0 + kSC, A.n) - p0);
+        const double ox = A.x[p0], oy = A.y[p0], oz = A.z[p0];
+        auto rel = [&](double v, double o, int d) {
+            double r = dsub(v, o);
+            if (A.box.per[d]) {
+                const double L = A.box.len[d];
+                if (r > 0.5 * L) r = dsub(r, L);
+                else if (r < -0.5 * L) r = dadd(r, L);
+            }
+            return r;
+        };
+        float eax = 0.f, eay = 0.f, eaz = 0.f, er = 0.f;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const uint32_t k = lane + 32u * s;
+            float fx = 0.f, fy = 0.f, fz = 0.f;
+            double r = -1.0, hk = 1.0;
+            double qx = 0, qy = 0, qz = 0;
+            if (k < np) {
+                qx = rel(A.x[p0 + k], ox, 0), qy = rel(A.y[p0 + k], oy, 1), qz = rel(A.z[p0 + k], oz, 2);
+                hk = A.h[p0 + k];
+                fx = float(qx), fy = float(qy), fz = float(qz);
+                r = dmul(A.qs, hk);
+                eax = fmaxf(eax, float(fabs(qx))), eay = fmaxf(eay, float(fabs(qy))), eaz = fmaxf(eaz, float(fabs(qz)));
+                er = fmaxf(er, float(r));
+            }
+            S.ix[k] = fx, S.iy[k] = fy, S.iz[k] = fz;
+            if (LJ) S.ilx[k] = float(qx - double(fx)), S.ily[k] = float(qy - double(fy)), S.ilz[k] = float(qz - double(fz));
+            S.ir[k] = r;
+            if (K == SFCNL_KERNEL_DENSITY) S.iscale[k] = 2.0 * (8.0 / (kPi * hk * hk * hk)), S.iinvh[k] = float(1.0 / hk);
+#pragma unroll
+            for (int o = 0; o < NO; ++o) S.acc[k][o] = 0.0;
+            S.cnt[k] = 0;
+        }
+        eax = warp_fmax(eax), eay = warp_fmax(eay), eaz = warp_fmax(eaz), er = warp_fmax(er);
+        // per-particle min-imaging against the SC origin is exact for every in-range
+        // pair when max|rel_i| + max r < L/2 on each periodic axis
+        const bool unsafe = (A.box.per[0] && double(eax) + double(er) >= 0.49 * A.box.len[0]) ||
+                            (A.box.per[1] && double(eay) + double(er) >= 0.49 * A.box.len[1]) ||
+                            (A.box.per[2] && double(eaz) + double(er) >= 0.49 * A.box.len[2]);
+        const float Ei = fmaxf(eax, fmaxf(eay, eaz));
+        __syncwarp();
+
+        bool coincident = false;
+        uint64_t pos = 0, running = 0;
+        const uint32_t nicl = tmin<uint32_t>(8u, uint32_t((np + 7) / 8));
+        for (uint32_t bb = 0; !bad && bb < count; bb += w) {
+            const uint32_t len = tmin<uint32_t>(w, count - bb);
+            // ---- decode one codec block into S.idx[0, len)
+            if (A.compress) {
+                uint64_t off = 0;
+                int msg = 0;
+                const uint64_t np2 = warp_decode_block(idata, ilen, pos, len, int(w), running, S.idx, &off, &msg);
+                if (np2 == ~0ull) {
+                    if (lane == 0) raise_error(A.err, sc, SFCNL_DECODE_ERROR, msg, off);
+                    bad = true;
+                    break;
+                }
+                pos = np2;
+                if (bb + len == count && pos != ilen) {
+                    if (lane == 0) raise_error(A.err, sc, SFCNL_DECODE_ERROR, kMsgTrailing, pos);
+                    bad = true;
+                    break;
+                }
+            } else {
+                for (uint32_t k = lane; k < len; k += 32) {
+                    const uint8_t* p = idata + 4ull * (bb + k);
+                    S.idx[k] = uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16) | (uint32_t(p[3]) << 24);
+                }
+            }
+            __syncwarp();
+            for (uint32_t h0 = 0; h0 < len; h0 += kPwChunk) {
+                const uint32_t n = tmin<uint32_t>(kPwChunk, len - h0);
+                const bool have = lane < n;
+                const uint32_t my_idx = have ? S.idx[h0 + lane] : 0u;
+                const uint32_t my_msk = have ? uint32_t(rec[bb + h0 + lane]) : 0u;
+                // ---- stage the chunk's j particles (8 per lane, 4 loads in flight each)
+                float emax = 0.f;
+                if (!unsafe) {
+                    float* sj = S.sj;
+                    float* sl = S.sl;
+#pragma unroll
+                    for (int k0 = 0; k0 < 8; k0 += 4) {
+                        double vx[4], vy[4], vz[4], vm[4];
+                        bool val[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const uint32_t e = uint32_t(k0 + u) * 4 + (lane >> 3), jj = lane & 7;
+                            const uint32_t ie = __shfl_sync(0xffffffffu, my_idx, e);
+                            const uint64_t j = uint64_t(ie) * CJ + jj;
+                            val[u] = e < n && jj < uint32_t(CJ) && j < A.n;
+                            vx[u] = vy[u] = vz[u] = vm[u] = 0.0;
+                            if (val[u]) {
+                                vx[u] = A.x[j], vy[u] = A.y[j], vz[u] = A.z[j];
+                                if (K == SFCNL_KERNEL_DENSITY) vm[u] = A.m[j];
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const uint32_t e = uint32_t(k0 + u) * 4 + (lane >> 3), jj = lane & 7;
+                            if (e >= n) continue;
+                            const uint32_t o = e * 32 + (jj & 3) * 8 + (jj >> 2);
+                            float fx = kFar, fy = kFar, fz = kFar, fm = 0.f, lx = 0.f, ly = 0.f, lz = 0.f;
+                            if (val[u]) {
+                                const double qx = rel(vx[u], ox, 0), qy = rel(vy[u], oy, 1), qz = rel(vz[u], oz, 2);
+                                fx = float(qx), fy = float(qy), fz = float(qz);
+                                fm = float(vm[u]);
+                                if (LJ) lx = float(qx - double(fx)), ly = float(qy - double(fy)), lz = float(qz - double(fz));
+                                emax = fmaxf(emax, fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz))));
+                            }
+                            if (jj < 4 || CJ == 8) {
+                                sj[o] = fx, sj[o + 2] = fy, sj[o + 4] = fz, sj[o + 6] = fm;
+                                if (LJ) sl[o] = lx, sl[o + 2] = ly, sl[o + 4] = lz;
+                            } else {
+                                // cj == 4: slot b of every quarter is a far dummy
+                                const uint32_t ob = e * 32 + (jj & 3) * 8 + 1;
+                                sj[ob] = kFar, sj[ob + 2] = kFar, sj[ob + 4] = kFar, sj[ob + 6] = 0.f;
+                                if (LJ) sl[ob] = 0.f, sl[ob + 2] = 0.f, sl[ob + 4] = 0.f;
+                            }
+                        }
+                    }
+                }
+                const float E = fmaxf(Ei, warp_fmax(emax));
+                const int self_lo = int(p0) - (CJ - 1);  // j-clusters overlapping [p0, p0 + 64)
+                const int jf = int(my_idx) * CJ - self_lo;
+                const unsigned selfm = __ballot_sync(0xffffffffu, have && jf >= 0 && jf < kSC + CJ - 1);
+                __syncwarp();
+
+                for (uint32_t b = 0; b < nicl; ++b) {
+                    unsigned mine = __ballot_sync(0xffffffffu, (my_msk >> b) & 1u);
+                    if (!mine) continue;
+                    const int li = int(b * 8 + il);
+                    const uint64_t i = p0 + uint64_t(li);
+                    const double r = S.ir[li];
+                    const double r2 = dmul(r, r);
+                    const bool active = r >= 0.0;
+                    uint32_t cnt = 0;
+                    if (unsafe) {
+                        // every slot through the reference predicate + fp64 kernel
+                        double* side = &S.acc[li][0];
+                        while (mine) {
+                            const uint32_t e = __ffs(mine) - 1;
+                            mine &= mine - 1;
+                            const uint64_t jb = uint64_t(__shfl_sync(0xffffffffu, my_idx, e)) * CJ;
+                            if (!active) continue;
+                            if (jb + jq < A.n) {
+                                const int rc = rare_slot<K>(A, i, jb + jq, r2, side);
+                                cnt += rc > 0, coincident |= rc < 0;
+                            }
+                            if (CJ == 8 && jb + jq + 4 < A.n) {
+                                const int rc = rare_slot<K>(A, i, jb + jq + 4, r2, side);
+                                cnt += rc > 0, coincident |= rc < 0;
+                            }
+                        }
+                        cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
+                        cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
+                        __syncwarp();
+                        if (jq == 0) S.cnt[li] += cnt;
+                        __syncwarp();
+                        continue;
+                    }
+                    float lo = -1.f, hi_t = -1.f;
+                    if (active) {
+                        const double ex = 1.1920928955078125e-07 * double(E) + 5.9604644775390625e-08 * r;
+                        const double guard = 4.0 * (1.7881393432617188e-07 * r2 + 3.5 * r * ex + 3.0 * ex * ex) + 1e-300;
+                        lo = __double2float_rd(r2 - guard);
+                        hi_t = __double2float_ru(r2 + guard);
+                    }
+                    const float fxi = S.ix[li], fyi = S.iy[li], fzi = S.iz[li];
+                    const f2 xi2 = f2p(fxi, fxi), yi2 = f2p(fyi, fyi), zi2 = f2p(fzi, fzi);
+                    f2 lxi2 = 0, lyi2 = 0, lzi2 = 0;
+                    if (LJ) {
+                        lxi2 = f2p(S.ilx[li], S.ilx[li]), lyi2 = f2p(S.ily[li], S.ily[li]), lzi2 = f2p(S.ilz[li], S.ilz[li]);
+                    }
+                    float inv_h = 0.f;
+                    if (K == SFCNL_KERNEL_DENSITY) inv_h = S.iinvh[li];
+                    const f2 invh2 = f2p(inv_h, inv_h);
+                    f2 acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+                    double accd0 = 0.0, accd1 = 0.0, accd2 = 0.0, accd3 = 0.0;  // LJ close pairs (fp64)
+
+                    struct Ld {
+                        f2 dx, dy, dz;
+                        float pma, pmb, d2a, d2b;
+                    };
+                    auto load = [&](uint32_t e) {
+                        Ld L;
+                        const ulonglong2 P0 = reinterpret_cast<const ulonglong2*>(S.sj)[e * 8 + jq * 2];
+                        const ulonglong2 P1 = reinterpret_cast<const ulonglong2*>(S.sj)[e * 8 + jq * 2 + 1];
+                        L.dx = f2sub(xi2, P0.x);
+                        L.dy = f2sub(yi2, P0.y);
+                        L.dz = f2sub(zi2, P1.x);
+                        if (LJ) {
+                            const ulonglong2 L0 = reinterpret_cast<const ulonglong2*>(S.sl)[e * 8 + jq * 2];
+                            const ulonglong2 L1 = reinterpret_cast<const ulonglong2*>(S.sl)[e * 8 + jq * 2 + 1];
+                            L.dx = f2add(L.dx, f2sub(lxi2, L0.x));
+                            L.dy = f2add(L.dy, f2sub(lyi2, L0.y));
+                            L.dz = f2add(L.dz, f2sub(lzi2, L1.x));
+                        }
+                        f2u(P1.y, L.pma, L.pmb);
+                        f2u(f2fma(L.dz, L.dz, f2fma(L.dy, L.dy, f2mul(L.dx, L.dx))), L.d2a, L.d2b);
+                        return L;
+                    };
+                    auto compute = [&](uint32_t e, const Ld& L, auto SELF) {
+                        constexpr bool kSelf = decltype(SELF)::value;
+                        bool self_a = false, self_b = false;
+                        if (kSelf) {
+                            const int jl0 = int(__shfl_sync(0xffffffffu, my_idx, e)) * CJ - int(p0);
+                            self_a = jl0 + int(jq) == li;
+                            self_b = CJ == 8 && jl0 + int(jq) + 4 == li;
+                        }
+                        bool in_a = L.d2a < lo && !self_a, in_b = L.d2b < lo && !self_b;
+                        bool rare_a = !in_a && !(L.d2a > hi_t) && !self_a;
+                        bool rare_b = !in_b && !(L.d2b > hi_t) && !self_b;
+                        bool cl_a = false, cl_b = false;
+                        if (LJ) {
+                            rare_a = rare_a || (in_a && L.d2a < tiny2);
+                            rare_b = rare_b || (in_b && L.d2b < tiny2);
+                            in_a = in_a && !(L.d2a < tiny2);
+                            in_b = in_b && !(L.d2b < tiny2);
+                            cl_a = in_a && L.d2a < close2, cl_b = in_b && L.d2b < close2;
+                            in_a = in_a && !cl_a, in_b = in_b && !cl_b;
+                            if (cl_a | cl_b) {
+                                // fp64 from the staged hi/lo coordinates (exact SC-relative values)
+                                const float* pj = S.sj + e * 32 + jq * 8;
+                                const float* pl = S.sl + e * 32 + jq * 8;
+#pragma unroll
+                                for (int sl2 = 0; sl2 < 2; ++sl2) {
+                                    if (!(sl2 ? cl_b : cl_a)) continue;
+                                    const double dx = (double(S.ix[li]) - double(pj[sl2])) + (double(S.ilx[li]) - double(pl[sl2]));
+                                    const double dy = (double(S.iy[li]) - double(pj[2 + sl2])) + (double(S.ily[li]) - double(pl[2 + sl2]));
+                                    const double dz = (double(S.iz[li]) - double(pj[4 + sl2])) + (double(S.ilz[li]) - double(pl[4 + sl2]));
+                                    const double inv2 = 1.0 / (dx * dx + dy * dy + dz * dz);
+                                    const double s2 = sig2d * inv2, s6 = s2 * s2 * s2;
+                                    double coef = eps24d * inv2 * s6 * (2.0 * s6 - 1.0);
+                                    double en = eps4d * s6 * (s6 - 1.0);
+                                    if (K == SFCNL_KERNEL_LJ_COULOMB) {
+                                        const uint64_t jj = uint64_t(S.idx[h0 + e]) * CJ + jq + 4 * sl2;
+                                        const double qq = A.ck * A.q[i] * A.q[jj], ir = sqrt(inv2);
+                                        en += qq * ir;
+                                        coef += qq * ir * inv2;
+                                    }
+                                    accd0 += coef * dx, accd1 += coef * dy, accd2 += coef * dz, accd3 += en;
+                                }
+                                cnt += uint32_t(cl_a) + uint32_t(cl_b);
+                            }
+                        }
+                        if (rare_a | rare_b) {
+                            double* side = &S.acc[li][0];
+                            const uint64_t jb = uint64_t(S.idx[h0 + e]) * CJ;
+                            if (rare_a && jb + jq < A.n) {
+                                const int rc = rare_slot<K>(A, i, jb + jq, r2, side);
+                                cnt += rc > 0, coincident |= rc < 0;
+                            }
+                            if (rare_b && jb + jq + 4 < A.n) {
+                                const int rc = rare_slot<K>(A, i, jb + jq + 4, r2, side);
+                                cnt += rc > 0, coincident |= rc < 0;
+                            }
+                        }
+                        cnt += uint32_t(in_a) + uint32_t(in_b);
+                        if (K == SFCNL_KERNEL_DENSITY) {
+                            // W(q)/(2 sigma) = max(1-q,0)^3 - 4 max(1/2-q,0)^3
+                            const f2 q = f2mul(f2p(sqrt_ftz(L.d2a), sqrt_ftz(L.d2b)), invh2);
+                            const f2 omq = f2sub(f2p(1.f, 1.f), q), hmq = f2sub(f2p(0.5f, 0.5f), q);
+                            float t0, t1, u0, u1;
+                            f2u(omq, t0, t1);
+                            f2u(hmq, u0, u1);
+                            const f2 t = f2p(fmaxf(t0, 0.f), fmaxf(t1, 0.f));
+                            const f2 u = f2p(fmaxf(u0, 0.f), fmaxf(u1, 0.f));
+                            const f2 t3 = f2mul(f2mul(t, t), t), u3 = f2mul(f2mul(u, u), u);
+                            const f2 wv = f2fma(f2p(-4.f, -4.f), u3, t3);
+                            acc0 = f2fma(f2p(in_a ? L.pma : 0.f, in_b ? L.pmb : 0.f), wv, acc0);
+                        } else if (LJ) {
+                            const f2 inv2 = f2p(in_a ? rcp_ftz(L.d2a) : 0.f, in_b ? rcp_ftz(L.d2b) : 0.f);
+                            const f2 s2 = f2mul(f2p(sig2, sig2), inv2);
+                            const f2 s6 = f2mul(f2mul(s2, s2), s2);
+                            const f2 coef = f2mul(f2mul(f2mul(f2p(eps24, eps24), inv2), s6),
+                                                  f2fma(f2p(2.f, 2.f), s6, f2p(-1.f, -1.f)));
+                            f2 ee = f2mul(f2mul(f2p(eps4, eps4), s6), f2sub(s6, f2p(1.f, 1.f)));
+                            f2 cf = coef;
+                            if (K == SFCNL_KERNEL_LJ_COULOMB) {
+                                const uint64_t jb = uint64_t(S.idx[h0 + e]) * CJ;
+                                const float qi = float(A.ck * A.q[i]);
+                                const float qa = in_a ? qi * float(A.q[jb + jq]) : 0.f;
+                                const float qb = (CJ == 8 && in_b) ? qi * float(A.q[jb + jq + 4]) : 0.f;
+                                float ra, rb;
+                                asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(L.d2a));
+                                asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rb) : "f"(L.d2b));
+                                const f2 qr = f2mul(f2p(qa, qb), f2p(ra, rb));
+                                ee = f2add(ee, qr);
+                                cf = f2fma(qr, inv2, cf);
+                            }
+                            acc0 = f2fma(cf, L.dx, acc0);
+                            acc1 = f2fma(cf, L.dy, acc1);
+                            acc2 = f2fma(cf, L.dz, acc2);
+                            acc3 = f2add(acc3, ee);
+                        }
+                    };
+                    unsigned ms = mine & selfm;
+                    mine &= ~selfm;
+                    while (mine) {
+                        const uint32_t e1 = __ffs(mine) - 1;
+                        mine &= mine - 1;
+                        if (kTwo && !LJ && mine) {  // two entries in flight
+                            const uint32_t e2 = __ffs(mine) - 1;
+                            mine &= mine - 1;
+                            const Ld L1 = load(e1), L2 = load(e2);
+                            compute(e1, L1, BoolC<false>());
+                            compute(e2, L2, BoolC<false>());
+                        } else {
+                            compute(e1, load(e1), BoolC<false>());
+                        }
+                    }
+                    while (ms) {
+                        const uint32_t e = __ffs(ms) - 1;
+                        ms &= ms - 1;
+                        compute(e, load(e), BoolC<true>());
+                    }
+                    // flush: pair halves, then the four j-quarter lanes of each i
+                    double tot[NO];
+                    const f2 accs[4] = {acc0, acc1, acc2, acc3};
+                    const double accds[4] = {accd0, accd1, accd2, accd3};
+#pragma unroll
+                    for (int o = 0; o < NO; ++o) {
+                        float a, c;
+                        f2u(accs[o], a, c);
+                        double v = double(a) + double(c) + (LJ ? accds[o] : 0.0);
+                        v += __shfl_xor_sync(0xffffffffu, v, 1);
+                        v += __shfl_xor_sync(0xffffffffu, v, 2);
+                        tot[o] = v;
+                    }
+                    cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
+                    cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
+                    __syncwarp();  // rare-slot side sums of this b are complete
+                    if (jq == 0 && active) {
+                        if (K == SFCNL_KERNEL_DENSITY) {
+                            S.acc[li][0] += S.iscale[li] * tot[0];
+                        } else if (LJ) {
+#pragma unroll
+                            for (int o = 0; o < NO; ++o) S.acc[li][o] += tot[o];
+                        }
+                        S.cnt[li] += cnt;
+                    }
+                    __syncwarp();
+                }
+                __syncwarp();  // the chunk's staging is consumed
+            }
+        }
+        if (coincident) raise_error(A.err, sc, SFCNL_INPUT_ERROR, kMsgCoincident, 0);
+        __syncwarp();
+        if (!bad) {
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const uint32_t k = lane + 32u * s;
+                if (k < np) {
+                    const uint64_t i = p0 + k;
+                    if (K == SFCNL_KERNEL_COUNT) {
+                        A.out[0][i] = double(S.cnt[k]);
+                    } else {
+#pragma unroll
+                        for (int o = 0; o < NO; ++o) A.out[o][i] = S.acc[k][o];
+                    }
+                    A.cnt[i] = S.cnt[k];
+                }
+            }
+        }
+        __syncwarp();  // the warp's slice is reused by its next SC
+    }
+}
