@@ -116,6 +116,7 @@ __device__ __noinline__ bool exact_hit(const BuildArgs& A, double xi, double yi,
 }
 
 #include "build_fast.cuh"
+#include "build_warp.cuh"
 
 // Ordered-frontier BFS over the octree for one SC (collect_candidates,
 // neighbor_build.cpp:43-65). Leaves the accepted leaves (tagged, key order) in
@@ -667,8 +668,20 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
         A.scratch_cap = c->scratch.bytes;
         SFCNL_CUDA_TRY(cudaMemsetAsync(c->build_ctl.p, 0, 3 * 8, c->stream));
         stage_begin(c, kBuild);
-        const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(num_sc, uint64_t(c->num_sms) * 64)));
-        launch(c, k_build_smem, dim3(grid), dim3(kBuildThreads), 0, A, sc0, sc1);
+        if (p.ci == 8 && (p.cj == 8 || p.cj == 4) && p.mode == 0) {
+            // warp-per-SC kernel (build_warp.cuh)
+            const size_t smem = size_t(kBwWarps) * sizeof(BwSmem);
+            cudaFuncSetAttribute(k_build_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            SFCNL_CUDA_TRY(c->work_ctr.reserve(8));
+            SFCNL_CUDA_TRY(cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream));
+            const unsigned grid = unsigned(std::max<uint64_t>(
+                1, std::min<uint64_t>((num_sc + kBwWarps - 1) / kBwWarps, uint64_t(c->num_sms) * 2)));
+            launch(c, k_build_warp, dim3(grid), dim3(kBwWarps * 32), smem, A, sc0, sc1,
+                   c->work_ctr.as<unsigned long long>());
+        } else {
+            const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(num_sc, uint64_t(c->num_sms) * 64)));
+            launch(c, k_build_smem, dim3(grid), dim3(kBuildThreads), 0, A, sc0, sc1);
+        }
         SFCNL_CUDA_TRY(cudaGetLastError());
         SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 3 * 8, cudaMemcpyDeviceToHost, c->stream));
         SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));

@@ -1,0 +1,497 @@
+// Warp-per-super-cluster list build for gather stores with ci == 8, cj in {4, 8}
+// (included by build.cu after build_fast.cuh, inside namespace sfcnl_cu::{anon}).
+//
+// Same results as build_sc (and so as build_neighbor_store, neighbor_build.cpp:74-184),
+// restructured for the GPU: every warp takes the next super-cluster (SC) from a
+// global counter and builds it alone, so there are no block barriers; the warps of
+// an SM hide each other's memory latency.
+//
+//  1. geometry: SC box = sequential union of its i-cluster boxes (every lane,
+//     neighbor_build.cpp:113-118); i particles relative to the SC's first particle
+//     (fp64, per-particle minimum image) rounded to fp32, i-cluster fp32 boxes.
+//  2. traversal (collect_candidates, :43-65): level-synchronous BFS over the octree
+//     with an ORDERED frontier in the warp's shared memory; 32 nodes tested per
+//     step (exact fp64 aabb_dist_sq), warp scans place children / tagged accepted
+//     leaves, so the accepted leaves come out in key order.
+//  3. candidates: per accepted leaf its j-cluster range minus the cluster shared with
+//     the previous leaf (`out.back() != j`, :57-58); a prefix sum over leaves lets each
+//     lane locate its candidate of a 32-wide chunk by binary search.
+//  4. masks (:128-161) per chunk of 32 candidates: stage the j particles in fp32
+//     (SC frame, packed-pair layout), conservative fp32 AABB prefilter (lane =
+//     candidate), pair tests per (i-cluster, candidate) with lane = 8 i x 4 j-quarters
+//     and two slots per lane in f32x2; guard-band pairs and prefilter confirmation
+//     in the reference's fp64 predicates (see build_fast.cuh for the argument).
+//     SCs whose periodic images are ambiguous in the SC frame run the reference
+//     loop in fp64 (lane = candidate).
+//  5. entries with mask != 0 are compacted in order (ballot), then encoded by the
+//     warp (codec::encode, nibble_codec.cpp:56-134) into a byte buffer that aliases
+//     the staging area, bump-allocated into the scratch and copied out.
+// An SC that exceeds a capacity (frontier, entries, bytes) is listed for the
+// global-memory fallback kernel (k_build_global), which runs the generic build_sc.
+constexpr int kBwWarps = 8;
+constexpr uint32_t kBwF = 512;   // frontier entries per buffer
+constexpr uint32_t kBwE = 512;   // entries per SC
+constexpr uint32_t kBwBytes = 32 * 32 * 4;  // encoded bytes (aliases the staging area)
+
+struct BwSmem {
+    uint32_t fa[kBwF], fb[kBwF];
+    float st[32 * 32];  // staging: per (candidate, j-quarter q) {x_a,x_b,y_a,y_b,z_a,z_b,-,-}
+    float ix[64], iy[64], iz[64], ilo[64], ihi[64];
+    float iab[8][6];
+    float pthr[8];
+    uint32_t eidx[kBwE];
+    uint8_t emsk[kBwE];
+};
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Returns false when a capacity is exceeded (nothing published).
+__device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
+    const unsigned lane = lane_id();
+    const uint64_t icl_base = sc * 8;
+    const uint32_t nicl = uint32_t(tmin<uint64_t>(icl_base + 8, A.num_icl) - icl_base);
+    const uint64_t p0 = sc * kSC;
+    const uint32_t np = uint32_t(tmin<uint64_t>(p0 + kSC, A.n) - p0);
+    const uint32_t cj = A.cj;
+
+    // ---- 1. SC geometry (sequential union, as sc_geometry) and the i side
+    Geo scg;
+    geo_init(scg);
+    for (uint32_t b = 0; b < nicl; ++b) {
+        const Geo g = A.igeo[icl_base + b];
+        geo_extend(scg, g);
+        scg.maxh = smax(scg.maxh, g.maxh);
+    }
+    const double r_sc = dmul(A.scale, scg.maxh);
+    const double r2 = dmul(r_sc, r_sc);
+    const double ox = A.x[p0], oy = A.y[p0], oz = A.z[p0];
+    auto rel = [&](double v, double o, int d) {
+        double r = dsub(v, o);
+        if (A.box.per[d]) {
+            const double L = A.box.len[d];
+            if (r > 0.5 * L) r = dsub(r, L);
+            else if (r < -0.5 * L) r = dadd(r, L);
+        }
+        return r;
+    };
+    float eax = 0.f, eay = 0.f, eaz = 0.f, er = 0.f;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        const uint32_t k = lane + 32u * s;
+        float fx = 1e30f, fy = 1e30f, fz = 1e30f;
+        if (k < np) {
+            const double qx = rel(A.x[p0 + k], ox, 0), qy = rel(A.y[p0 + k], oy, 1), qz = rel(A.z[p0 + k], oz, 2);
+            fx = float(qx), fy = float(qy), fz = float(qz);
+            eax = fmaxf(eax, float(fabs(qx))), eay = fmaxf(eay, float(fabs(qy))), eaz = fmaxf(eaz, float(fabs(qz)));
+            er = fmaxf(er, float(dmul(A.scale, A.h[p0 + k])));
+        }
+        S.ix[k] = fx, S.iy[k] = fy, S.iz[k] = fz;
+    }
+    eax = warp_fmax(eax), eay = warp_fmax(eay), eaz = warp_fmax(eaz), er = warp_fmax(er);
+    const bool unsafe = (A.box.per[0] && double(eax) + double(er) >= 0.49 * A.box.len[0]) ||
+                        (A.box.per[1] && double(eay) + double(er) >= 0.49 * A.box.len[1]) ||
+                        (A.box.per[2] && double(eaz) + double(er) >= 0.49 * A.box.len[2]);
+    const float Ei = fmaxf(eax, fmaxf(eay, eaz));
+    __syncwarp();
+    if (lane < nicl) {  // fp32 boxes of the i-clusters (SC frame)
+        float lo[3] = {1e30f, 1e30f, 1e30f}, hi[3] = {-1e30f, -1e30f, -1e30f};
+        for (uint32_t k = lane * 8; k < tmin<uint32_t>(lane * 8 + 8, np); ++k) {
+            lo[0] = fminf(lo[0], S.ix[k]), hi[0] = fmaxf(hi[0], S.ix[k]);
+            lo[1] = fminf(lo[1], S.iy[k]), hi[1] = fmaxf(hi[1], S.iy[k]);
+            lo[2] = fminf(lo[2], S.iz[k]), hi[2] = fmaxf(hi[2], S.iz[k]);
+        }
+        for (int d = 0; d < 3; ++d) S.iab[lane][d] = lo[d], S.iab[lane][3 + d] = hi[d];
+    }
+
+    // ---- 2. ordered-frontier BFS (exact fp64 node test)
+    uint32_t* fa = S.fa;
+    uint32_t* fb = S.fb;
+    if (lane == 0) fa[0] = 0;
+    uint32_t nA = 1;
+    __syncwarp();
+    for (;;) {
+        uint32_t nB = 0;
+        bool expanded = false;
+        for (uint32_t base = 0; base < nA; base += 32) {
+            const uint32_t k = base + lane;
+            uint32_t emit = 0, e = 0;
+            int32_t fc = -1;
+            if (k < nA) {
+                e = fa[k];
+                if (e & kTag) {
+                    emit = 1;
+                } else {
+                    const Node nd = A.nodes[e];
+                    if (nd.pend > nd.pbegin) {
+                        const Geo ng = A.ngeo[e];
+                        if (!(aabb_dist_sq(scg, ng, A.box) > r2)) {
+                            fc = nd.first_child;
+                            emit = fc < 0 ? 1 : 8;
+                        }
+                    }
+                }
+            }
+            const uint32_t inc = warp_incl_scan(emit);
+            const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+            if (nB + tot > kBwF) return false;
+            const uint32_t at = nB + inc - emit;
+            if (emit == 1) fb[at] = e | kTag;
+            if (emit == 8) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) fb[at + c] = uint32_t(fc + c);
+            }
+            expanded |= __any_sync(0xffffffffu, emit == 8);
+            nB += tot;
+        }
+        __syncwarp();
+        uint32_t* t = fa;
+        fa = fb, fb = t;
+        nA = nB;
+        if (!expanded) break;
+    }
+
+    // ---- 3. candidate ranges per accepted leaf: fa[k] <- first candidate, fb[k] <- prefix
+    uint32_t nC = 0;
+    {
+        uint32_t prev_last = 0xffffffffu;  // last cluster of the previous leaf
+        for (uint32_t base = 0; base < nA; base += 32) {
+            const uint32_t k = base + lane;
+            uint32_t f = 0, l = 0;
+            if (k < nA) {
+                const Node nd = A.nodes[fa[k] & ~kTag];
+                f = nd.pbegin / cj, l = (nd.pend - 1) / cj;
+            }
+            uint32_t pl = __shfl_up_sync(0xffffffffu, l, 1);
+            if (lane == 0) pl = prev_last;
+            uint32_t start = f, cnt = 0;
+            if (k < nA) {
+                if (k > 0 && pl == f) start = f + 1;
+                cnt = l + 1 - start;
+            }
+            const uint32_t inc = warp_incl_scan(cnt);
+            __syncwarp();
+            if (k < nA) fa[k] = start, fb[k] = nC + inc - cnt;
+            nC += __shfl_sync(0xffffffffu, inc, 31);
+            prev_last = __shfl_sync(0xffffffffu, l, 31);
+        }
+        __syncwarp();
+    }
+
+    // ---- 4. masks, chunk by chunk; 5a. ordered compaction of mask != 0
+    uint32_t nE = 0;
+    const uint32_t il = lane >> 2, jq = lane & 3;
+    for (uint32_t c0 = 0; c0 < nC; c0 += 32) {
+        const uint32_t n = tmin<uint32_t>(32, nC - c0);
+        const bool valid = lane < n;
+        uint32_t cand = 0;
+        if (valid) {  // leaf k = last with prefix <= pos
+            const uint32_t pos = c0 + lane;
+            uint32_t lo = 0, hi = nA;  // fb[lo] <= pos < fb[hi]
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (fb[mid] <= pos) lo = mid;
+                else hi = mid;
+            }
+            cand = fa[lo] + (pos - fb[lo]);
+        }
+        const int jl0 = int(cand) * int(cj) - int(p0);
+        const unsigned selfm = __ballot_sync(0xffffffffu, valid && jl0 >= -7 && jl0 < kSC);
+        uint32_t mask = 0;
+        if (unsafe) {
+            // reference loop in fp64, lane = candidate (neighbor_build.cpp:128-161)
+            if (valid) {
+                const Geo jg = A.jgeo[cand];
+                const uint64_t jb = uint64_t(cand) * cj, je = tmin<uint64_t>(jb + cj, A.n);
+                for (uint32_t b = 0; b < nicl; ++b) {
+                    const Geo ig = A.igeo[icl_base + b];
+                    const double pre_r = dmul(A.scale, ig.maxh);
+                    if (aabb_dist_sq(ig, jg, A.box) > dmul(pre_r, pre_r)) continue;
+                    const uint64_t ib = (icl_base + b) * 8, ie = tmin<uint64_t>(ib + 8, A.n);
+                    bool hit = false;
+                    for (uint64_t i = ib; i < ie && !hit; ++i) {
+                        const double xi = A.x[i], yi = A.y[i], zi = A.z[i];
+                        const double rr = dmul(A.scale, A.h[i]);
+                        for (uint64_t j = jb; j < je; ++j) {
+                            if (i == j) continue;
+                            const double d2 = pair_d2_exact(xi, yi, zi, A.x[j], A.y[j], A.z[j], A.box, nullptr, nullptr, nullptr);
+                            if (d2 <= dmul(rr, rr)) {
+                                hit = true;
+                                break;
+                            }
+                        }
+                    }
+                    if (hit) mask |= 1u << b;
+                }
+            }
+        } else {
+            // stage: particle t = u*32 + lane -> candidate e = t/8, slot jj = t%8
+            float emax = 0.f;
+#pragma unroll
+            for (int u0 = 0; u0 < 8; u0 += 4) {
+                double vx[4], vy[4], vz[4];
+                bool val[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t e = uint32_t(u0 + u) * 4 + (lane >> 3), jj = lane & 7;
+                    const uint32_t ce = __shfl_sync(0xffffffffu, cand, e);
+                    const uint64_t j = uint64_t(ce) * cj + jj;
+                    val[u] = e < n && jj < cj && j < A.n;
+                    vx[u] = vy[u] = vz[u] = 0.0;
+                    if (val[u]) vx[u] = A.x[j], vy[u] = A.y[j], vz[u] = A.z[j];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t e = uint32_t(u0 + u) * 4 + (lane >> 3), jj = lane & 7;
+                    if (e >= n) continue;
+                    float fx = 1e30f, fy = 1e30f, fz = 1e30f;
+                    if (val[u]) {
+                        fx = float(rel(vx[u], ox, 0)), fy = float(rel(vy[u], oy, 1)), fz = float(rel(vz[u], oz, 2));
+                        emax = fmaxf(emax, fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz))));
+                    }
+                    if (jj < 4 || cj == 8) {
+                        const uint32_t o = e * 32 + (jj & 3) * 8 + (jj >> 2);
+                        S.st[o] = fx, S.st[o + 2] = fy, S.st[o + 4] = fz;
+                    } else {  // cj == 4: slot b of every quarter is a far dummy
+                        const uint32_t o = e * 32 + (jj & 3) * 8 + 1;
+                        S.st[o] = 1e30f, S.st[o + 2] = 1e30f, S.st[o + 4] = 1e30f;
+                    }
+                }
+            }
+            const float E = fmaxf(Ei, warp_fmax(emax));
+            // per-i cutoff thresholds with the guard band, per-i-cluster prefilter thresholds
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const uint32_t k = lane + 32u * s;
+                float lo = -1.f, hi = -1.f;
+                if (k < np) {
+                    const double r = dmul(A.scale, A.h[p0 + k]);
+                    const double rr2 = dmul(r, r), g = d2_guard(r, rr2, E);
+                    lo = __double2float_rd(rr2 - g);
+                    hi = __double2float_ru(rr2 + g);
+                }
+                S.ilo[k] = lo, S.ihi[k] = hi;
+            }
+            if (lane < nicl) {
+                const double pr = dmul(A.scale, A.igeo[icl_base + lane].maxh);
+                const double pr2 = dmul(pr, pr);
+                S.pthr[lane] = __double2float_ru(pr2 + d2_guard(pr, pr2, E));
+            }
+            __syncwarp();
+            // conservative fp32 prefilter, lane = candidate
+            uint32_t pm = 0;
+            if (valid) {
+                float jlo[3] = {1e30f, 1e30f, 1e30f}, jhi[3] = {-1e30f, -1e30f, -1e30f};
+                for (uint32_t jj = 0; jj < cj; ++jj) {
+                    const uint32_t o = lane * 32 + (jj & 3) * 8 + (jj >> 2);
+                    const float vx = S.st[o];
+                    if (vx == 1e30f) continue;
+                    jlo[0] = fminf(jlo[0], vx), jhi[0] = fmaxf(jhi[0], vx);
+                    jlo[1] = fminf(jlo[1], S.st[o + 2]), jhi[1] = fmaxf(jhi[1], S.st[o + 2]);
+                    jlo[2] = fminf(jlo[2], S.st[o + 4]), jhi[2] = fmaxf(jhi[2], S.st[o + 4]);
+                }
+                for (uint32_t b = 0; b < nicl; ++b) {
+                    float s2 = 0.f;
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        const float g = fmaxf(fmaxf(S.iab[b][d], jlo[d]) - fminf(S.iab[b][3 + d], jhi[d]), 0.f);
+                        s2 = fmaf(g, g, s2);
+                    }
+                    if (!(s2 > S.pthr[b])) pm |= 1u << b;
+                }
+            }
+            // pair tests: warp per (i-cluster b, candidate), lane = (i, j-quarter)
+            for (uint32_t b = 0; b < nicl; ++b) {
+                const unsigned todo_all = __ballot_sync(0xffffffffu, (pm >> b) & 1u);
+                if (!todo_all) continue;
+                const uint32_t li = b * 8 + il;
+                const float xi = S.ix[li], yi = S.iy[li], zi = S.iz[li];
+                const f2 xi2 = f2p(xi, xi), yi2 = f2p(yi, yi), zi2 = f2p(zi, zi);
+                const float lo = S.ilo[li], hi = S.ihi[li];
+                unsigned hits = 0;
+                auto d2pair = [&](uint32_t c, float& d2a, float& d2b) {
+                    const ulonglong2 P0 = reinterpret_cast<const ulonglong2*>(S.st)[c * 8 + jq * 2];
+                    const f2 Pz = reinterpret_cast<const f2*>(S.st)[c * 16 + jq * 4 + 2];
+                    const f2 dx = f2sub(xi2, P0.x);
+                    const f2 dy = f2sub(yi2, P0.y);
+                    const f2 dz = f2sub(zi2, Pz);
+                    f2u(f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx))), d2a, d2b);
+                };
+                // guard-band pairs: the reference's fp64 predicates decide
+                auto band = [&](uint32_t c, float d2a, float d2b, bool sa, bool sb) {
+                    const bool band_a = !sa && !(d2a > hi), band_b = !sb && !(d2b > hi);
+                    if (!__any_sync(0xffffffffu, band_a || band_b)) return false;
+                    const uint32_t cc = __shfl_sync(0xffffffffu, cand, c);
+                    bool ex = false;
+                    const uint64_t jb = uint64_t(cc) * cj;
+                    const uint64_t gi = p0 + li;
+                    if (band_a) ex = exact_hit(A, A.x[gi], A.y[gi], A.z[gi], A.h[gi], jb + jq);
+                    if (band_b && !ex) ex = exact_hit(A, A.x[gi], A.y[gi], A.z[gi], A.h[gi], jb + jq + 4);
+                    if (!__any_sync(0xffffffffu, ex)) return false;
+                    // the reference prefilter must pass too (neighbor_build.cpp:136-138)
+                    const Geo ig = A.igeo[icl_base + b];
+                    const double pr = dmul(A.scale, ig.maxh);
+                    return !(aabb_dist_sq(ig, A.jgeo[cc], A.box) > dmul(pr, pr));
+                };
+                unsigned todo = todo_all & ~selfm;
+                while (todo) {
+                    const uint32_t ca = __ffs(todo) - 1;
+                    todo &= todo - 1;
+                    float a0, a1;
+                    d2pair(ca, a0, a1);
+                    if (todo) {  // two candidates in flight
+                        const uint32_t cb = __ffs(todo) - 1;
+                        todo &= todo - 1;
+                        float b0, b1;
+                        d2pair(cb, b0, b1);
+                        const unsigned va = __ballot_sync(0xffffffffu, fminf(a0, a1) < lo);
+                        const unsigned vb = __ballot_sync(0xffffffffu, fminf(b0, b1) < lo);
+                        if (va || band(ca, a0, a1, false, false)) hits |= 1u << ca;
+                        if (vb || band(cb, b0, b1, false, false)) hits |= 1u << cb;
+                    } else {
+                        if (__any_sync(0xffffffffu, fminf(a0, a1) < lo) || band(ca, a0, a1, false, false)) hits |= 1u << ca;
+                    }
+                }
+                unsigned todo_self = todo_all & selfm;
+                while (todo_self) {
+                    const uint32_t cs = __ffs(todo_self) - 1;
+                    todo_self &= todo_self - 1;
+                    float d2a, d2b;
+                    d2pair(cs, d2a, d2b);
+                    const int j0 = __shfl_sync(0xffffffffu, jl0, cs);
+                    const bool sa = j0 + int(jq) == int(li), sb = j0 + int(jq) + 4 == int(li);
+                    const bool clear = (d2a < lo && !sa) || (d2b < lo && !sb);
+                    if (__any_sync(0xffffffffu, clear) || band(cs, d2a, d2b, sa, sb)) hits |= 1u << cs;
+                }
+                mask |= ((hits >> lane) & 1u) << b;
+            }
+        }
+        // ordered compaction of the chunk's entries with mask != 0
+        const bool keep = valid && mask != 0;
+        const unsigned kb = __ballot_sync(0xffffffffu, keep);
+        if (nE + __popc(kb) > kBwE) return false;
+        if (keep) {
+            const uint32_t at = nE + __popc(kb & lanemask_lt());
+            S.eidx[at] = cand, S.emsk[at] = uint8_t(mask);
+        }
+        nE += __popc(kb);
+        __syncwarp();  // staging consumed
+    }
+    __syncwarp();
+
+    // ---- 5b. serialization (neighbor_build.cpp:164-182): masks, then the index list
+    uint8_t* ebuf = reinterpret_cast<uint8_t*>(S.st);
+    const uint32_t mbytes = nE;  // one mask byte per entry (ci == 8)
+    if (mbytes + 4 > kBwBytes) return false;
+    for (uint32_t k = lane; k < nE; k += 32) ebuf[k] = S.emsk[k];
+    uint32_t pos = mbytes;
+    if (!A.compress) {
+        if (mbytes + 4 * nE > kBwBytes) return false;
+        for (uint32_t k = lane; k < nE; k += 32) {
+            const uint32_t v = S.eidx[k];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) ebuf[mbytes + 4 * k + b] = uint8_t(v >> (8 * b));
+        }
+        pos = mbytes + 4 * nE;
+    } else {
+        // nibble codec (nibble_codec.cpp:56-134): blocks of w differences
+        const uint32_t w = uint32_t(A.w);
+        for (uint32_t bb = 0; bb < nE; bb += w) {
+            const uint32_t len = min(w, nE - bb);
+            uint64_t dv[2];
+            uint32_t nd[2], isset[2];
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const uint32_t k = lane + 32u * s;
+                dv[s] = 1, nd[s] = 0, isset[s] = 0;
+                if (k < len && (s == 0 || w == 64)) {
+                    const uint64_t cur = S.eidx[bb + k];
+                    dv[s] = (bb + k == 0) ? cur + 1 : cur - uint64_t(S.eidx[bb + k - 1]);
+                    isset[s] = dv[s] != 1;
+                    nd[s] = (dv[s] > 9) ? uint32_t(nibble_count(dv[s])) : 0u;
+                }
+            }
+            const unsigned m0 = __ballot_sync(0xffffffffu, isset[0]);
+            const unsigned m1 = __ballot_sync(0xffffffffu, isset[1]);
+            const uint32_t ninfo = __popc(m0) + __popc(m1);
+            const uint32_t inc0 = warp_incl_scan(nd[0]);
+            const uint32_t tot0 = __shfl_sync(0xffffffffu, inc0, 31);
+            const uint32_t inc1 = warp_incl_scan(nd[1]);
+            const uint32_t nib = ninfo + tot0 + __shfl_sync(0xffffffffu, inc1, 31);
+            const uint32_t bsize = w / 8 + (nib + 1) / 2;
+            if (pos + bsize > kBwBytes) return false;
+            const unsigned long long bm = (unsigned long long)m0 | ((unsigned long long)m1 << 32);
+            if (lane < w / 8) ebuf[pos + lane] = uint8_t(bm >> (8 * lane));
+            if (lane == 0 && A.btab && bb / w < 16) A.btab[sc * 16 + bb / w] = uint16_t(pos - mbytes);
+            for (uint32_t q = lane; q < (nib + 1) / 2; q += 32) ebuf[pos + w / 8 + q] = 0;
+            __syncwarp();
+            const uint32_t nbase = (pos + w / 8) * 2;  // nibble index of the block's first nibble
+            unsigned int* words = reinterpret_cast<unsigned int*>(ebuf);
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                if (!isset[s]) continue;
+                const uint32_t info_at = s == 0 ? __popc(m0 & lanemask_lt()) : __popc(m0) + __popc(m1 & lanemask_lt());
+                const uint64_t v = dv[s];
+                const uint32_t infov = v <= 9 ? uint32_t(v + 6) : nd[s] - 1;
+                uint32_t t = nbase + info_at;
+                atomicOr(&words[t >> 3], infov << (4 * (t & 7)));
+                if (nd[s]) {
+                    uint32_t dstart = ninfo + (s == 0 ? inc0 - nd[0] : tot0 + inc1 - nd[1]);
+                    for (int p = int(nd[s]) - 1; p >= 0; --p, ++dstart) {
+                        t = nbase + dstart;
+                        atomicOr(&words[t >> 3], uint32_t((v >> (4 * p)) & 15u) << (4 * (t & 7)));
+                    }
+                }
+            }
+            __syncwarp();
+            pos += bsize;
+        }
+    }
+    const uint32_t size = pos;
+
+    // ---- publish: bump-allocate the scratch and copy
+    unsigned long long off = 0;
+    if (lane == 0) {
+        const unsigned long long need = (size + 15ull) & ~15ull;
+        off = atomicAdd(&A.ctl[0], need);
+        if (off + need > A.scratch_cap) {
+            A.ctl[2] = 1;
+            off = ~0ull;
+        }
+        A.counts[sc] = nE;
+        A.sizes[sc] = size;
+        A.soff[sc] = off;
+    }
+    off = __shfl_sync(0xffffffffu, off, 0);
+    if (off != ~0ull) {
+        const unsigned int* src = reinterpret_cast<const unsigned int*>(ebuf);
+        unsigned int* dst = reinterpret_cast<unsigned int*>(A.scratch + off);
+        for (uint32_t q = lane; q < (size + 3) / 4; q += 32) dst[q] = src[q];
+    }
+    __syncwarp();
+    return true;
+}
+
+__global__ void __launch_bounds__(kBwWarps * 32, 2) k_build_warp(const __grid_constant__ BuildArgs A, uint64_t sc_begin,
+                                                                  uint64_t sc_end, unsigned long long* __restrict__ work) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    BwSmem& S = reinterpret_cast<BwSmem*>(dsm)[threadIdx.x >> 5];
+    const unsigned lane = lane_id();
+    for (;;) {
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(work, 1ull);
+        const uint64_t sc = sc_begin + __shfl_sync(0xffffffffu, t, 0);
+        if (sc >= sc_end) break;
+        if (!build_sc_warp(A, S, sc)) {
+            if (lane == 0) {
+                const unsigned long long slot = atomicAdd(&A.ctl[1], 1ull);
+                A.overflow_list[slot] = uint32_t(sc);
+                A.counts[sc] = 0, A.sizes[sc] = 0, A.soff[sc] = 0;
+            }
+        }
+        __syncwarp();
+    }
+}

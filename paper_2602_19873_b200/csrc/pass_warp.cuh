@@ -61,12 +61,6 @@ constexpr size_t pw_smem() {
     return size_t(kPwWarps) * sizeof(PwSmem<K>);
 }
 
-__device__ __forceinline__ float warp_fmax(float v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
-
 template <int K, int CJ>
 __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_warp(const __grid_constant__ PassArgs A,
                                                              unsigned long long* __restrict__ work) {
