@@ -125,6 +125,7 @@ struct sfcnl_cu_ctx {
     // (5) pass
     sfcnl_cu::DBuf outs[4], ncount, jstage;
     sfcnl_cu::DBuf work_ctr;  // dynamic work counter of the warp-per-SC kernels
+    sfcnl_cu::DBuf frame, frame_x;  // cluster-frame fp32 positions (+ payload), max |offset| per axis (frame.cu)
 
     // errors
     sfcnl_cu::DBuf derr;  // DevError
@@ -159,6 +160,8 @@ int run_cluster_geometry(sfcnl_cu_ctx* c, uint32_t ci, uint32_t cj, uint64_t p0 
                          const uint8_t* jflags = nullptr);
 int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, uint64_t sc1, double max_h);
 int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p);
+// cluster-frame staging copy of the sorted positions (frame.cu); m = payload or null
+int run_frame(sfcnl_cu_ctx* c, uint32_t cj, const double* m);
 int run_halo_mark(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, uint64_t sc1);
 
 // Host helpers shared with the C++ drop-in.

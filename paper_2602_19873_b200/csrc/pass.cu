@@ -54,6 +54,8 @@ struct PassArgs {
     const double* q;
     double qs, eps, sigma, ck;
     float lj_close2;  // LJ pairs with d2 < lj_close2 * sigma^2 take the fp64 path
+    const float4* frame;     // cluster-frame staging copy (frame.cu), density/count
+    const unsigned* frame_x; // its max |offset| per axis (float bits)
     double* out[4];
     uint32_t* cnt;
     DevError* err;
@@ -339,6 +341,7 @@ __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& 
 #include "pass_fast.cuh"
 #include "pass_ws.cuh"
 #include "pass_warp.cuh"
+#include "pass_item.cuh"
 
 // Device-side block-offset index of an uploaded store: warp per SC walks the codec
 // block headers (first kBtab blocks) and records where each block starts.
@@ -378,16 +381,28 @@ void launch_pass_warp(sfcnl_cu_ctx* c, const PassArgs& A) {
     launch(c, k_pass_warp<K, CJ>, dim3(grid), dim3(kPwWarps * 32), smem, A, c->work_ctr.as<unsigned long long>());
 }
 
+template <int K, int CJ>
+void launch_pass_item(sfcnl_cu_ctx* c, const PassArgs& A) {
+    const size_t smem = pi_smem<K>();
+    cudaFuncSetAttribute(k_pass_item<K, CJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass_item<K, CJ>, kPiWarps * 32, smem);
+    const uint64_t warps = A.num_sc - A.sc_begin;
+    const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((warps + kPiWarps - 1) / kPiWarps,
+                                                                            uint64_t(c->num_sms) * std::max(per_sm, 1))));
+    cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream);
+    launch(c, k_pass_item<K, CJ>, dim3(grid), dim3(kPiWarps * 32), smem, A, c->work_ctr.as<unsigned long long>());
+}
+
 template <int K>
 void launch_pass(sfcnl_cu_ctx* c, const PassArgs& A, bool fast) {
-    if (fast && getenv("SFCNL_PASS_WS")) {
-        const unsigned grid = unsigned(std::min<uint64_t>(A.num_sc - A.sc_begin, uint64_t(c->num_sms) * 2));
-        const size_t smem = ws_smem<K, 8>();
-        cudaFuncSetAttribute(k_pass_ws<K, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        launch(c, k_pass_ws<K, 8>, dim3(grid), dim3(kWsThreads), smem, A);
-    } else if (fast) {
+    constexpr bool kLJ = K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB;
+    if (fast && kLJ) {  // warp-per-SC lane = (i, j-quarter) layout (pass_warp.cuh)
         if (A.cj == 8) launch_pass_warp<K, 8>(c, A);
         else launch_pass_warp<K, 4>(c, A);
+    } else if (fast) {  // item-parallel layout (pass_item.cuh)
+        if (A.cj == 8) launch_pass_item<K, 8>(c, A);
+        else launch_pass_item<K, 4>(c, A);
     } else {
         const unsigned grid = unsigned(std::min<uint64_t>(A.num_sc - A.sc_begin, uint64_t(c->num_sms) * 32));
         launch(c, k_pass_exact<K>, dim3(grid), dim3(kExactThreads), 0, A);
@@ -434,6 +449,12 @@ int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p) {
     }
     SFCNL_CUDA_TRY(cudaMemsetAsync(c->derr.p, 0xff, sizeof(DevError), c->stream));
     SFCNL_CUDA_TRY(c->work_ctr.reserve(8));
+    if (fast && (p.kernel == SFCNL_KERNEL_DENSITY || p.kernel == SFCNL_KERNEL_COUNT)) {
+        const int rc = run_frame(c, c->sp.cj, A.m);  // staging copy for the item pass
+        if (rc) return rc;
+        A.frame = c->frame.as<const float4>();
+        A.frame_x = c->frame_x.as<const unsigned>();
+    }
     A.n = n;
     A.box = c->sorted.box;
     A.ci = c->sp.ci, A.cj = c->sp.cj, A.icl_per_sc = 64 / c->sp.ci, A.mask_bytes = (A.icl_per_sc + 7) / 8;
