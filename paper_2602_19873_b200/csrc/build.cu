@@ -61,6 +61,8 @@ struct BuildArgs {
     uint64_t scratch_cap;
     uint32_t* overflow_list;
     uint16_t* btab;  // device-side block-offset index for the pass (first 16 blocks per SC)
+    const float4* frame;       // cluster-frame staging copy (frame.cu)
+    const unsigned* frame_x;   // its max |offset| per axis (float bits)
     DevError* err;
 };
 
@@ -669,7 +671,13 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
         SFCNL_CUDA_TRY(cudaMemsetAsync(c->build_ctl.p, 0, 3 * 8, c->stream));
         stage_begin(c, kBuild);
         if (p.ci == 8 && (p.cj == 8 || p.cj == 4) && p.mode == 0) {
-            // warp-per-SC kernel (build_warp.cuh)
+            // warp-per-SC kernel (build_warp.cuh) on the cluster-frame staging copy
+            {
+                const int rc = run_frame(c, p.cj, nullptr);
+                if (rc) return rc;
+            }
+            A.frame = c->frame.as<const float4>();
+            A.frame_x = c->frame_x.as<const unsigned>();
             const size_t smem = size_t(kBwWarps) * sizeof(BwSmem);
             cudaFuncSetAttribute(k_build_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             SFCNL_CUDA_TRY(c->work_ctr.reserve(8));

@@ -16,11 +16,13 @@
 //  3. candidates: per accepted leaf its j-cluster range minus the cluster shared with
 //     the previous leaf (`out.back() != j`, :57-58); a prefix sum over leaves lets each
 //     lane locate its candidate of a 32-wide chunk by binary search.
-//  4. masks (:128-161) per chunk of 32 candidates: stage the j particles in fp32
-//     (SC frame, packed-pair layout), conservative fp32 AABB prefilter (lane =
-//     candidate), pair tests per (i-cluster, candidate) with lane = 8 i x 4 j-quarters
-//     and two slots per lane in f32x2; guard-band pairs and prefilter confirmation
-//     in the reference's fp64 predicates (see build_fast.cuh for the argument).
+//  4. masks (:128-161) per chunk of 32 candidates: stage the j particles in fp32 in
+//     the SC frame from the cluster-frame copy (frame.cu), conservative fp32 AABB
+//     prefilter (lane = candidate), then ONE (i-cluster, candidate) ITEM PER LANE: the
+//     lane holds the candidate's 8 j particles in registers and walks the 8 i rows
+//     (two slots per FFMA2), tracking the row minimum of d2; a hit is d2 < lo (exact
+//     d2 < r_i^2), a row minimum in [lo, hi] is decided by the reference's fp64 pair
+//     predicate and prefilter (see build_fast.cuh for the argument).
 //     SCs whose periodic images are ambiguous in the SC frame run the reference
 //     loop in fp64 (lane = candidate).
 //  5. entries with mask != 0 are compacted in order (ballot), then encoded by the
@@ -31,17 +33,33 @@
 constexpr int kBwWarps = 8;
 constexpr uint32_t kBwF = 512;   // frontier entries per buffer
 constexpr uint32_t kBwE = 512;   // entries per SC
-constexpr uint32_t kBwBytes = 32 * 32 * 4;  // encoded bytes (aliases the staging area)
+constexpr uint32_t kBwBytes = 4096;  // encoded bytes (aliases the staging area)
 
 struct BwSmem {
     uint32_t fa[kBwF], fb[kBwF];
-    float st[32 * 32];  // staging: per (candidate, j-quarter q) {x_a,x_b,y_a,y_b,z_a,z_b,-,-}
-    float ix[64], iy[64], iz[64], ilo[64], ihi[64];
+    union {
+        struct {
+            float4 sa[4][32];  // staged j pairs [p][candidate]: {x_2p, x_2p+1, y_2p, y_2p+1}
+            float2 sz[4][32];  //                                 {z_2p, z_2p+1}
+        } st;
+        uint8_t ebuf[kBwBytes];  // encoder output (after the masks)
+    } u;
+    float4 ia[64];   // [ii*8 + b] {x, y, z, -} SC frame
+    float2 it[64];   // [ii*8 + b] {lo, hi} cutoff thresholds with the guard band
     float iab[8][6];
     float pthr[8];
+    uint32_t cmask[32];
+    uint8_t items[256];
     uint32_t eidx[kBwE];
     uint8_t emsk[kBwE];
 };
+
+// Guard band on a squared distance near r^2 when every coordinate difference carries
+// an absolute error <= ecoord + 2^-24 r (see pass.cu); factor 4 margin.
+__device__ __forceinline__ double guard_band(double r, double r2, double ecoord) {
+    const double ex = ecoord + 5.9604644775390625e-08 * r;
+    return 4.0 * (1.7881393432617188e-07 * r2 + 3.5 * r * ex + 3.0 * ex * ex) + 1e-300;
+}
 
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
@@ -79,30 +97,38 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
         return r;
     };
     float eax = 0.f, eay = 0.f, eaz = 0.f, er = 0.f;
+    double ri[2];
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
         const uint32_t k = lane + 32u * s;
         float fx = 1e30f, fy = 1e30f, fz = 1e30f;
+        ri[s] = -1.0;
         if (k < np) {
             const double qx = rel(A.x[p0 + k], ox, 0), qy = rel(A.y[p0 + k], oy, 1), qz = rel(A.z[p0 + k], oz, 2);
             fx = float(qx), fy = float(qy), fz = float(qz);
             eax = fmaxf(eax, float(fabs(qx))), eay = fmaxf(eay, float(fabs(qy))), eaz = fmaxf(eaz, float(fabs(qz)));
-            er = fmaxf(er, float(dmul(A.scale, A.h[p0 + k])));
+            ri[s] = dmul(A.scale, A.h[p0 + k]);
+            er = fmaxf(er, float(ri[s]));
         }
-        S.ix[k] = fx, S.iy[k] = fy, S.iz[k] = fz;
+        S.ia[(k & 7) * 8 + (k >> 3)] = make_float4(fx, fy, fz, 0.f);
     }
     eax = warp_fmax(eax), eay = warp_fmax(eay), eaz = warp_fmax(eaz), er = warp_fmax(er);
-    const bool unsafe = (A.box.per[0] && double(eax) + double(er) >= 0.49 * A.box.len[0]) ||
-                        (A.box.per[1] && double(eay) + double(er) >= 0.49 * A.box.len[1]) ||
-                        (A.box.per[2] && double(eaz) + double(er) >= 0.49 * A.box.len[2]);
+    // per-particle (i) and per-cluster (j, cluster frame) images against the SC origin are
+    // exact for every in-range pair when max|rel_i| + max r + X < 0.49 L (frame.cu)
+    const float Xx = __uint_as_float(A.frame_x[0]), Xy = __uint_as_float(A.frame_x[1]), Xz = __uint_as_float(A.frame_x[2]);
+    const bool unsafe = (A.box.per[0] && double(eax) + double(er) + double(Xx) >= 0.49 * A.box.len[0]) ||
+                        (A.box.per[1] && double(eay) + double(er) + double(Xy) >= 0.49 * A.box.len[1]) ||
+                        (A.box.per[2] && double(eaz) + double(er) + double(Xz) >= 0.49 * A.box.len[2]);
+    const float Xo = fmaxf(Xx, fmaxf(Xy, Xz));
     const float Ei = fmaxf(eax, fmaxf(eay, eaz));
     __syncwarp();
     if (lane < nicl) {  // fp32 boxes of the i-clusters (SC frame)
         float lo[3] = {1e30f, 1e30f, 1e30f}, hi[3] = {-1e30f, -1e30f, -1e30f};
         for (uint32_t k = lane * 8; k < tmin<uint32_t>(lane * 8 + 8, np); ++k) {
-            lo[0] = fminf(lo[0], S.ix[k]), hi[0] = fmaxf(hi[0], S.ix[k]);
-            lo[1] = fminf(lo[1], S.iy[k]), hi[1] = fmaxf(hi[1], S.iy[k]);
-            lo[2] = fminf(lo[2], S.iz[k]), hi[2] = fmaxf(hi[2], S.iz[k]);
+            const float4 v = S.ia[(k & 7) * 8 + lane];
+            lo[0] = fminf(lo[0], v.x), hi[0] = fmaxf(hi[0], v.x);
+            lo[1] = fminf(lo[1], v.y), hi[1] = fmaxf(hi[1], v.y);
+            lo[2] = fminf(lo[2], v.z), hi[2] = fmaxf(hi[2], v.z);
         }
         for (int d = 0; d < 3; ++d) S.iab[lane][d] = lo[d], S.iab[lane][3 + d] = hi[d];
     }
@@ -228,70 +254,71 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
                 }
             }
         } else {
-            // stage: particle t = u*32 + lane -> candidate e = t/8, slot jj = t%8
-            float emax = 0.f;
-#pragma unroll
-            for (int u0 = 0; u0 < 8; u0 += 4) {
-                double vx[4], vy[4], vz[4];
-                bool val[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t e = uint32_t(u0 + u) * 4 + (lane >> 3), jj = lane & 7;
-                    const uint32_t ce = __shfl_sync(0xffffffffu, cand, e);
-                    const uint64_t j = uint64_t(ce) * cj + jj;
-                    val[u] = e < n && jj < cj && j < A.n;
-                    vx[u] = vy[u] = vz[u] = 0.0;
-                    if (val[u]) vx[u] = A.x[j], vy[u] = A.y[j], vz[u] = A.z[j];
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t e = uint32_t(u0 + u) * 4 + (lane >> 3), jj = lane & 7;
-                    if (e >= n) continue;
-                    float fx = 1e30f, fy = 1e30f, fz = 1e30f;
-                    if (val[u]) {
-                        fx = float(rel(vx[u], ox, 0)), fy = float(rel(vy[u], oy, 1)), fz = float(rel(vz[u], oz, 2));
-                        emax = fmaxf(emax, fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz))));
-                    }
-                    if (jj < 4 || cj == 8) {
-                        const uint32_t o = e * 32 + (jj & 3) * 8 + (jj >> 2);
-                        S.st[o] = fx, S.st[o + 2] = fy, S.st[o + 4] = fz;
-                    } else {  // cj == 4: slot b of every quarter is a far dummy
-                        const uint32_t o = e * 32 + (jj & 3) * 8 + 1;
-                        S.st[o] = 1e30f, S.st[o + 2] = 1e30f, S.st[o + 4] = 1e30f;
-                    }
-                }
+            // stage (cluster frame, frame.cu): shift = fl32(minimage(c_J - o)) per candidate,
+            // s = shift + off per particle; [p][candidate] pair-packed
+            float shx = 0.f, shy = 0.f, shz = 0.f;
+            if (valid) {
+                const uint64_t c0 = uint64_t(cand) * cj;
+                shx = float(rel(A.x[c0], ox, 0)), shy = float(rel(A.y[c0], oy, 1)), shz = float(rel(A.z[c0], oz, 2));
             }
-            const float E = fmaxf(Ei, warp_fmax(emax));
-            // per-i cutoff thresholds with the guard band, per-i-cluster prefilter thresholds
+            float Ej = 0.f;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t e = uint32_t(u) * 4 + (lane >> 3), jj = lane & 7;
+                const uint32_t ce = __shfl_sync(0xffffffffu, cand, e);
+                const float sx = __shfl_sync(0xffffffffu, shx, e), sy = __shfl_sync(0xffffffffu, shy, e);
+                const float sz = __shfl_sync(0xffffffffu, shz, e);
+                if (e >= n) continue;
+                const uint64_t j = uint64_t(ce) * cj + jj;
+                float vx = 1e30f, vy = 1e30f, vz = 1e30f;
+                if (jj < cj && j < A.n) {
+                    const float4 f = __ldg(A.frame + j);
+                    vx = sx + f.x, vy = sy + f.y, vz = sz + f.z;
+                    Ej = fmaxf(Ej, fmaxf(fabsf(vx), fmaxf(fabsf(vy), fabsf(vz))));
+                }
+                float* pa = reinterpret_cast<float*>(&S.u.st.sa[jj >> 1][e]) + (jj & 1);
+                float* pz = reinterpret_cast<float*>(&S.u.st.sz[jj >> 1][e]) + (jj & 1);
+                pa[0] = vx, pa[2] = vy, pz[0] = vz;
+            }
+            Ej = warp_fmax(Ej);
+            // coordinate errors: 2^-24 Ei (i side), 2^-23 (Ej + X) (cluster frame)
+            const double ecoord = 5.9604644775390625e-08 * double(Ei) + 1.1920928955078125e-07 * (double(Ej) + double(Xo));
 #pragma unroll
             for (int s = 0; s < 2; ++s) {
                 const uint32_t k = lane + 32u * s;
                 float lo = -1.f, hi = -1.f;
-                if (k < np) {
-                    const double r = dmul(A.scale, A.h[p0 + k]);
-                    const double rr2 = dmul(r, r), g = d2_guard(r, rr2, E);
+                if (ri[s] >= 0.0) {
+                    const double rr2 = dmul(ri[s], ri[s]), g = guard_band(ri[s], rr2, ecoord);
                     lo = __double2float_rd(rr2 - g);
                     hi = __double2float_ru(rr2 + g);
                 }
-                S.ilo[k] = lo, S.ihi[k] = hi;
+                S.it[(k & 7) * 8 + (k >> 3)] = make_float2(lo, hi);
             }
             if (lane < nicl) {
                 const double pr = dmul(A.scale, A.igeo[icl_base + lane].maxh);
                 const double pr2 = dmul(pr, pr);
-                S.pthr[lane] = __double2float_ru(pr2 + d2_guard(pr, pr2, E));
+                S.pthr[lane] = __double2float_ru(pr2 + guard_band(pr, pr2, ecoord));
             }
+            if (lane < 32) S.cmask[lane] = 0;
             __syncwarp();
             // conservative fp32 prefilter, lane = candidate
             uint32_t pm = 0;
             if (valid) {
                 float jlo[3] = {1e30f, 1e30f, 1e30f}, jhi[3] = {-1e30f, -1e30f, -1e30f};
-                for (uint32_t jj = 0; jj < cj; ++jj) {
-                    const uint32_t o = lane * 32 + (jj & 3) * 8 + (jj >> 2);
-                    const float vx = S.st[o];
-                    if (vx == 1e30f) continue;
-                    jlo[0] = fminf(jlo[0], vx), jhi[0] = fmaxf(jhi[0], vx);
-                    jlo[1] = fminf(jlo[1], S.st[o + 2]), jhi[1] = fmaxf(jhi[1], S.st[o + 2]);
-                    jlo[2] = fminf(jlo[2], S.st[o + 4]), jhi[2] = fmaxf(jhi[2], S.st[o + 4]);
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    const float4 a = S.u.st.sa[p][lane];
+                    const float2 z = S.u.st.sz[p][lane];
+                    if (a.x != 1e30f) {
+                        jlo[0] = fminf(jlo[0], a.x), jhi[0] = fmaxf(jhi[0], a.x);
+                        jlo[1] = fminf(jlo[1], a.z), jhi[1] = fmaxf(jhi[1], a.z);
+                        jlo[2] = fminf(jlo[2], z.x), jhi[2] = fmaxf(jhi[2], z.x);
+                    }
+                    if (a.y != 1e30f) {
+                        jlo[0] = fminf(jlo[0], a.y), jhi[0] = fmaxf(jhi[0], a.y);
+                        jlo[1] = fminf(jlo[1], a.w), jhi[1] = fmaxf(jhi[1], a.w);
+                        jlo[2] = fminf(jlo[2], z.y), jhi[2] = fmaxf(jhi[2], z.y);
+                    }
                 }
                 for (uint32_t b = 0; b < nicl; ++b) {
                     float s2 = 0.f;
@@ -303,71 +330,87 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
                     if (!(s2 > S.pthr[b])) pm |= 1u << b;
                 }
             }
-            // pair tests: warp per (i-cluster b, candidate), lane = (i, j-quarter)
-            for (uint32_t b = 0; b < nicl; ++b) {
-                const unsigned todo_all = __ballot_sync(0xffffffffu, (pm >> b) & 1u);
-                if (!todo_all) continue;
-                const uint32_t li = b * 8 + il;
-                const float xi = S.ix[li], yi = S.iy[li], zi = S.iz[li];
-                const f2 xi2 = f2p(xi, xi), yi2 = f2p(yi, yi), zi2 = f2p(zi, zi);
-                const float lo = S.ilo[li], hi = S.ihi[li];
-                unsigned hits = 0;
-                auto d2pair = [&](uint32_t c, float& d2a, float& d2b) {
-                    const ulonglong2 P0 = reinterpret_cast<const ulonglong2*>(S.st)[c * 8 + jq * 2];
-                    const f2 Pz = reinterpret_cast<const f2*>(S.st)[c * 16 + jq * 4 + 2];
-                    const f2 dx = f2sub(xi2, P0.x);
-                    const f2 dy = f2sub(yi2, P0.y);
-                    const f2 dz = f2sub(zi2, Pz);
-                    f2u(f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx))), d2a, d2b);
+            // items (b << 5 | c), b-major; candidates overlapping the SC's particles last
+            const bool self_me = valid && jl0 >= -7 && jl0 < kSC;
+            uint32_t nItems = 0;
+#pragma unroll 1
+            for (int pass = 0; pass < 2; ++pass) {
+                for (uint32_t b = 0; b < nicl; ++b) {
+                    const bool in = ((pm >> b) & 1u) && (self_me == (pass == 1));
+                    const unsigned bal = __ballot_sync(0xffffffffu, in);
+                    if (in) S.items[nItems + __popc(bal & lanemask_lt())] = uint8_t((b << 5) | lane);
+                    nItems += __popc(bal);
+                }
+            }
+            __syncwarp();
+            // pair tests, one item per lane: hit iff some pair has d2 < lo (exact: d2 < r_i^2);
+            // a row whose minimum lands in [lo, hi] is decided by the reference predicates
+            for (uint32_t t0 = 0; t0 < nItems; t0 += 32) {
+                const uint32_t t = t0 + lane;
+                const bool iv = t < nItems;
+                const uint32_t it8 = iv ? S.items[t] : 0u;
+                const uint32_t c = it8 & 31u, b = it8 >> 5;
+                const int j0 = __shfl_sync(0xffffffffu, jl0, c);
+                const uint32_t cc = __shfl_sync(0xffffffffu, cand, c);
+                const bool self = iv && j0 >= -7 && j0 < kSC;
+                ulonglong2 Ja[4];
+                f2 Jz[4];
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    Ja[p] = reinterpret_cast<const ulonglong2&>(S.u.st.sa[p][c]);
+                    Jz[p] = reinterpret_cast<const f2&>(S.u.st.sz[p][c]);
+                }
+                bool hit = false;
+                uint32_t band_rows = 0;
+                auto rows = [&](auto SELF) {
+                    constexpr bool kSelf = decltype(SELF)::value;
+#pragma unroll 1
+                    for (int ii = 0; ii < 8 && iv && !hit; ++ii) {
+                        const float4 I = S.ia[ii * 8 + b];
+                        const float2 T = S.it[ii * 8 + b];
+                        const f2 xi2 = f2p(I.x, I.x), yi2 = f2p(I.y, I.y), zi2 = f2p(I.z, I.z);
+                        const int iself = kSelf && self ? int(b * 8 + ii) - j0 : -1;
+                        float mn = 3.0e38f;
+#pragma unroll
+                        for (int p = 0; p < 4; ++p) {
+                            const f2 dx = f2sub(xi2, Ja[p].x), dy = f2sub(yi2, Ja[p].y), dz = f2sub(zi2, Jz[p]);
+                            float d2a, d2b;
+                            f2u(f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx))), d2a, d2b);
+                            if (kSelf) {
+                                if (iself == 2 * p) d2a = 3.0e38f;
+                                if (iself == 2 * p + 1) d2b = 3.0e38f;
+                            }
+                            mn = fminf(mn, fminf(d2a, d2b));
+                        }
+                        if (mn < T.x) hit = true;
+                        else if (mn <= T.y) band_rows |= 1u << ii;
+                    }
                 };
-                // guard-band pairs: the reference's fp64 predicates decide
-                auto band = [&](uint32_t c, float d2a, float d2b, bool sa, bool sb) {
-                    const bool band_a = !sa && !(d2a > hi), band_b = !sb && !(d2b > hi);
-                    if (!__any_sync(0xffffffffu, band_a || band_b)) return false;
-                    const uint32_t cc = __shfl_sync(0xffffffffu, cand, c);
-                    bool ex = false;
+                if (__any_sync(0xffffffffu, self)) rows(BoolC<true>());
+                else rows(BoolC<false>());
+                if (iv && !hit && band_rows) {
+                    // guard band: the reference's exact pair predicate, then its prefilter
+                    // (neighbor_build.cpp:136-155) -- any exact hit suffices
                     const uint64_t jb = uint64_t(cc) * cj;
-                    const uint64_t gi = p0 + li;
-                    if (band_a) ex = exact_hit(A, A.x[gi], A.y[gi], A.z[gi], A.h[gi], jb + jq);
-                    if (band_b && !ex) ex = exact_hit(A, A.x[gi], A.y[gi], A.z[gi], A.h[gi], jb + jq + 4);
-                    if (!__any_sync(0xffffffffu, ex)) return false;
-                    // the reference prefilter must pass too (neighbor_build.cpp:136-138)
-                    const Geo ig = A.igeo[icl_base + b];
-                    const double pr = dmul(A.scale, ig.maxh);
-                    return !(aabb_dist_sq(ig, A.jgeo[cc], A.box) > dmul(pr, pr));
-                };
-                unsigned todo = todo_all & ~selfm;
-                while (todo) {
-                    const uint32_t ca = __ffs(todo) - 1;
-                    todo &= todo - 1;
-                    float a0, a1;
-                    d2pair(ca, a0, a1);
-                    if (todo) {  // two candidates in flight
-                        const uint32_t cb = __ffs(todo) - 1;
-                        todo &= todo - 1;
-                        float b0, b1;
-                        d2pair(cb, b0, b1);
-                        const unsigned va = __ballot_sync(0xffffffffu, fminf(a0, a1) < lo);
-                        const unsigned vb = __ballot_sync(0xffffffffu, fminf(b0, b1) < lo);
-                        if (va || band(ca, a0, a1, false, false)) hits |= 1u << ca;
-                        if (vb || band(cb, b0, b1, false, false)) hits |= 1u << cb;
-                    } else {
-                        if (__any_sync(0xffffffffu, fminf(a0, a1) < lo) || band(ca, a0, a1, false, false)) hits |= 1u << ca;
+                    bool ex = false;
+                    for (int ii = 0; ii < 8 && !ex; ++ii) {
+                        if (!((band_rows >> ii) & 1u)) continue;
+                        const uint64_t gi = p0 + b * 8 + ii;
+                        for (uint32_t jj = 0; jj < cj && !ex; ++jj) {
+                            if (jb + jj >= A.n || jb + jj == gi) continue;
+                            ex = exact_hit(A, A.x[gi], A.y[gi], A.z[gi], A.h[gi], jb + jj);
+                        }
+                    }
+                    if (ex) {
+                        const Geo ig = A.igeo[icl_base + b];
+                        const double pr = dmul(A.scale, ig.maxh);
+                        hit = !(aabb_dist_sq(ig, A.jgeo[cc], A.box) > dmul(pr, pr));
                     }
                 }
-                unsigned todo_self = todo_all & selfm;
-                while (todo_self) {
-                    const uint32_t cs = __ffs(todo_self) - 1;
-                    todo_self &= todo_self - 1;
-                    float d2a, d2b;
-                    d2pair(cs, d2a, d2b);
-                    const int j0 = __shfl_sync(0xffffffffu, jl0, cs);
-                    const bool sa = j0 + int(jq) == int(li), sb = j0 + int(jq) + 4 == int(li);
-                    const bool clear = (d2a < lo && !sa) || (d2b < lo && !sb);
-                    if (__any_sync(0xffffffffu, clear) || band(cs, d2a, d2b, sa, sb)) hits |= 1u << cs;
-                }
-                mask |= ((hits >> lane) & 1u) << b;
+                if (hit) atomicOr(&S.cmask[c], 1u << b);
             }
+            __syncwarp();
+            mask = valid ? S.cmask[lane] : 0u;
         }
         // ordered compaction of the chunk's entries with mask != 0
         const bool keep = valid && mask != 0;
@@ -383,7 +426,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
     __syncwarp();
 
     // ---- 5b. serialization (neighbor_build.cpp:164-182): masks, then the index list
-    uint8_t* ebuf = reinterpret_cast<uint8_t*>(S.st);
+    uint8_t* ebuf = S.u.ebuf;
     const uint32_t mbytes = nE;  // one mask byte per entry (ci == 8)
     if (mbytes + 4 > kBwBytes) return false;
     for (uint32_t k = lane; k < nE; k += 32) ebuf[k] = S.emsk[k];

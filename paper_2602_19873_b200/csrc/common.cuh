@@ -116,6 +116,12 @@ __device__ __forceinline__ void geo_extend(Geo& a, const Geo& o) {
     geo_extend_pt(a, o.hi[0], o.hi[1], o.hi[2]);
 }
 
+// compile-time bool tag for generic lambdas (template specialisation of a loop body)
+template <bool B>
+struct BoolC {
+    static constexpr bool value = B;
+};
+
 template <class T>
 __host__ __device__ __forceinline__ T tmin(T a, T b) { return b < a ? b : a; }
 

@@ -18,10 +18,6 @@
 constexpr int kWsConsumers = 256, kWsProducers = 128, kWsThreads = kWsConsumers + kWsProducers;
 constexpr int kWsCap = 128;  // entries per chunk (double-buffered)
 
-template <bool B>
-struct BoolC {
-    static constexpr bool value = B;
-};
 
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
