@@ -54,6 +54,7 @@ struct PassArgs {
     const double* q;
     double qs, eps, sigma, ck;
     float lj_close2;  // LJ pairs with d2 < lj_close2 * sigma^2 take the fp64 path
+    float sig2f;      // float(sigma^2)
     const float4* frame;     // cluster-frame staging copy (frame.cu), density/count
     const unsigned* frame_x; // its max |offset| per axis (float bits)
     double* out[4];
@@ -397,7 +398,7 @@ void launch_pass_item(sfcnl_cu_ctx* c, const PassArgs& A) {
 template <int K>
 void launch_pass(sfcnl_cu_ctx* c, const PassArgs& A, bool fast) {
     constexpr bool kLJ = K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB;
-    if (fast && kLJ) {  // warp-per-SC lane = (i, j-quarter) layout (pass_warp.cuh)
+    if (fast && kLJ && !getenv("SFCNL_PASS_ITEM_LJ")) {  // warp-per-SC lane = (i, j-quarter) layout (pass_warp.cuh)
         if (A.cj == 8) launch_pass_warp<K, 8>(c, A);
         else launch_pass_warp<K, 4>(c, A);
     } else if (fast) {  // item-parallel layout (pass_item.cuh)
@@ -476,6 +477,7 @@ int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p) {
     A.h = c->sorted.h.as<double>();
     A.qs = p.query_scale, A.eps = p.epsilon, A.sigma = p.sigma, A.ck = p.coulomb_k;
     A.lj_close2 = kLjClose2;
+    A.sig2f = float(p.sigma * p.sigma);
     if (const char* e = getenv("SFCNL_LJ_CLOSE2")) A.lj_close2 = float(atof(e));
     for (int o = 0; o < 4; ++o) A.out[o] = c->outs[o].as<double>() - p0;
     A.cnt = c->ncount.as<uint32_t>() - p0;

@@ -55,16 +55,6 @@ constexpr size_t pi_smem() {
     return size_t(kPiWarps) * sizeof(PiSmem<K>);
 }
 
-__device__ __forceinline__ float fset_lt(float a, float b) {  // 1.0f if a < b else 0.0f
-    float r;
-    asm("set.lt.f32.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ float fset_le(float a, float b) {
-    float r;
-    asm("set.le.f32.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
-    return r;
-}
 __device__ __forceinline__ f2 f2lo(ulonglong2 v) { return v.x; }
 __device__ __forceinline__ f2 f2hi(ulonglong2 v) { return v.y; }
 

@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                     float inv_h = 0.f;
                     if (K == SFCNL_KERNEL_DENSITY) inv_h = S.iinvh[li];
                     const f2 invh2 = f2p(inv_h, inv_h);
-                    f2 acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+                    f2 acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0, cntf = 0;
                     double accd0 = 0.0, accd1 = 0.0, accd2 = 0.0, accd3 = 0.0;  // LJ close pairs (fp64)
 
                     struct Ld {
@@ -309,66 +309,59 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                         f2u(f2fma(L.dz, L.dz, f2fma(L.dy, L.dy, f2mul(L.dx, L.dx))), L.d2a, L.d2b);
                         return L;
                     };
+                    // special slot (divergent, rare): an in-range LJ pair closer than
+                    // kLjClose * sigma (fp64 from the staged hi/lo coordinates; coincidence
+                    // range through the reference path) or a cutoff inside the guard band
+                    // (the reference predicate and fp64 kernel decide)
+                    auto special = [&](uint32_t e, int sl2, float d2) {
+                        const uint64_t j = uint64_t(S.idx[h0 + e]) * CJ + jq + 4 * sl2;
+                        if (j >= A.n) return;
+                        if (LJ && d2 < lo) {
+                            const float* pj = S.sj + e * 32 + jq * 8;
+                            const float* pl = S.sl + e * 32 + jq * 8;
+                            const double dx = (double(S.ix[li]) - double(pj[sl2])) + (double(S.ilx[li]) - double(pl[sl2]));
+                            const double dy = (double(S.iy[li]) - double(pj[2 + sl2])) + (double(S.ily[li]) - double(pl[2 + sl2]));
+                            const double dz = (double(S.iz[li]) - double(pj[4 + sl2])) + (double(S.ilz[li]) - double(pl[4 + sl2]));
+                            const double dd2 = dx * dx + dy * dy + dz * dz;
+                            if (dd2 >= double(kLjTiny2) * sig2d) {
+                                const double inv2 = 1.0 / dd2;
+                                const double s2 = sig2d * inv2, s6 = s2 * s2 * s2;
+                                double coef = eps24d * inv2 * s6 * (2.0 * s6 - 1.0);
+                                double en = eps4d * s6 * (s6 - 1.0);
+                                if (K == SFCNL_KERNEL_LJ_COULOMB) {
+                                    const double qq = A.ck * A.q[i] * A.q[j], ir = sqrt(inv2);
+                                    en += qq * ir;
+                                    coef += qq * ir * inv2;
+                                }
+                                accd0 += coef * dx, accd1 += coef * dy, accd2 += coef * dz, accd3 += en;
+                                ++cnt;
+                                return;
+                            }
+                        }
+                        const int rc = rare_slot<K>(A, i, j, r2, &S.acc[li][0]);
+                        cnt += rc > 0, coincident |= rc < 0;
+                    };
                     auto compute = [&](uint32_t e, const Ld& L, auto SELF) {
                         constexpr bool kSelf = decltype(SELF)::value;
-                        bool self_a = false, self_b = false;
-                        if (kSelf) {
+                        float d2a = L.d2a, d2b = L.d2b;
+                        if (kSelf) {  // i == j slots drop out
                             const int jl0 = int(__shfl_sync(0xffffffffu, my_idx, e)) * CJ - int(p0);
-                            self_a = jl0 + int(jq) == li;
-                            self_b = CJ == 8 && jl0 + int(jq) + 4 == li;
+                            if (jl0 + int(jq) == li) d2a = kFar;
+                            if (CJ == 8 && jl0 + int(jq) + 4 == li) d2b = kFar;
                         }
-                        bool in_a = L.d2a < lo && !self_a, in_b = L.d2b < lo && !self_b;
-                        bool rare_a = !in_a && !(L.d2a > hi_t) && !self_a;
-                        bool rare_b = !in_b && !(L.d2b > hi_t) && !self_b;
-                        bool cl_a = false, cl_b = false;
-                        if (LJ) {
-                            rare_a = rare_a || (in_a && L.d2a < tiny2);
-                            rare_b = rare_b || (in_b && L.d2b < tiny2);
-                            in_a = in_a && !(L.d2a < tiny2);
-                            in_b = in_b && !(L.d2b < tiny2);
-                            cl_a = in_a && L.d2a < close2, cl_b = in_b && L.d2b < close2;
-                            in_a = in_a && !cl_a, in_b = in_b && !cl_b;
-                            if (cl_a | cl_b) {
-                                // fp64 from the staged hi/lo coordinates (exact SC-relative values)
-                                const float* pj = S.sj + e * 32 + jq * 8;
-                                const float* pl = S.sl + e * 32 + jq * 8;
-#pragma unroll
-                                for (int sl2 = 0; sl2 < 2; ++sl2) {
-                                    if (!(sl2 ? cl_b : cl_a)) continue;
-                                    const double dx = (double(S.ix[li]) - double(pj[sl2])) + (double(S.ilx[li]) - double(pl[sl2]));
-                                    const double dy = (double(S.iy[li]) - double(pj[2 + sl2])) + (double(S.ily[li]) - double(pl[2 + sl2]));
-                                    const double dz = (double(S.iz[li]) - double(pj[4 + sl2])) + (double(S.ilz[li]) - double(pl[4 + sl2]));
-                                    const double inv2 = 1.0 / (dx * dx + dy * dy + dz * dz);
-                                    const double s2 = sig2d * inv2, s6 = s2 * s2 * s2;
-                                    double coef = eps24d * inv2 * s6 * (2.0 * s6 - 1.0);
-                                    double en = eps4d * s6 * (s6 - 1.0);
-                                    if (K == SFCNL_KERNEL_LJ_COULOMB) {
-                                        const uint64_t jj = uint64_t(S.idx[h0 + e]) * CJ + jq + 4 * sl2;
-                                        const double qq = A.ck * A.q[i] * A.q[jj], ir = sqrt(inv2);
-                                        en += qq * ir;
-                                        coef += qq * ir * inv2;
-                                    }
-                                    accd0 += coef * dx, accd1 += coef * dy, accd2 += coef * dz, accd3 += en;
-                                }
-                                cnt += uint32_t(cl_a) + uint32_t(cl_b);
-                            }
+                        float ma = fset_lt(d2a, lo), mb = fset_lt(d2b, lo);
+                        // special: inside the guard band [lo, hi], or (LJ) closer than close2
+                        const bool sa = (LJ && d2a < close2) || (!(d2a < lo) && d2a <= hi_t);
+                        const bool sb = (LJ && d2b < close2) || (!(d2b < lo) && d2b <= hi_t);
+                        if (sa | sb) {
+                            if (sa) special(e, 0, d2a), ma = 0.f;
+                            if (sb) special(e, 1, d2b), mb = 0.f;
                         }
-                        if (rare_a | rare_b) {
-                            double* side = &S.acc[li][0];
-                            const uint64_t jb = uint64_t(S.idx[h0 + e]) * CJ;
-                            if (rare_a && jb + jq < A.n) {
-                                const int rc = rare_slot<K>(A, i, jb + jq, r2, side);
-                                cnt += rc > 0, coincident |= rc < 0;
-                            }
-                            if (rare_b && jb + jq + 4 < A.n) {
-                                const int rc = rare_slot<K>(A, i, jb + jq + 4, r2, side);
-                                cnt += rc > 0, coincident |= rc < 0;
-                            }
-                        }
-                        cnt += uint32_t(in_a) + uint32_t(in_b);
+                        const f2 m2 = f2p(ma, mb);
+                        cntf = f2add(cntf, m2);
                         if (K == SFCNL_KERNEL_DENSITY) {
                             // W(q)/(2 sigma) = max(1-q,0)^3 - 4 max(1/2-q,0)^3
-                            const f2 q = f2mul(f2p(sqrt_ftz(L.d2a), sqrt_ftz(L.d2b)), invh2);
+                            const f2 q = f2mul(f2p(sqrt_ftz(d2a), sqrt_ftz(d2b)), invh2);
                             const f2 omq = f2sub(f2p(1.f, 1.f), q), hmq = f2sub(f2p(0.5f, 0.5f), q);
                             float t0, t1, u0, u1;
                             f2u(omq, t0, t1);
@@ -377,23 +370,25 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                             const f2 u = f2p(fmaxf(u0, 0.f), fmaxf(u1, 0.f));
                             const f2 t3 = f2mul(f2mul(t, t), t), u3 = f2mul(f2mul(u, u), u);
                             const f2 wv = f2fma(f2p(-4.f, -4.f), u3, t3);
-                            acc0 = f2fma(f2p(in_a ? L.pma : 0.f, in_b ? L.pmb : 0.f), wv, acc0);
+                            acc0 = f2fma(f2mul(f2p(L.pma, L.pmb), m2), wv, acc0);
                         } else if (LJ) {
-                            const f2 inv2 = f2p(in_a ? rcp_ftz(L.d2a) : 0.f, in_b ? rcp_ftz(L.d2b) : 0.f);
-                            const f2 s2 = f2mul(f2p(sig2, sig2), inv2);
+                            // m2 = 0 for out-of-range / special slots; d2 >= close2 > 0 here, so rcp is finite
+                            const f2 inv2 = f2mul(f2p(rcp_ftz(d2a), rcp_ftz(d2b)), m2);
+                            const f2 s2 = f2mul(f2p(A.sig2f, A.sig2f), inv2);
                             const f2 s6 = f2mul(f2mul(s2, s2), s2);
-                            const f2 coef = f2mul(f2mul(f2mul(f2p(eps24, eps24), inv2), s6),
-                                                  f2fma(f2p(2.f, 2.f), s6, f2p(-1.f, -1.f)));
-                            f2 ee = f2mul(f2mul(f2p(eps4, eps4), s6), f2sub(s6, f2p(1.f, 1.f)));
-                            f2 cf = coef;
+                            // 24 eps / 4 eps are applied at the flush (K == LJ)
+                            f2 cf = f2mul(inv2, f2mul(s6, f2fma(f2p(2.f, 2.f), s6, f2p(-1.f, -1.f))));
+                            f2 ee = f2fma(s6, s6, f2mul(s6, f2p(-1.f, -1.f)));
                             if (K == SFCNL_KERNEL_LJ_COULOMB) {
+                                cf = f2mul(cf, f2p(eps24, eps24));
+                                ee = f2mul(ee, f2p(eps4, eps4));
                                 const uint64_t jb = uint64_t(S.idx[h0 + e]) * CJ;
                                 const float qi = float(A.ck * A.q[i]);
-                                const float qa = in_a ? qi * float(A.q[jb + jq]) : 0.f;
-                                const float qb = (CJ == 8 && in_b) ? qi * float(A.q[jb + jq + 4]) : 0.f;
+                                const float qa = ma != 0.f ? qi * float(A.q[jb + jq]) : 0.f;
+                                const float qb = (CJ == 8 && mb != 0.f) ? qi * float(A.q[jb + jq + 4]) : 0.f;
                                 float ra, rb;
-                                asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(L.d2a));
-                                asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rb) : "f"(L.d2b));
+                                asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(d2a));
+                                asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rb) : "f"(d2b));
                                 const f2 qr = f2mul(f2p(qa, qb), f2p(ra, rb));
                                 ee = f2add(ee, qr);
                                 cf = f2fma(qr, inv2, cf);
@@ -432,10 +427,16 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                     for (int o = 0; o < NO; ++o) {
                         float a, c;
                         f2u(accs[o], a, c);
-                        double v = double(a) + double(c) + (LJ ? accds[o] : 0.0);
+                        const double sc_o = K == SFCNL_KERNEL_LJ ? (o < 3 ? eps24d : eps4d) : 1.0;
+                        double v = (double(a) + double(c)) * sc_o + (LJ ? accds[o] : 0.0);
                         v += __shfl_xor_sync(0xffffffffu, v, 1);
                         v += __shfl_xor_sync(0xffffffffu, v, 2);
                         tot[o] = v;
+                    }
+                    {
+                        float c0, c1;
+                        f2u(cntf, c0, c1);
+                        cnt += uint32_t(c0 + c1);
                     }
                     cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
                     cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
