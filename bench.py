@@ -189,8 +189,13 @@ def run_reference(args, ws, rank):
 
 
 # ---------------------------------------------------------------- B200 arm
+_TORCH_DT = {}
+
+
 def run_b200(args, ws, rank, local):
     import torch
+    _TORCH_DT.update({np.dtype(np.uint32): torch.int32, np.dtype(np.uint64): torch.int64,
+                      np.dtype(np.uint8): torch.uint8, np.dtype(np.float64): torch.float64})
     import paper_2602_19873_b200 as S
 
     n = args.n
@@ -213,6 +218,8 @@ def run_b200(args, ws, rank, local):
     bp = S.BuildParams(S.ClusterParams(8, 8, 32), S.GATHER, True, 1.0)
     pipe = S.Pipeline(ctx, pps, box, bp, kernels, S.PassConfig(1.0, S.MIXED))
     pipe.upload()
+    # pinned host result buffers for the end-to-end leg (a serving loop reuses them)
+    pipe.host_buffers(lambda cnt, dt: torch.empty(int(cnt), dtype=_TORCH_DT[np.dtype(dt)], pin_memory=True).numpy().view(dt))
     stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
 
     for _ in range(args.warmup):

@@ -350,10 +350,15 @@ class Context:
         self.check(self.L.sfcnl_cu_build_store(self.h, C.byref(p), C.byref(nsc), C.byref(nb)))
         return nsc.value, nb.value
 
-    def get_store(self, bp: BuildParams, n, nsc, nb) -> NeighborStore:
-        counts = np.empty(nsc, np.uint32)
-        offsets = np.empty(nsc + 1, np.uint64)
-        blob = np.empty(max(nb, 1), np.uint8)
+    def get_store(self, bp: BuildParams, n, nsc, nb, into=None) -> NeighborStore:
+        """Downloads the store; `into` = (counts, offsets, blob) host arrays to fill
+        (e.g. pinned buffers reused across steps), large enough for nsc / nb."""
+        if into is not None:
+            counts, offsets, blob = into[0][:nsc], into[1][:nsc + 1], into[2][:max(nb, 1)]
+        else:
+            counts = np.empty(nsc, np.uint32)
+            offsets = np.empty(nsc + 1, np.uint64)
+            blob = np.empty(max(nb, 1), np.uint8)
         self.check(self.L.sfcnl_cu_get_store(self.h, _ptr(counts), _ptr(offsets), _ptr(blob)))
         return NeighborStore(bp, n, counts, offsets, blob[:nb])
 
@@ -366,15 +371,19 @@ class Context:
         self.check(self.L.sfcnl_cu_set_store(self.h, C.byref(p), int(store.n), len(counts), _ptr(counts),
                                              _ptr(offsets), _ptr(buf), len(blob)))
 
-    def reduce(self, kernel: Kernel, cfg: PassConfig, n, download=True):
+    def reduce(self, kernel: Kernel, cfg: PassConfig, n, download=True, into=None):
+        """`into` = (list of output arrays, count array) host buffers to fill."""
         pp = N.PassParamsC(kernel.kind, int(cfg.precision), float(cfg.query_scale), kernel.epsilon,
                            kernel.sigma, kernel.coulomb_k)
         nout = len(kernel.names)
         if not download:
             self.check(self.L.sfcnl_cu_reduce(self.h, C.byref(pp), None, None))
             return None
-        outs = [np.empty(n) for _ in range(nout)]
-        cnt = np.empty(n, np.uint32)
+        if into is not None:
+            outs, cnt = [o[:n] for o in into[0][:nout]], into[1][:n]
+        else:
+            outs = [np.empty(n) for _ in range(nout)]
+            cnt = np.empty(n, np.uint32)
         arr = (C.c_void_p * 4)(*([o.ctypes.data for o in outs] + [None] * (4 - nout)))
         self.check(self.L.sfcnl_cu_reduce(self.h, C.byref(pp), arr, _ptr(cnt)))
         return ReduceResult(list(kernel.names), outs, cnt)

@@ -40,16 +40,33 @@ class Pipeline:
         for k in self.kernels:
             c.reduce(k, self.cfg, self.n, download=False)
 
+    def host_buffers(self, alloc=np.empty):
+        """Reusable host result buffers for run_e2e (pass e.g. a pinned allocator):
+        store arrays sized for the worst case (w/8 + 10 bytes per possible entry is
+        never reached; blob capacity grows on demand) and per-kernel outputs."""
+        nsc = (self.n + 63) // 64
+        self._out = {
+            "store": [alloc(nsc, np.uint32), alloc(nsc + 1, np.uint64), alloc(max(16 * self.n // 4, 16), np.uint8)],
+            "pass": [([alloc(self.n, np.float64) for _ in k.names], alloc(self.n, np.uint32)) for k in self.kernels],
+        }
+        self._alloc = alloc
+        return self._out
+
     def run_e2e(self):
-        """Upload -> step -> download (store + every kernel's outputs)."""
+        """Upload -> step -> download (store + every kernel's outputs) into the host
+        buffers of host_buffers() when set (fresh arrays otherwise)."""
         self.upload()
         c = self.ctx
         c.sort(self.bits)
         c.apply_order()
         self.num_nodes = c.octree(self.bucket)
         self.num_sc, self.blob_bytes = c.build_store(self.bp)
-        store = c.get_store(self.bp, self.n, self.num_sc, self.blob_bytes)
-        results = [c.reduce(k, self.cfg, self.n, download=True) for k in self.kernels]
+        out = getattr(self, "_out", None)
+        if out is not None and len(out["store"][2]) < self.blob_bytes:
+            out["store"][2] = self._alloc(self.blob_bytes, np.uint8)
+        store = c.get_store(self.bp, self.n, self.num_sc, self.blob_bytes, into=out["store"] if out else None)
+        results = [c.reduce(k, self.cfg, self.n, download=True, into=out["pass"][i] if out else None)
+                   for i, k in enumerate(self.kernels)]
         return store, results
 
     def h2d_bytes(self):
