@@ -26,6 +26,7 @@
 // SCs whose frontier/candidates/bytes exceed the shared-memory capacities are
 // re-run by the same code with global-memory workspaces (fallback launch).
 #include <algorithm>
+#include <cstdio>
 #include <vector>
 
 #include "ctx.hpp"
@@ -63,6 +64,7 @@ struct BuildArgs {
     uint16_t* btab;  // device-side block-offset index for the pass (first 16 blocks per SC)
     const float4* frame;       // cluster-frame staging copy (frame.cu)
     const unsigned* frame_x;   // its max |offset| per axis (float bits)
+    unsigned long long* prof;  // phase clocks (SFCNL_PHASE_PROF builds)
     DevError* err;
 };
 
@@ -578,8 +580,8 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
     if (sc0 > sc1) return set_error(c, 1, "build_neighbor_store: bad super-cluster range");
     const uint64_t p_lo = sc0 * 64, p_hi = tmin<uint64_t>(sc1 * 64, n);
 
-    SFCNL_CUDA_TRY(c->build_ctl.reserve(8 * 8));
-    SFCNL_CUDA_TRY(cudaMemsetAsync(c->build_ctl.p, 0, 8 * 8, c->stream));
+    SFCNL_CUDA_TRY(c->build_ctl.reserve(24 * 8));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(c->build_ctl.p, 0, 24 * 8, c->stream));
     SFCNL_CUDA_TRY(cudaMemsetAsync(c->derr.p, 0xff, sizeof(DevError), c->stream));
     if (p_hi > p_lo) {
         const uint64_t m = p_hi - p_lo;
@@ -655,6 +657,7 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
     A.sizes = c->sc_size.as<uint32_t>() - sc0;
     A.soff = c->sc_scratch_off.as<uint64_t>() - sc0;
     A.ctl = c->build_ctl.as<unsigned long long>();
+    A.prof = c->build_ctl.as<unsigned long long>() + 8;
     A.overflow_list = c->overflow_list.as<uint32_t>();
     A.err = c->derr.as<DevError>();
     A.btab = nullptr;
@@ -714,6 +717,15 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
             if (rc) return rc;
         }
         stage_end(c, kBuild);
+#ifdef SFCNL_PHASE_PROF
+        {
+            unsigned long long pr[9] = {};
+            cudaMemcpy(pr, A.prof, 9 * 8, cudaMemcpyDeviceToHost);
+            fprintf(stderr, "build phases (Gclk): geo %.2f trav %.2f cand %.2f masks-rest %.2f encode %.2f publish %.2f | stage %.2f thr+pref+items %.2f pairs %.2f overflow %llu\n",
+                    pr[0] * 1e-9, pr[1] * 1e-9, pr[2] * 1e-9, pr[3] * 1e-9, pr[4] * 1e-9, pr[5] * 1e-9, pr[6] * 1e-9,
+                    pr[7] * 1e-9, pr[8] * 1e-9, ctl[1]);
+        }
+#endif
         if (!ctl[2]) break;
         scratch_cap = ctl[0] + (1 << 20);  // scratch overflow: grow to the needed size and redo
         if (attempt == 2) return set_error(c, 4, "build_neighbor_store: scratch allocation failed");

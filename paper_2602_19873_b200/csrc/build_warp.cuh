@@ -68,8 +68,24 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }
 
 // Returns false when a capacity is exceeded (nothing published).
+#ifdef SFCNL_PHASE_PROF
+#define PHASE(k)                                                                   \
+    do {                                                                           \
+        const long long _t = clock64();                                            \
+        if (lane == 0) atomicAdd(A.prof + (k), (unsigned long long)(_t - _tprev)); \
+        _tprev = _t;                                                               \
+    } while (0)
+#else
+#define PHASE(k) \
+    do {         \
+    } while (0)
+#endif
+
 __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
     const unsigned lane = lane_id();
+#ifdef SFCNL_PHASE_PROF
+    long long _tprev = clock64();
+#endif
     const uint64_t icl_base = sc * 8;
     const uint32_t nicl = uint32_t(tmin<uint64_t>(icl_base + 8, A.num_icl) - icl_base);
     const uint64_t p0 = sc * kSC;
@@ -133,6 +149,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
         for (int d = 0; d < 3; ++d) S.iab[lane][d] = lo[d], S.iab[lane][3 + d] = hi[d];
     }
 
+    PHASE(0);
     // ---- 2. ordered-frontier BFS (exact fp64 node test)
     uint32_t* fa = S.fa;
     uint32_t* fb = S.fb;
@@ -180,6 +197,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
         if (!expanded) break;
     }
 
+    PHASE(1);
     // ---- 3. candidate ranges per accepted leaf: fa[k] <- first candidate, fb[k] <- prefix
     uint32_t nC = 0;
     {
@@ -207,8 +225,11 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
         __syncwarp();
     }
 
+    PHASE(2);
     // ---- 4. masks, chunk by chunk; 5a. ordered compaction of mask != 0
     uint32_t nE = 0;
+    double pr_me = 0.0, pr2_me = 0.0;  // prefilter radius of i-cluster `lane` (neighbor_build.cpp:136)
+    if (lane < nicl) pr_me = dmul(A.scale, A.igeo[icl_base + lane].maxh), pr2_me = dmul(pr_me, pr_me);
     const uint32_t il = lane >> 2, jq = lane & 3;
     for (uint32_t c0 = 0; c0 < nC; c0 += 32) {
         const uint32_t n = tmin<uint32_t>(32, nC - c0);
@@ -255,25 +276,36 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
             }
         } else {
             // stage (cluster frame, frame.cu): shift = fl32(minimage(c_J - o)) per candidate,
-            // s = shift + off per particle; [p][candidate] pair-packed
-            float shx = 0.f, shy = 0.f, shz = 0.f;
+            // s = shift + off per particle; [p][candidate] pair-packed. Every load of the
+            // chunk (origins: lane = candidate; offsets: lane = particle) is issued first.
+            double cx = 0.0, cy = 0.0, cz = 0.0;
             if (valid) {
                 const uint64_t c0 = uint64_t(cand) * cj;
-                shx = float(rel(A.x[c0], ox, 0)), shy = float(rel(A.y[c0], oy, 1)), shz = float(rel(A.z[c0], oz, 2));
+                cx = A.x[c0], cy = A.y[c0], cz = A.z[c0];
             }
-            float Ej = 0.f;
+            float4 fo[8];
+            uint32_t okm = 0;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const uint32_t e = uint32_t(u) * 4 + (lane >> 3), jj = lane & 7;
                 const uint32_t ce = __shfl_sync(0xffffffffu, cand, e);
+                const uint64_t j = uint64_t(ce) * cj + jj;
+                const bool ok = e < n && jj < cj && j < A.n;
+                fo[u] = ok ? __ldg(A.frame + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+                okm |= uint32_t(ok) << u;
+            }
+            float shx = 0.f, shy = 0.f, shz = 0.f;
+            if (valid) shx = float(rel(cx, ox, 0)), shy = float(rel(cy, oy, 1)), shz = float(rel(cz, oz, 2));
+            float Ej = 0.f;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t e = uint32_t(u) * 4 + (lane >> 3), jj = lane & 7;
                 const float sx = __shfl_sync(0xffffffffu, shx, e), sy = __shfl_sync(0xffffffffu, shy, e);
                 const float sz = __shfl_sync(0xffffffffu, shz, e);
                 if (e >= n) continue;
-                const uint64_t j = uint64_t(ce) * cj + jj;
                 float vx = 1e30f, vy = 1e30f, vz = 1e30f;
-                if (jj < cj && j < A.n) {
-                    const float4 f = __ldg(A.frame + j);
-                    vx = sx + f.x, vy = sy + f.y, vz = sz + f.z;
+                if ((okm >> u) & 1u) {
+                    vx = sx + fo[u].x, vy = sy + fo[u].y, vz = sz + fo[u].z;
                     Ej = fmaxf(Ej, fmaxf(fabsf(vx), fmaxf(fabsf(vy), fabsf(vz))));
                 }
                 float* pa = reinterpret_cast<float*>(&S.u.st.sa[jj >> 1][e]) + (jj & 1);
@@ -281,6 +313,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
                 pa[0] = vx, pa[2] = vy, pz[0] = vz;
             }
             Ej = warp_fmax(Ej);
+            PHASE(6);
             // coordinate errors: 2^-24 Ei (i side), 2^-23 (Ej + X) (cluster frame)
             const double ecoord = 5.9604644775390625e-08 * double(Ei) + 1.1920928955078125e-07 * (double(Ej) + double(Xo));
 #pragma unroll
@@ -294,11 +327,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
                 }
                 S.it[(k & 7) * 8 + (k >> 3)] = make_float2(lo, hi);
             }
-            if (lane < nicl) {
-                const double pr = dmul(A.scale, A.igeo[icl_base + lane].maxh);
-                const double pr2 = dmul(pr, pr);
-                S.pthr[lane] = __double2float_ru(pr2 + guard_band(pr, pr2, ecoord));
-            }
+            if (lane < nicl) S.pthr[lane] = __double2float_ru(pr2_me + guard_band(pr_me, pr2_me, ecoord));
             if (lane < 32) S.cmask[lane] = 0;
             __syncwarp();
             // conservative fp32 prefilter, lane = candidate
@@ -343,6 +372,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
                 }
             }
             __syncwarp();
+            PHASE(7);
             // pair tests, one item per lane: hit iff some pair has d2 < lo (exact: d2 < r_i^2);
             // a row whose minimum lands in [lo, hi] is decided by the reference predicates
             for (uint32_t t0 = 0; t0 < nItems; t0 += 32) {
@@ -410,6 +440,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
                 if (hit) atomicOr(&S.cmask[c], 1u << b);
             }
             __syncwarp();
+            PHASE(8);
             mask = valid ? S.cmask[lane] : 0u;
         }
         // ordered compaction of the chunk's entries with mask != 0
@@ -425,6 +456,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
     }
     __syncwarp();
 
+    PHASE(3);
     // ---- 5b. serialization (neighbor_build.cpp:164-182): masks, then the index list
     uint8_t* ebuf = S.u.ebuf;
     const uint32_t mbytes = nE;  // one mask byte per entry (ci == 8)
@@ -495,6 +527,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
     }
     const uint32_t size = pos;
 
+    PHASE(4);
     // ---- publish: bump-allocate the scratch and copy
     unsigned long long off = 0;
     if (lane == 0) {
@@ -515,6 +548,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
         for (uint32_t q = lane; q < (size + 3) / 4; q += 32) dst[q] = src[q];
     }
     __syncwarp();
+    PHASE(5);
     return true;
 }
 

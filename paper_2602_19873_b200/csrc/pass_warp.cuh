@@ -38,6 +38,7 @@ constexpr int kPwChunk = 32;   // entries staged at a time
 constexpr float kLjClose2 = 1.5f;
 constexpr float kLjTiny2 = 1e-6f;
 constexpr bool kTwo = false;
+constexpr bool kTwoDensityOff = true;
 
 template <int K>
 struct PwSmem {
@@ -404,7 +405,7 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                     while (mine) {
                         const uint32_t e1 = __ffs(mine) - 1;
                         mine &= mine - 1;
-                        if (kTwo && !LJ && mine) {  // two entries in flight
+                        if (kTwo && (LJ || !kTwoDensityOff) && mine) {  // two entries in flight
                             const uint32_t e2 = __ffs(mine) - 1;
                             mine &= mine - 1;
                             const Ld L1 = load(e1), L2 = load(e2);
