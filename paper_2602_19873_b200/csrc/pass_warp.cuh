@@ -27,7 +27,7 @@
 //    the reference's fp64 predicate and kernel (rare_slot), so neighbor_count is
 //    exact. SCs whose periodic images are ambiguous in the SC frame ("unsafe")
 //    evaluate every slot that way.
-constexpr int kPwWarps = 8;    // independent warps per CTA
+constexpr int kPwWarps = 4;    // independent warps per CTA
 constexpr int kPwChunk = 32;   // entries staged at a time
 // LJ pairs with d2 < kLjClose2 * sigma^2 are evaluated in fp64 from the staged
 // hi/lo coordinates (in registers): the energy (s6 - 1) and force (2 s6 - 1)
@@ -44,13 +44,13 @@ template <int K>
 struct PwSmem {
     static constexpr bool LJ = (K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB);
     static constexpr int NO = nout<K>();
-    static constexpr int kMinBlocks = LJ ? 2 : 3;  // CTAs per SM (registers: 128 / 85)
+    static constexpr int kMinBlocks = LJ ? 4 : 6;  // CTAs of 4 warps per SM (registers: 128 / 85)
     float sj[kPwChunk * 32];              // hi x,y,z + payload
-    float sl[LJ ? kPwChunk * 32 : 4];     // lo x,y,z (LJ)
+    float4 sl4[LJ ? kPwChunk * 4 : 1];    // lo (LJ) per (entry, j-quarter): {lx_a, lx_b, ly_a, ly_b}
+    float2 sl2[LJ ? kPwChunk * 4 : 1];    //                                  {lz_a, lz_b}
     uint32_t idx[64];                     // decoded block
     float ix[64], iy[64], iz[64];
     float ilx[LJ ? 64 : 1], ily[LJ ? 64 : 1], ilz[LJ ? 64 : 1];
-    double ir[64];     // r_i = query_scale * h_i (< 0: inactive)
     double iscale[64]; // density: 8/(pi h^3) * 2 (the spline's factor 2 folded in)
     float iinvh[64];   // density: 1 / h_i
     double acc[64][NO];
@@ -136,7 +136,6 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
             }
             S.ix[k] = fx, S.iy[k] = fy, S.iz[k] = fz;
             if (LJ) S.ilx[k] = float(qx - double(fx)), S.ily[k] = float(qy - double(fy)), S.ilz[k] = float(qz - double(fz));
-            S.ir[k] = r;
             if (K == SFCNL_KERNEL_DENSITY) S.iscale[k] = 2.0 * (8.0 / (kPi * hk * hk * hk)), S.iinvh[k] = float(1.0 / hk);
 #pragma unroll
             for (int o = 0; o < NO; ++o) S.acc[k][o] = 0.0;
@@ -188,7 +187,6 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                 float emax = 0.f;
                 if (!unsafe) {
                     float* sj = S.sj;
-                    float* sl = S.sl;
 #pragma unroll
                     for (int k0 = 0; k0 < 8; k0 += 4) {
                         double vx[4], vy[4], vz[4], vm[4];
@@ -220,12 +218,20 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                             }
                             if (jj < 4 || CJ == 8) {
                                 sj[o] = fx, sj[o + 2] = fy, sj[o + 4] = fz, sj[o + 6] = fm;
-                                if (LJ) sl[o] = lx, sl[o + 2] = ly, sl[o + 4] = lz;
+                                if (LJ) {
+                                    float* l4 = reinterpret_cast<float*>(&S.sl4[e * 4 + (jj & 3)]) + (jj >> 2);
+                                    float* l2 = reinterpret_cast<float*>(&S.sl2[e * 4 + (jj & 3)]) + (jj >> 2);
+                                    l4[0] = lx, l4[2] = ly, l2[0] = lz;
+                                }
                             } else {
                                 // cj == 4: slot b of every quarter is a far dummy
                                 const uint32_t ob = e * 32 + (jj & 3) * 8 + 1;
                                 sj[ob] = kFar, sj[ob + 2] = kFar, sj[ob + 4] = kFar, sj[ob + 6] = 0.f;
-                                if (LJ) sl[ob] = 0.f, sl[ob + 2] = 0.f, sl[ob + 4] = 0.f;
+                                if (LJ) {
+                                    float* l4 = reinterpret_cast<float*>(&S.sl4[e * 4 + (jj & 3)]) + 1;
+                                    float* l2 = reinterpret_cast<float*>(&S.sl2[e * 4 + (jj & 3)]) + 1;
+                                    l4[0] = 0.f, l4[2] = 0.f, l2[0] = 0.f;
+                                }
                             }
                         }
                     }
@@ -241,7 +247,7 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                     if (!mine) continue;
                     const int li = int(b * 8 + il);
                     const uint64_t i = p0 + uint64_t(li);
-                    const double r = S.ir[li];
+                    const double r = uint32_t(li) < np ? dmul(A.qs, A.h[p0 + li]) : -1.0;
                     const double r2 = dmul(r, r);
                     const bool active = r >= 0.0;
                     uint32_t cnt = 0;
@@ -300,8 +306,8 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                         L.dy = f2sub(yi2, P0.y);
                         L.dz = f2sub(zi2, P1.x);
                         if (LJ) {
-                            const ulonglong2 L0 = reinterpret_cast<const ulonglong2*>(S.sl)[e * 8 + jq * 2];
-                            const ulonglong2 L1 = reinterpret_cast<const ulonglong2*>(S.sl)[e * 8 + jq * 2 + 1];
+                            const ulonglong2 L0 = reinterpret_cast<const ulonglong2&>(S.sl4[e * 4 + jq]);
+                            const ulonglong2 L1 = make_ulonglong2(reinterpret_cast<const f2&>(S.sl2[e * 4 + jq]), 0ull);
                             L.dx = f2add(L.dx, f2sub(lxi2, L0.x));
                             L.dy = f2add(L.dy, f2sub(lyi2, L0.y));
                             L.dz = f2add(L.dz, f2sub(lzi2, L1.x));
@@ -319,10 +325,11 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                         if (j >= A.n) return;
                         if (LJ && d2 < lo) {
                             const float* pj = S.sj + e * 32 + jq * 8;
-                            const float* pl = S.sl + e * 32 + jq * 8;
+                            const float* pl = reinterpret_cast<const float*>(&S.sl4[e * 4 + jq]);
+                            const float* pz = reinterpret_cast<const float*>(&S.sl2[e * 4 + jq]);
                             const double dx = (double(S.ix[li]) - double(pj[sl2])) + (double(S.ilx[li]) - double(pl[sl2]));
                             const double dy = (double(S.iy[li]) - double(pj[2 + sl2])) + (double(S.ily[li]) - double(pl[2 + sl2]));
-                            const double dz = (double(S.iz[li]) - double(pj[4 + sl2])) + (double(S.ilz[li]) - double(pl[4 + sl2]));
+                            const double dz = (double(S.iz[li]) - double(pj[4 + sl2])) + (double(S.ilz[li]) - double(pz[sl2]));
                             const double dd2 = dx * dx + dy * dy + dz * dz;
                             if (dd2 >= double(kLjTiny2) * sig2d) {
                                 const double inv2 = 1.0 / dd2;
