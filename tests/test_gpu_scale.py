@@ -1,0 +1,117 @@
+"""Full-size parity (BASELINE.json configs[1], C2: 2^26 uniform particles, 200
+neighbours, 8x8 gather compressed): the CUDA build and mixed pass at the bench
+size, checked on sampled super-cluster ranges against the plain-C restatement
+(oracle/sfcnl_oracle.c build_store_range / reduce_range, which follow
+neighbor_build.cpp:74-184 and reduce.hpp:38-231 and are pinned to the reference's
+golden fixtures by tests/test_oracle_golden.py).
+
+* store: counts and every byte of the sampled SCs' slices are bit-exact;
+* density (mixed): neighbor_count exact, relative error <= 1e-5;
+* LJ (mixed): neighbor_count exact, force error <= 1e-5 * sum_j |F_ij|, energy error
+  <= 1e-5 * sum_j |E_ij| (same bar as tests/test_gpu_parity.py).
+
+SFCNL_SCALE_N overrides the particle count (default 2^26)."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2602_19873_b200 as S
+from oracle.oracle import Oracle, Particles, Tree, Store
+
+pytestmark = pytest.mark.gpu
+P = Oracle("port")
+N = int(os.environ.get("SFCNL_SCALE_N", str(1 << 26)))
+
+
+@pytest.fixture(scope="module")
+def run():
+    ctx = S.Context(0)
+    ps, box = S.make_uniform(S.UniformSpec(n=N, density=float(N), target_neighbors=200.0, seed=42))
+    bp = S.BuildParams(S.ClusterParams(8, 8, 32), S.GATHER, True, 1.0)
+    sigma = 0.5 * (1.0 / N) ** (1.0 / 3.0)
+    ctx.set_particles(ps, box)
+    ctx.sort()
+    ctx.apply_order()
+    nn = ctx.octree(64)
+    nsc, nb = ctx.build_store(bp)
+    store = ctx.get_store(bp, N, nsc, nb)
+    nodes = ctx.get_octree(nn)
+    geo = ctx.node_geometry(nn)
+    rho = ctx.reduce(S.sph_density_kernel(), S.PassConfig(1.0, S.MIXED), N)
+    lj = ctx.reduce(S.lj_kernel(1.0, sigma), S.PassConfig(1.0, S.MIXED), N)
+    sp = Particles(*(ctx.get_sorted(f, N) for f in ("x", "y", "z", "h", "m")), np.zeros(N),
+                   np.array(list(box.lo) + list(box.hi)), tuple(int(v) for v in box.periodic))
+    f = lambda k, dt: np.ascontiguousarray(nodes[k], dt)  # structured-array fields are strided views
+    tree = Tree(f("key_first", np.uint64), f("key_last", np.uint64), f("particle_begin", np.uint32),
+                f("particle_end", np.uint32), f("first_child", np.int32), f("depth", np.uint8), 21)
+    rng = np.random.default_rng(5)
+    starts = sorted({0, nsc - 48} | set(int(v) for v in rng.integers(0, nsc - 48, 3)))
+    return dict(store=store, geo=geo, rho=rho, lj=lj, sp=sp, tree=tree, sigma=sigma, ranges=[(s, s + 48) for s in starts])
+
+
+def _slice(store, sc0, sc1):
+    o = store.offsets
+    return store.counts[sc0:sc1], store.blob[int(o[sc0]):int(o[sc1])]
+
+
+def test_store_bit_exact_on_sampled_ranges(run):
+    sp, tree, geo = run["sp"], run["tree"], run["geo"]
+    for sc0, sc1 in run["ranges"]:
+        ref = P.build_store_range(sp, tree, geo, sc0, sc1, float(sp.h.max()))
+        counts, blob = _slice(run["store"], sc0, sc1)
+        assert np.array_equal(counts, ref.counts), (sc0, sc1)
+        assert np.array_equal(blob, ref.blob), (sc0, sc1)
+
+
+def _range_store(run, sc0, sc1):
+    st = run["store"]
+    counts, blob = _slice(st, sc0, sc1)
+    offs = st.offsets[sc0:sc1 + 1] - st.offsets[sc0]
+    return Store(run["sp"].n, 8, 8, 32, 0, 1, 1.0, counts.copy(), offs.astype(np.uint64), blob.copy())
+
+
+def test_density_mixed_on_sampled_ranges(run):
+    for sc0, sc1 in run["ranges"]:
+        outs, cnt = P.reduce_range("density", run["sp"], _range_store(run, sc0, sc1), sc0)
+        p0, p1 = 64 * sc0, 64 * sc0 + len(cnt)
+        assert np.array_equal(run["rho"].neighbor_count[p0:p1], cnt)
+        assert np.max(np.abs(run["rho"].outputs[0][p0:p1] - outs[0]) / np.abs(outs[0])) <= 1e-5
+
+
+def test_lj_mixed_on_sampled_ranges(run):
+    sp, sigma = run["sp"], run["sigma"]
+    L = sp.box6[3:] - sp.box6[:3]
+    for sc0, sc1 in run["ranges"]:
+        rs = _range_store(run, sc0, sc1)
+        outs, cnt = P.reduce_range("lj", sp, rs, sc0, eps=1.0, sigma=sigma)
+        p0, p1 = 64 * sc0, 64 * sc0 + len(cnt)
+        assert np.array_equal(run["lj"].neighbor_count[p0:p1], cnt)
+        # sum_j |F_ij| and sum_j |E_ij| over the in-range pairs of the decoded entries
+        absf, abse = np.zeros(p1 - p0), np.zeros(p1 - p0)
+        pos = np.stack([sp.x, sp.y, sp.z], 1)
+        for s in range(sc1 - sc0):
+            c = int(rs.counts[s])
+            if not c:
+                continue
+            b, e = int(rs.offsets[s]), int(rs.offsets[s + 1])
+            idx, _ = P.decode(rs.blob[b + c:e], c, 32)
+            for k, jc in enumerate(idx):
+                mask = int(rs.blob[b + k])
+                js = np.arange(int(jc) * 8, min(int(jc) * 8 + 8, sp.n))
+                for bit in range(8):
+                    if not (mask >> bit) & 1:
+                        continue
+                    ii = np.arange(64 * (sc0 + s) + 8 * bit, min(64 * (sc0 + s) + 8 * bit + 8, sp.n))
+                    d = pos[ii][:, None, :] - pos[js][None, :, :]
+                    d -= L * np.rint(d / L)
+                    d2 = (d * d).sum(2)
+                    ok = (d2 <= (sp.h[ii] ** 2)[:, None]) & (js[None, :] != ii[:, None])
+                    inv2 = np.where(ok, 1.0 / np.where(ok, d2, 1.0), 0.0)
+                    s6 = (sigma * sigma * inv2) ** 3
+                    absf[ii - p0] += np.sum(np.abs(24.0 * inv2 * (2 * s6 * s6 - s6)) * np.sqrt(d2) * ok, 1)
+                    abse[ii - p0] += np.sum(np.abs(4.0 * (s6 * s6 - s6)) * ok, 1)
+        f = run["lj"].outputs
+        err = np.sqrt(sum((f[k][p0:p1] - outs[k]) ** 2 for k in range(3)))
+        assert np.max(err / np.maximum(absf, 1e-300)) <= 1e-5
+        assert np.max(np.abs(f[3][p0:p1] - outs[3]) / np.maximum(abse, 1e-300)) <= 1e-5
