@@ -84,6 +84,7 @@ struct sfcnl_cu_ctx {
     int bits = 21;
     uint64_t order_n = 0;
     sfcnl_cu::DBuf keys, perm, keys_alt, perm_alt;
+    sfcnl_cu::DBuf records;  // apply_order: packed particle records (sfc_sort.cu)
     sfcnl_cu::DBuf hist, digit_base, status, tile_counter;
     sfcnl_cu::DBuf hilbert_table;
 

@@ -250,12 +250,32 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     }
 }
 
-__global__ void k_gather(uint64_t n, const uint32_t* __restrict__ perm, int narr,
-                         const double* const* __restrict__ src, double* const* __restrict__ dst) {
+// apply_sfc_order (hilbert.cpp:28-44) as two HBM passes: the SoA inputs are packed
+// into narr-double records (sequential), then every output particle fetches its
+// whole record (one random 8*narr-byte read instead of narr random 8-byte reads).
+__global__ void k_pack_records(uint64_t n, int narr, const double* const* __restrict__ src,
+                               double* __restrict__ rec) {
+    for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n;
+         k += uint64_t(gridDim.x) * blockDim.x)
+        for (int a = 0; a < narr; ++a) rec[k * narr + a] = __ldg(src[a] + k);
+}
+
+template <int NA>
+__global__ void k_gather_records(uint64_t n, const uint32_t* __restrict__ perm, int narr,
+                                 const double* __restrict__ rec, double* const* __restrict__ dst) {
+    const int na = NA > 0 ? NA : narr;
     for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n;
          k += uint64_t(gridDim.x) * blockDim.x) {
-        const uint32_t p = perm[k];
-        for (int a = 0; a < narr; ++a) dst[a][k] = __ldg(src[a] + p);
+        const double* r = rec + uint64_t(perm[k]) * na;
+        if (NA > 0) {
+            double v[NA > 0 ? NA : 1];
+#pragma unroll
+            for (int a = 0; a < NA; ++a) v[a] = __ldg(r + a);
+#pragma unroll
+            for (int a = 0; a < NA; ++a) dst[a][k] = v[a];
+        } else {
+            for (int a = 0; a < na; ++a) dst[a][k] = __ldg(r + a);
+        }
     }
 }
 
@@ -382,10 +402,19 @@ int run_apply_order(sfcnl_cu_ctx* c, int64_t into) {
     std::vector<void*> host(2 * narr);
     for (int a = 0; a < narr; ++a) host[a] = (void*)src[a], host[narr + a] = dst[a];
     SFCNL_CUDA_TRY(cudaMemcpyAsync(tbl, host.data(), 2 * narr * sizeof(void*), cudaMemcpyHostToDevice, c->stream));
+    SFCNL_CUDA_TRY(c->records.reserve(n * narr * 8));
     stage_begin(c, kPermute);
     const int grid = int(std::min<uint64_t>((n + 255) / 256, uint64_t(c->num_sms) * 16));
-    launch(c, k_gather, dim3(grid), dim3(256), 0, n, (const uint32_t*)c->perm.as<uint32_t>(), narr,
-           (const double* const*)tbl, (double* const*)(tbl + narr));
+    launch(c, k_pack_records, dim3(grid), dim3(256), 0, n, narr, (const double* const*)tbl, c->records.as<double>());
+    const uint32_t* pm = c->perm.as<uint32_t>();
+    const double* rc = c->records.as<double>();
+    double* const* dt = (double* const*)(tbl + narr);
+    switch (narr) {
+        case 4: launch(c, k_gather_records<4>, dim3(grid), dim3(256), 0, n, pm, narr, rc, dt); break;
+        case 5: launch(c, k_gather_records<5>, dim3(grid), dim3(256), 0, n, pm, narr, rc, dt); break;
+        case 6: launch(c, k_gather_records<6>, dim3(grid), dim3(256), 0, n, pm, narr, rc, dt); break;
+        default: launch(c, k_gather_records<0>, dim3(grid), dim3(256), 0, n, pm, narr, rc, dt); break;
+    }
     SFCNL_CUDA_TRY(cudaGetLastError());
     stage_end(c, kPermute);
     return 0;
