@@ -253,20 +253,21 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
 // apply_sfc_order (hilbert.cpp:28-44) as two HBM passes: the SoA inputs are packed
 // into narr-double records (sequential), then every output particle fetches its
 // whole record (one random 8*narr-byte read instead of narr random 8-byte reads).
-__global__ void k_pack_records(uint64_t n, int narr, const double* const* __restrict__ src,
+// Records of narr doubles, packed back to back.
+__global__ void k_pack_records(uint64_t n, int narr, int stride, const double* const* __restrict__ src,
                                double* __restrict__ rec) {
     for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n;
          k += uint64_t(gridDim.x) * blockDim.x)
-        for (int a = 0; a < narr; ++a) rec[k * narr + a] = __ldg(src[a] + k);
+        for (int a = 0; a < narr; ++a) rec[k * stride + a] = __ldg(src[a] + k);
 }
 
 template <int NA>
-__global__ void k_gather_records(uint64_t n, const uint32_t* __restrict__ perm, int narr,
+__global__ void k_gather_records(uint64_t n, const uint32_t* __restrict__ perm, int narr, int stride,
                                  const double* __restrict__ rec, double* const* __restrict__ dst) {
     const int na = NA > 0 ? NA : narr;
     for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n;
          k += uint64_t(gridDim.x) * blockDim.x) {
-        const double* r = rec + uint64_t(perm[k]) * na;
+        const double* r = rec + uint64_t(perm[k]) * stride;
         if (NA > 0) {
             double v[NA > 0 ? NA : 1];
 #pragma unroll
@@ -402,18 +403,19 @@ int run_apply_order(sfcnl_cu_ctx* c, int64_t into) {
     std::vector<void*> host(2 * narr);
     for (int a = 0; a < narr; ++a) host[a] = (void*)src[a], host[narr + a] = dst[a];
     SFCNL_CUDA_TRY(cudaMemcpyAsync(tbl, host.data(), 2 * narr * sizeof(void*), cudaMemcpyHostToDevice, c->stream));
-    SFCNL_CUDA_TRY(c->records.reserve(n * narr * 8));
+    const int stride = narr;  // (64-byte padding measured slower: more pack traffic, no fewer bursts)
+    SFCNL_CUDA_TRY(c->records.reserve(n * stride * 8));
     stage_begin(c, kPermute);
     const int grid = int(std::min<uint64_t>((n + 255) / 256, uint64_t(c->num_sms) * 16));
-    launch(c, k_pack_records, dim3(grid), dim3(256), 0, n, narr, (const double* const*)tbl, c->records.as<double>());
+    launch(c, k_pack_records, dim3(grid), dim3(256), 0, n, narr, stride, (const double* const*)tbl, c->records.as<double>());
     const uint32_t* pm = c->perm.as<uint32_t>();
     const double* rc = c->records.as<double>();
     double* const* dt = (double* const*)(tbl + narr);
     switch (narr) {
-        case 4: launch(c, k_gather_records<4>, dim3(grid), dim3(256), 0, n, pm, narr, rc, dt); break;
-        case 5: launch(c, k_gather_records<5>, dim3(grid), dim3(256), 0, n, pm, narr, rc, dt); break;
-        case 6: launch(c, k_gather_records<6>, dim3(grid), dim3(256), 0, n, pm, narr, rc, dt); break;
-        default: launch(c, k_gather_records<0>, dim3(grid), dim3(256), 0, n, pm, narr, rc, dt); break;
+        case 4: launch(c, k_gather_records<4>, dim3(grid), dim3(256), 0, n, pm, narr, stride, rc, dt); break;
+        case 5: launch(c, k_gather_records<5>, dim3(grid), dim3(256), 0, n, pm, narr, stride, rc, dt); break;
+        case 6: launch(c, k_gather_records<6>, dim3(grid), dim3(256), 0, n, pm, narr, stride, rc, dt); break;
+        default: launch(c, k_gather_records<0>, dim3(grid), dim3(256), 0, n, pm, narr, stride, rc, dt); break;
     }
     SFCNL_CUDA_TRY(cudaGetLastError());
     stage_end(c, kPermute);
