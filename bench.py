@@ -279,6 +279,15 @@ def run_b200(args, ws, rank, local):
     dom_ms = stage[dom]
     ab = algo_bytes.get(dom, 48.0) * n
     achieved = ab / (dom_ms * 1e-3) / 1e9
+    traffic, pipe_util = None, None
+    try:  # DRAM bytes of the same kernel from the committed ncu capture of this workload
+        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
+            tj = json.load(f)
+        if int(tj["n"]) == n:
+            traffic = tj["dram_bytes_per_launch"].get(dom)
+            pipe_util = tj["pipe_util_pct_8m"].get(dom)
+    except (OSError, KeyError, ValueError):
+        pass
     out = {
         "metric": METRIC, "value": round(value_job, 4), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_max, 3), "higher_is_better": False, "scaling": "weak",
@@ -293,9 +302,10 @@ def run_b200(args, ws, rank, local):
         "gpu_launches": int(launches),
         "stages_ms": {k: round(v, 3) for k, v in stage.items()},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
-                     "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": None,
-                     "peak_kind": pk_kind,
-                     "note": "pass/build are FP32/FP64-pipe bound (SURVEY §8(d)); HBM frac is per the schema"},
+                     "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
+                     "peak_kind": pk_kind, "pipe_util_pct": pipe_util,
+                     "note": "pass/build are FP32-pipe/latency bound (SURVEY §8(d)): the HBM fraction is per the "
+                             "schema; pipe_util_pct = ncu FMA/ALU pipe and issue utilisation of this kernel"},
         "clocks": clk.summary(),
     }
     if rank == 0 and not args.no_cpu_baseline:
