@@ -676,7 +676,10 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
         if (p.ci == 8 && (p.cj == 8 || p.cj == 4) && p.mode == 0) {
             // warp-per-SC kernel (build_warp.cuh) on the cluster-frame staging copy
             {
-                const int rc = run_frame(c, p.cj, nullptr);
+                const bool whole = sc0 == 0 && sc1 == total_sc;
+                const bool halo = !whole && c->jflags_valid && c->jflags_sc0 == sc0 && c->jflags_sc1 == sc1;
+                const int rc = halo ? run_frame(c, p.cj, nullptr, p_lo, p_hi, c->jflags.as<uint8_t>())
+                                    : run_frame(c, p.cj, nullptr);
                 if (rc) return rc;
             }
             A.frame = c->frame.as<const float4>();

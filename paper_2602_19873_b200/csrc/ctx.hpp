@@ -162,7 +162,9 @@ int run_cluster_geometry(sfcnl_cu_ctx* c, uint32_t ci, uint32_t cj, uint64_t p0 
 int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, uint64_t sc1, double max_h);
 int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p);
 // cluster-frame staging copy of the sorted positions (frame.cu); m = payload or null
-int run_frame(sfcnl_cu_ctx* c, uint32_t cj, const double* m);
+// clusters overlapping particles [p_lo, p_hi) plus those flagged in jflags (if non-null)
+int run_frame(sfcnl_cu_ctx* c, uint32_t cj, const double* m, uint64_t p_lo = 0, uint64_t p_hi = ~0ull,
+              const uint8_t* jflags = nullptr);
 int run_halo_mark(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, uint64_t sc1);
 
 // Host helpers shared with the C++ drop-in.

@@ -17,12 +17,17 @@
 namespace sfcnl_cu {
 namespace {
 
+// Clusters [c_lo, c_hi) plus those flagged in jflags (domain decomposition: the
+// rank's own range and its halo; other slots of the global-index arrays are stale).
 __global__ void k_frame(uint64_t n, uint32_t cj, const double* __restrict__ x, const double* __restrict__ y,
-                        const double* __restrict__ z, const double* __restrict__ m, Box box,
-                        float4* __restrict__ frame, unsigned* __restrict__ xmax) {
+                        const double* __restrict__ z, const double* __restrict__ m, Box box, uint64_t c_lo,
+                        uint64_t c_hi, const uint8_t* __restrict__ jflags, float4* __restrict__ frame,
+                        unsigned* __restrict__ xmax) {
     float ax = 0.f, ay = 0.f, az = 0.f;
     for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n; p += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t c0 = (p / cj) * cj;
+        const uint64_t cl = p / cj;
+        if ((cl < c_lo || cl >= c_hi) && !(jflags && jflags[cl])) continue;
+        const uint64_t c0 = cl * cj;
         const double v[3] = {x[p], y[p], z[p]}, o[3] = {x[c0], y[c0], z[c0]};
         float f[3];
 #pragma unroll
@@ -48,15 +53,18 @@ __global__ void k_frame(uint64_t n, uint32_t cj, const double* __restrict__ x, c
 
 }  // namespace
 
-int run_frame(sfcnl_cu_ctx* c, uint32_t cj, const double* m) {
+int run_frame(sfcnl_cu_ctx* c, uint32_t cj, const double* m, uint64_t p_lo, uint64_t p_hi, const uint8_t* jflags) {
     const uint64_t n = c->sorted.n;
+    if (p_hi > n) p_hi = n;
+    const uint64_t c_lo = p_lo / cj, c_hi = (p_hi + cj - 1) / cj;
     SFCNL_CUDA_TRY(c->frame.reserve(std::max<uint64_t>(n, 1) * sizeof(float4)));
     SFCNL_CUDA_TRY(c->frame_x.reserve(4 * sizeof(unsigned)));
     SFCNL_CUDA_TRY(cudaMemsetAsync(c->frame_x.p, 0, 4 * sizeof(unsigned), c->stream));
     if (n) {
         const int grid = int(std::min<uint64_t>((n + 255) / 256, uint64_t(c->num_sms) * 16));
         launch(c, k_frame, dim3(grid), dim3(256), 0, n, cj, c->sorted.x.as<const double>(), c->sorted.y.as<const double>(),
-               c->sorted.z.as<const double>(), m, c->sorted.box, c->frame.as<float4>(), c->frame_x.as<unsigned>());
+               c->sorted.z.as<const double>(), m, c->sorted.box, c_lo, c_hi, jflags, c->frame.as<float4>(),
+               c->frame_x.as<unsigned>());
     }
     return 0;
 }

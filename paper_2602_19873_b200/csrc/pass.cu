@@ -451,7 +451,12 @@ int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p) {
     SFCNL_CUDA_TRY(cudaMemsetAsync(c->derr.p, 0xff, sizeof(DevError), c->stream));
     SFCNL_CUDA_TRY(c->work_ctr.reserve(8));
     if (fast && (p.kernel == SFCNL_KERNEL_DENSITY || p.kernel == SFCNL_KERNEL_COUNT)) {
-        const int rc = run_frame(c, c->sp.cj, A.m);  // staging copy for the item pass
+        // staging copy for the item pass: the store's range (+ its halo clusters)
+        const uint64_t sc0 = c->sc_base, sc1 = c->sc_base + c->num_sc;
+        const bool whole = sc0 == 0 && sc1 == (n + 63) / 64;
+        const bool halo = !whole && c->jflags_valid && c->jflags_sc0 == sc0 && c->jflags_sc1 == sc1;
+        const int rc = halo ? run_frame(c, c->sp.cj, A.m, sc0 * 64, sc1 * 64, c->jflags.as<uint8_t>())
+                            : run_frame(c, c->sp.cj, A.m);
         if (rc) return rc;
         A.frame = c->frame.as<const float4>();
         A.frame_x = c->frame_x.as<const unsigned>();
