@@ -689,7 +689,7 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
             SFCNL_CUDA_TRY(c->work_ctr.reserve(8));
             SFCNL_CUDA_TRY(cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream));
             const unsigned grid = unsigned(std::max<uint64_t>(
-                1, std::min<uint64_t>((num_sc + kBwWarps - 1) / kBwWarps, uint64_t(c->num_sms) * 2)));
+                1, std::min<uint64_t>((num_sc + kBwWarps - 1) / kBwWarps, uint64_t(c->num_sms) * 5)));
             launch(c, k_build_warp, dim3(grid), dim3(kBwWarps * 32), smem, A, sc0, sc1,
                    c->work_ctr.as<unsigned long long>());
         } else {

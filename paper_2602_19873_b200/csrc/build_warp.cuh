@@ -30,22 +30,22 @@
 //     the staging area, bump-allocated into the scratch and copied out.
 // An SC that exceeds a capacity (frontier, entries, bytes) is listed for the
 // global-memory fallback kernel (k_build_global), which runs the generic build_sc.
-constexpr int kBwWarps = 8;
+constexpr int kBwWarps = 4;
 constexpr uint32_t kBwF = 512;   // frontier entries per buffer
-constexpr uint32_t kBwE = 512;   // entries per SC
-constexpr uint32_t kBwBytes = 4096;  // encoded bytes (aliases the staging area)
+constexpr uint32_t kBwE = 384;   // entries per SC (~170 at 200 neighbours)
+constexpr uint32_t kBwBytes = 4096;  // encoded bytes (aliases the frontier)
 
 struct BwSmem {
-    uint32_t fa[kBwF], fb[kBwF];
     union {
         struct {
-            float4 sa[4][32];  // staged j pairs [p][candidate]: {x_2p, x_2p+1, y_2p, y_2p+1}
-            float2 sz[4][32];  //                                 {z_2p, z_2p+1}
-        } st;
-        uint8_t ebuf[kBwBytes];  // encoder output (after the masks)
+            uint32_t fa[kBwF], fb[kBwF];  // traversal frontier, then per-leaf candidate prefix
+        } t;
+        uint8_t ebuf[kBwBytes];  // encoder output (after the masks: the frontier is dead)
     } u;
-    float4 ia[64];   // [ii*8 + b] {x, y, z, -} SC frame
-    float2 it[64];   // [ii*8 + b] {lo, hi} cutoff thresholds with the guard band
+    float4 sa[4][32];  // staged j pairs [p][candidate]: {x_2p, x_2p+1, y_2p, y_2p+1}
+    float2 sz[4][32];  //                                 {z_2p, z_2p+1}
+    float4 ia[64];     // [ii*8 + b] {x, y, z, lo} SC frame + cutoff threshold (guard band below)
+    float ihi[64];     // [ii*8 + b] hi threshold (guard band above)
     float iab[8][6];
     float pthr[8];
     uint32_t cmask[32];
@@ -151,8 +151,8 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
 
     PHASE(0);
     // ---- 2. ordered-frontier BFS (exact fp64 node test)
-    uint32_t* fa = S.fa;
-    uint32_t* fb = S.fb;
+    uint32_t* fa = S.u.t.fa;
+    uint32_t* fb = S.u.t.fb;
     if (lane == 0) fa[0] = 0;
     uint32_t nA = 1;
     __syncwarp();
@@ -308,8 +308,8 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
                     vx = sx + fo[u].x, vy = sy + fo[u].y, vz = sz + fo[u].z;
                     Ej = fmaxf(Ej, fmaxf(fabsf(vx), fmaxf(fabsf(vy), fabsf(vz))));
                 }
-                float* pa = reinterpret_cast<float*>(&S.u.st.sa[jj >> 1][e]) + (jj & 1);
-                float* pz = reinterpret_cast<float*>(&S.u.st.sz[jj >> 1][e]) + (jj & 1);
+                float* pa = reinterpret_cast<float*>(&S.sa[jj >> 1][e]) + (jj & 1);
+                float* pz = reinterpret_cast<float*>(&S.sz[jj >> 1][e]) + (jj & 1);
                 pa[0] = vx, pa[2] = vy, pz[0] = vz;
             }
             Ej = warp_fmax(Ej);
@@ -325,7 +325,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
                     lo = __double2float_rd(rr2 - g);
                     hi = __double2float_ru(rr2 + g);
                 }
-                S.it[(k & 7) * 8 + (k >> 3)] = make_float2(lo, hi);
+                S.ia[(k & 7) * 8 + (k >> 3)].w = lo, S.ihi[(k & 7) * 8 + (k >> 3)] = hi;
             }
             if (lane < nicl) S.pthr[lane] = __double2float_ru(pr2_me + guard_band(pr_me, pr2_me, ecoord));
             if (lane < 32) S.cmask[lane] = 0;
@@ -336,8 +336,8 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
                 float jlo[3] = {1e30f, 1e30f, 1e30f}, jhi[3] = {-1e30f, -1e30f, -1e30f};
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
-                    const float4 a = S.u.st.sa[p][lane];
-                    const float2 z = S.u.st.sz[p][lane];
+                    const float4 a = S.sa[p][lane];
+                    const float2 z = S.sz[p][lane];
                     if (a.x != 1e30f) {
                         jlo[0] = fminf(jlo[0], a.x), jhi[0] = fmaxf(jhi[0], a.x);
                         jlo[1] = fminf(jlo[1], a.z), jhi[1] = fmaxf(jhi[1], a.z);
@@ -359,17 +359,17 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
                     if (!(s2 > S.pthr[b])) pm |= 1u << b;
                 }
             }
-            // items (b << 5 | c), b-major; candidates overlapping the SC's particles last
+            // items (b << 5 | c), candidate-major (one warp scan places each lane's set bits);
+            // candidates overlapping the SC's own particles (i == j possible) last
             const bool self_me = valid && jl0 >= -7 && jl0 < kSC;
-            uint32_t nItems = 0;
-#pragma unroll 1
-            for (int pass = 0; pass < 2; ++pass) {
-                for (uint32_t b = 0; b < nicl; ++b) {
-                    const bool in = ((pm >> b) & 1u) && (self_me == (pass == 1));
-                    const unsigned bal = __ballot_sync(0xffffffffu, in);
-                    if (in) S.items[nItems + __popc(bal & lanemask_lt())] = uint8_t((b << 5) | lane);
-                    nItems += __popc(bal);
-                }
+            const uint32_t npm = __popc(pm);
+            const uint32_t c_ns = self_me ? 0u : npm, c_s = self_me ? npm : 0u;
+            const uint32_t inc_ns = warp_incl_scan(c_ns), inc_s = warp_incl_scan(c_s);
+            const uint32_t tot_ns = __shfl_sync(0xffffffffu, inc_ns, 31);
+            const uint32_t nItems = tot_ns + __shfl_sync(0xffffffffu, inc_s, 31);
+            {
+                uint32_t at = self_me ? tot_ns + inc_s - c_s : inc_ns - c_ns;
+                for (uint32_t m = pm; m; m &= m - 1) S.items[at++] = uint8_t(((__ffs(m) - 1) << 5) | lane);
             }
             __syncwarp();
             PHASE(7);
@@ -387,8 +387,8 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
                 f2 Jz[4];
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
-                    Ja[p] = reinterpret_cast<const ulonglong2&>(S.u.st.sa[p][c]);
-                    Jz[p] = reinterpret_cast<const f2&>(S.u.st.sz[p][c]);
+                    Ja[p] = reinterpret_cast<const ulonglong2&>(S.sa[p][c]);
+                    Jz[p] = reinterpret_cast<const f2&>(S.sz[p][c]);
                 }
                 bool hit = false;
                 uint32_t band_rows = 0;
@@ -397,7 +397,6 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
 #pragma unroll 1
                     for (int ii = 0; ii < 8 && iv && !hit; ++ii) {
                         const float4 I = S.ia[ii * 8 + b];
-                        const float2 T = S.it[ii * 8 + b];
                         const f2 xi2 = f2p(I.x, I.x), yi2 = f2p(I.y, I.y), zi2 = f2p(I.z, I.z);
                         const int iself = kSelf && self ? int(b * 8 + ii) - j0 : -1;
                         float mn = 3.0e38f;
@@ -412,8 +411,8 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
                             }
                             mn = fminf(mn, fminf(d2a, d2b));
                         }
-                        if (mn < T.x) hit = true;
-                        else if (mn <= T.y) band_rows |= 1u << ii;
+                        if (mn < I.w) hit = true;
+                        else if (mn <= S.ihi[ii * 8 + b]) band_rows |= 1u << ii;
                     }
                 };
                 if (__any_sync(0xffffffffu, self)) rows(BoolC<true>());
@@ -552,7 +551,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
     return true;
 }
 
-__global__ void __launch_bounds__(kBwWarps * 32, 2) k_build_warp(const __grid_constant__ BuildArgs A, uint64_t sc_begin,
+__global__ void __launch_bounds__(kBwWarps * 32, 5) k_build_warp(const __grid_constant__ BuildArgs A, uint64_t sc_begin,
                                                                   uint64_t sc_end, unsigned long long* __restrict__ work) {
     extern __shared__ __align__(16) unsigned char dsm[];
     BwSmem& S = reinterpret_cast<BwSmem*>(dsm)[threadIdx.x >> 5];
