@@ -722,8 +722,9 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
         stage_end(c, kBuild);
 #ifdef SFCNL_PHASE_PROF
         {
-            unsigned long long pr[9] = {};
-            cudaMemcpy(pr, A.prof, 9 * 8, cudaMemcpyDeviceToHost);
+            unsigned long long pr[11] = {};
+            cudaMemcpy(pr, A.prof, 11 * 8, cudaMemcpyDeviceToHost);
+            fprintf(stderr, "band items %llu\n", pr[10]);
             fprintf(stderr, "build phases (Gclk): geo %.2f trav %.2f cand %.2f masks-rest %.2f encode %.2f publish %.2f | stage %.2f thr+pref+items %.2f pairs %.2f overflow %llu\n",
                     pr[0] * 1e-9, pr[1] * 1e-9, pr[2] * 1e-9, pr[3] * 1e-9, pr[4] * 1e-9, pr[5] * 1e-9, pr[6] * 1e-9,
                     pr[7] * 1e-9, pr[8] * 1e-9, ctl[1]);

@@ -418,6 +418,9 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
                 if (__any_sync(0xffffffffu, self)) rows(BoolC<true>());
                 else rows(BoolC<false>());
                 if (iv && !hit && band_rows) {
+#ifdef SFCNL_PHASE_PROF
+                    atomicAdd(A.prof + 10, 1ull);
+#endif
                     // guard band: the reference's exact pair predicate, then its prefilter
                     // (neighbor_build.cpp:136-155) -- any exact hit suffices
                     const uint64_t jb = uint64_t(cc) * cj;

@@ -55,6 +55,7 @@ struct PwSmem {
     float iinvh[64];   // density: 1 / h_i
     double acc[64][NO];
     uint32_t cnt[64];
+    float ilo[64], ihi[64];  // per-chunk cutoff thresholds with the guard band
 };
 
 template <int K>
@@ -237,6 +238,21 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                     }
                 }
                 const float E = fmaxf(Ei, warp_fmax(emax));
+                if (!unsafe) {  // per-i thresholds for this chunk (guard band of pass.cu)
+#pragma unroll
+                    for (int s = 0; s < 2; ++s) {
+                        const uint32_t k = lane + 32u * s;
+                        float lo = -1.f, hi = -1.f;
+                        if (k < np) {
+                            const double r = dmul(A.qs, A.h[p0 + k]), r2 = dmul(r, r);
+                            const double ex = 1.1920928955078125e-07 * double(E) + 5.9604644775390625e-08 * r;
+                            const double guard = 4.0 * (1.7881393432617188e-07 * r2 + 3.5 * r * ex + 3.0 * ex * ex) + 1e-300;
+                            lo = __double2float_rd(r2 - guard);
+                            hi = __double2float_ru(r2 + guard);
+                        }
+                        S.ilo[k] = lo, S.ihi[k] = hi;
+                    }
+                }
                 const int self_lo = int(p0) - (CJ - 1);  // j-clusters overlapping [p0, p0 + 64)
                 const int jf = int(my_idx) * CJ - self_lo;
                 const unsigned selfm = __ballot_sync(0xffffffffu, have && jf >= 0 && jf < kSC + CJ - 1);
@@ -247,11 +263,11 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                     if (!mine) continue;
                     const int li = int(b * 8 + il);
                     const uint64_t i = p0 + uint64_t(li);
-                    const double r = uint32_t(li) < np ? dmul(A.qs, A.h[p0 + li]) : -1.0;
-                    const double r2 = dmul(r, r);
-                    const bool active = r >= 0.0;
+                    const bool active = uint32_t(li) < np;
                     uint32_t cnt = 0;
                     if (unsafe) {
+                        const double r = active ? dmul(A.qs, A.h[i]) : -1.0;
+                        const double r2 = dmul(r, r);
                         // every slot through the reference predicate + fp64 kernel
                         double* side = &S.acc[li][0];
                         while (mine) {
@@ -275,13 +291,7 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                         __syncwarp();
                         continue;
                     }
-                    float lo = -1.f, hi_t = -1.f;
-                    if (active) {
-                        const double ex = 1.1920928955078125e-07 * double(E) + 5.9604644775390625e-08 * r;
-                        const double guard = 4.0 * (1.7881393432617188e-07 * r2 + 3.5 * r * ex + 3.0 * ex * ex) + 1e-300;
-                        lo = __double2float_rd(r2 - guard);
-                        hi_t = __double2float_ru(r2 + guard);
-                    }
+                    const float lo = S.ilo[li], hi_t = S.ihi[li];
                     const float fxi = S.ix[li], fyi = S.iy[li], fzi = S.iz[li];
                     const f2 xi2 = f2p(fxi, fxi), yi2 = f2p(fyi, fyi), zi2 = f2p(fzi, fzi);
                     f2 lxi2 = 0, lyi2 = 0, lzi2 = 0;
@@ -346,7 +356,8 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                                 return;
                             }
                         }
-                        const int rc = rare_slot<K>(A, i, j, r2, &S.acc[li][0]);
+                        const double r = dmul(A.qs, A.h[i]);
+                        const int rc = rare_slot<K>(A, i, j, dmul(r, r), &S.acc[li][0]);
                         cnt += rc > 0, coincident |= rc < 0;
                     };
                     auto compute = [&](uint32_t e, const Ld& L, auto SELF) {
@@ -427,19 +438,29 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                         ms &= ms - 1;
                         compute(e, load(e), BoolC<true>());
                     }
-                    // flush: pair halves, then the four j-quarter lanes of each i
+                    // flush: pair halves and the four j-quarter lanes of each i in fp32 (<= 2 x 64
+                    // terms per lane), added to the per-i fp64 sums; fp64 close-pair sums separately
                     double tot[NO];
                     const f2 accs[4] = {acc0, acc1, acc2, acc3};
-                    const double accds[4] = {accd0, accd1, accd2, accd3};
 #pragma unroll
                     for (int o = 0; o < NO; ++o) {
                         float a, c;
                         f2u(accs[o], a, c);
-                        const double sc_o = K == SFCNL_KERNEL_LJ ? (o < 3 ? eps24d : eps4d) : 1.0;
-                        double v = (double(a) + double(c)) * sc_o + (LJ ? accds[o] : 0.0);
+                        float v = a + c;
                         v += __shfl_xor_sync(0xffffffffu, v, 1);
                         v += __shfl_xor_sync(0xffffffffu, v, 2);
-                        tot[o] = v;
+                        const double sc_o = K == SFCNL_KERNEL_LJ ? (o < 3 ? eps24d : eps4d) : 1.0;
+                        tot[o] = double(v) * sc_o;
+                    }
+                    if (LJ && __any_sync(0xffffffffu, accd0 != 0.0 || accd1 != 0.0 || accd2 != 0.0 || accd3 != 0.0)) {
+                        double accds[4] = {accd0, accd1, accd2, accd3};
+#pragma unroll
+                        for (int o = 0; o < NO; ++o) {
+                            double v = accds[o];
+                            v += __shfl_xor_sync(0xffffffffu, v, 1);
+                            v += __shfl_xor_sync(0xffffffffu, v, 2);
+                            tot[o] += v;
+                        }
                     }
                     {
                         float c0, c1;
