@@ -55,7 +55,7 @@ def dist_init(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1:
+    if ws > 1 or os.environ.get("SFCNL_BENCH_FORCE_DIST"):
         import torch
         import torch.distributed as dist
         backend = os.environ.get("SFCNL_BENCH_BACKEND", "nccl")  # gloo: several ranks on one GPU (testing)
@@ -414,11 +414,11 @@ def main():
     ws, rank, local = dist_init(args)
     if args.impl == "reference":
         run_reference(args, ws, rank)
-    elif ws > 1:
+    elif ws > 1 or os.environ.get("SFCNL_BENCH_FORCE_DIST"):
         run_b200_distributed(args, ws, rank, local)
     else:
         run_b200(args, ws, rank, local)
-    if ws > 1:
+    if ws > 1 or os.environ.get("SFCNL_BENCH_FORCE_DIST"):
         import torch.distributed as dist
         dist.destroy_process_group()
 

@@ -500,19 +500,6 @@ __device__ bool halo_sc(const BuildArgs& A, const Workspace& W, uint64_t sc, uin
     return true;
 }
 
-__global__ void __launch_bounds__(kBuildThreads) k_halo_smem(const __grid_constant__ BuildArgs A, uint64_t sc_begin, uint64_t sc_end,
-                                                             uint8_t* jflags) {
-    __shared__ uint32_t front[2 * kFCap];
-    const Workspace W{front, front + kFCap, nullptr, nullptr, nullptr, kFCap, 0, 0, false};
-    for (uint64_t sc = sc_begin + blockIdx.x; sc < sc_end; sc += gridDim.x) {
-        if (!halo_sc(A, W, sc, jflags) && threadIdx.x == 0) {
-            const unsigned long long slot = atomicAdd(&A.ctl[1], 1ull);
-            A.overflow_list[slot] = uint32_t(sc);
-        }
-        __syncthreads();
-    }
-}
-
 __global__ void __launch_bounds__(kBuildThreads) k_halo_global(const __grid_constant__ BuildArgs A, const uint32_t* list, uint64_t count,
                                                                uint32_t* ws, uint32_t fcap, uint8_t* jflags) {
     uint32_t* base = ws + uint64_t(blockIdx.x) * 2 * fcap;
@@ -791,8 +778,11 @@ int run_halo_mark(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, ui
         A.ctl = c->build_ctl.as<unsigned long long>();
         A.overflow_list = c->overflow_list.as<uint32_t>();
         A.err = c->derr.as<DevError>();
-        const unsigned grid = unsigned(std::min<uint64_t>(sc1 - sc0, uint64_t(c->num_sms) * 16));
-        launch(c, k_halo_smem, dim3(grid), dim3(kBuildThreads), 0, A, sc0, sc1, c->jflags.as<uint8_t>());
+        SFCNL_CUDA_TRY(c->work_ctr.reserve(8));
+        SFCNL_CUDA_TRY(cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream));
+        const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((sc1 - sc0 + 7) / 8, uint64_t(c->num_sms) * 3)));
+        launch(c, k_halo_warp, dim3(grid), dim3(256), 0, A, sc0, sc1, c->jflags.as<uint8_t>(),
+               c->work_ctr.as<unsigned long long>());
         SFCNL_CUDA_TRY(cudaGetLastError());
         unsigned long long ctl[2];
         SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 2 * 8, cudaMemcpyDeviceToHost, c->stream));

@@ -67,6 +67,74 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
+// Ordered-frontier BFS of one SC over the octree (collect_candidates,
+// neighbor_build.cpp:43-65) by one warp: 32 nodes per step, exact fp64 aabb_dist_sq;
+// warp scans place children and tagged accepted leaves, so the accepted leaves end
+// up in key order in *out (one of the two buffers). Returns their number, or ~0u
+// when the frontier exceeds kBwF.
+__device__ __forceinline__ uint32_t warp_bfs(const BuildArgs& A, const Geo& scg, double r2, uint32_t* fa,
+                                             uint32_t* fb, uint32_t** out) {
+    const unsigned lane = lane_id();
+    if (lane == 0) fa[0] = 0;
+    uint32_t nA = 1;
+    __syncwarp();
+    for (;;) {
+        uint32_t nB = 0;
+        bool expanded = false;
+        for (uint32_t base = 0; base < nA; base += 32) {
+            const uint32_t k = base + lane;
+            uint32_t emit = 0, e = 0;
+            int32_t fc = -1;
+            if (k < nA) {
+                e = fa[k];
+                if (e & kTag) {
+                    emit = 1;
+                } else {
+                    const Node nd = A.nodes[e];
+                    if (nd.pend > nd.pbegin) {
+                        const Geo ng = A.ngeo[e];
+                        if (!(aabb_dist_sq(scg, ng, A.box) > r2)) {
+                            fc = nd.first_child;
+                            emit = fc < 0 ? 1 : 8;
+                        }
+                    }
+                }
+            }
+            const uint32_t inc = warp_incl_scan(emit);
+            const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+            if (nB + tot > kBwF) return ~0u;
+            const uint32_t at = nB + inc - emit;
+            if (emit == 1) fb[at] = e | kTag;
+            if (emit == 8) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) fb[at + c] = uint32_t(fc + c);
+            }
+            expanded |= __any_sync(0xffffffffu, emit == 8);
+            nB += tot;
+        }
+        __syncwarp();
+        uint32_t* t = fa;
+        fa = fb, fb = t;
+        nA = nB;
+        if (!expanded) break;
+    }
+    *out = fa;
+    return nA;
+}
+
+// SC box = sequential union of its i-cluster boxes (neighbor_build.cpp:113-118) and the
+// traversal radius; every lane.
+__device__ __forceinline__ void sc_box(const BuildArgs& A, uint64_t icl_base, uint32_t nicl, Geo& scg, double& r2) {
+    geo_init(scg);
+    for (uint32_t b = 0; b < nicl; ++b) {
+        const Geo g = A.igeo[icl_base + b];
+        geo_extend(scg, g);
+        scg.maxh = smax(scg.maxh, g.maxh);
+    }
+    const double r = dmul(A.scale, scg.maxh);
+    r2 = dmul(r, r);
+}
+
 // Returns false when a capacity is exceeded (nothing published).
 #ifdef SFCNL_PHASE_PROF
 #define PHASE(k)                                                                   \
@@ -94,14 +162,8 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
 
     // ---- 1. SC geometry (sequential union, as sc_geometry) and the i side
     Geo scg;
-    geo_init(scg);
-    for (uint32_t b = 0; b < nicl; ++b) {
-        const Geo g = A.igeo[icl_base + b];
-        geo_extend(scg, g);
-        scg.maxh = smax(scg.maxh, g.maxh);
-    }
-    const double r_sc = dmul(A.scale, scg.maxh);
-    const double r2 = dmul(r_sc, r_sc);
+    double r2;
+    sc_box(A, icl_base, nicl, scg, r2);
     const double ox = A.x[p0], oy = A.y[p0], oz = A.z[p0];
     auto rel = [&](double v, double o, int d) {
         double r = dsub(v, o);
@@ -151,51 +213,10 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
 
     PHASE(0);
     // ---- 2. ordered-frontier BFS (exact fp64 node test)
-    uint32_t* fa = S.u.t.fa;
-    uint32_t* fb = S.u.t.fb;
-    if (lane == 0) fa[0] = 0;
-    uint32_t nA = 1;
-    __syncwarp();
-    for (;;) {
-        uint32_t nB = 0;
-        bool expanded = false;
-        for (uint32_t base = 0; base < nA; base += 32) {
-            const uint32_t k = base + lane;
-            uint32_t emit = 0, e = 0;
-            int32_t fc = -1;
-            if (k < nA) {
-                e = fa[k];
-                if (e & kTag) {
-                    emit = 1;
-                } else {
-                    const Node nd = A.nodes[e];
-                    if (nd.pend > nd.pbegin) {
-                        const Geo ng = A.ngeo[e];
-                        if (!(aabb_dist_sq(scg, ng, A.box) > r2)) {
-                            fc = nd.first_child;
-                            emit = fc < 0 ? 1 : 8;
-                        }
-                    }
-                }
-            }
-            const uint32_t inc = warp_incl_scan(emit);
-            const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
-            if (nB + tot > kBwF) return false;
-            const uint32_t at = nB + inc - emit;
-            if (emit == 1) fb[at] = e | kTag;
-            if (emit == 8) {
-#pragma unroll
-                for (int c = 0; c < 8; ++c) fb[at + c] = uint32_t(fc + c);
-            }
-            expanded |= __any_sync(0xffffffffu, emit == 8);
-            nB += tot;
-        }
-        __syncwarp();
-        uint32_t* t = fa;
-        fa = fb, fb = t;
-        nA = nB;
-        if (!expanded) break;
-    }
+    uint32_t* fa;
+    const uint32_t nA = warp_bfs(A, scg, r2, S.u.t.fa, S.u.t.fb, &fa);
+    if (nA == ~0u) return false;
+    uint32_t* fb = fa == S.u.t.fa ? S.u.t.fb : S.u.t.fa;
 
     PHASE(1);
     // ---- 3. candidate ranges per accepted leaf: fa[k] <- first candidate, fb[k] <- prefix
@@ -570,6 +591,42 @@ __global__ void __launch_bounds__(kBwWarps * 32, 5) k_build_warp(const __grid_co
                 A.overflow_list[slot] = uint32_t(sc);
                 A.counts[sc] = 0, A.sizes[sc] = 0, A.soff[sc] = 0;
             }
+        }
+        __syncwarp();
+    }
+}
+
+// Halo marking for a domain decomposition: the candidate j-clusters of
+// the range's SCs, i.e. the clusters of every leaf the build's traversal accepts, are
+// flagged. Warp per SC (same BFS as the build); SCs whose frontier overflows are
+// listed for the global-memory fallback (k_halo_global).
+__global__ void __launch_bounds__(256) k_halo_warp(const __grid_constant__ BuildArgs A, uint64_t sc_begin, uint64_t sc_end,
+                                                   uint8_t* __restrict__ jflags, unsigned long long* __restrict__ work) {
+    __shared__ uint32_t fr[8][2 * kBwF];
+    const unsigned lane = lane_id(), w = threadIdx.x >> 5;
+    for (;;) {
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(work, 1ull);
+        const uint64_t sc = sc_begin + __shfl_sync(0xffffffffu, t, 0);
+        if (sc >= sc_end) break;
+        const uint64_t icl_base = sc * A.icl_per_sc;
+        const uint32_t nicl = uint32_t(tmin<uint64_t>(icl_base + A.icl_per_sc, A.num_icl) - icl_base);
+        Geo scg;
+        double r2;
+        sc_box(A, icl_base, nicl, scg, r2);
+        uint32_t* fa;
+        const uint32_t nA = warp_bfs(A, scg, r2, fr[w], fr[w] + kBwF, &fa);
+        if (nA == ~0u) {
+            if (lane == 0) {
+                const unsigned long long slot = atomicAdd(&A.ctl[1], 1ull);
+                A.overflow_list[slot] = uint32_t(sc);
+            }
+            __syncwarp();
+            continue;
+        }
+        for (uint32_t k = lane; k < nA; k += 32) {
+            const Node nd = A.nodes[fa[k] & ~kTag];
+            for (uint32_t j = nd.pbegin / A.cj; j <= (nd.pend - 1) / A.cj; ++j) jflags[j] = 1;
         }
         __syncwarp();
     }

@@ -36,6 +36,8 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
+import os
+
 import numpy as np
 
 from .api import (BuildParams, Context, Kernel, NeighborStore, ParticleSet, PassConfig, ReduceResult,
@@ -242,8 +244,19 @@ class DomainDecomposition:
         E, comm = self.E, self.comm
         P, r = comm.world, comm.rank
         dev = E.device
+        prof = os.environ.get("SFCNL_DD_PROF") is not None and dev.type == "cuda"
+        marks = []
+
+        def mark(name):
+            if prof:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record()
+                marks.append((name, ev))
+
+        mark("start")
         # (1) local keys
         keys = E.local_sort()
+        mark("local_sort")
         n_l = int(keys.numel())
         counts = comm.all_gather(torch.tensor([n_l], dtype=torch.int64, device=dev)).view(-1).tolist()
         N = int(sum(counts))
@@ -270,18 +283,23 @@ class DomainDecomposition:
             take = torch.minimum(torch.clamp(need.unsqueeze(0) - eq_before, min=0), eq_all)
             cut[:, 1:P] = less_all + take
         cut[:, P] = torch.tensor(counts, dtype=torch.int64, device=dev)
+        mark("split")
         cut_h = cut.cpu().numpy()
         send = np.diff(cut_h[r]).tolist()
         recv = [int(cut_h[s, r + 1] - cut_h[s, r]) for s in range(P)]
         # (3) payload to owners
         moved = comm.all_to_all_v(E.payload(), send, recv)
+        mark("payload_a2a")
         # (4) owners place their particles at global positions [p0, p1)
         p0, p1 = pb[r], pb[r + 1]
         assert moved.shape[0] == p1 - p0, "distributed split lost particles"
         own_keys = E.own(moved, N, p0)
+        mark("own_sort_place")
         # (5) global keys -> global octree
         gkeys = comm.all_gather_v(own_keys, [pb[q + 1] - pb[q] for q in range(P)])
+        mark("gather_keys")
         nn = E.octree(gkeys, self.bucket)
+        mark("octree")
         # (6) node geometry: partial over owned particles, exact MIN all-reduce
         geo = E.node_geometry_partial(p0, p1)
         geo[:, 3:7].neg_()
@@ -289,6 +307,7 @@ class DomainDecomposition:
         geo[:, 3:7].neg_()
         E.set_node_geometry(geo)
         max_h = float(geo[0, 6]) if nn else 0.0  # root max h = max over all particles
+        mark("node_geometry")
         # (7) halo exchange
         sc0, sc1 = scb[r], scb[r + 1]
         halo = 0
@@ -313,9 +332,16 @@ class DomainDecomposition:
             keep = widx < N
             E.scatter_rows(widx[keep], back[keep])
             halo = int(keep.sum())
+        mark("halo")
         # (8) range build + pass
         store = E.build_range(self.bp, sc0, sc1, max_h, download)
+        mark("build")
         results = [E.reduce(k, self.cfg, p1 - p0, download) for k in self.kernels]
+        mark("passes")
+        if prof:
+            marks[-1][1].synchronize()
+            print("dd phases ms:", {b[0]: round(a[1].elapsed_time(b[1]), 2) for a, b in zip(marks, marks[1:])},
+                  flush=True)
         return RankResult(r, N, p0, p1, sc0, sc1, nn, halo, store, results)
 
 
