@@ -187,6 +187,11 @@ int sfcnl_cu_reduce(sfcnl_cu_ctx* ctx, const sfcnl_pass_params* params, double* 
 int sfcnl_cu_build_store_range(sfcnl_cu_ctx* ctx, const sfcnl_build_params* params, uint64_t sc_begin,
                                uint64_t sc_end, double max_h, uint64_t* num_superclusters,
                                uint64_t* blob_bytes);
+/* Input slot from a DEVICE row-major [n, ncols] record array whose columns are
+ * x, y, z, h and then the ncols - 4 named fields (the layout an all-to-all of
+ * particle rows delivers); same effect as set_particles + set_field. */
+int sfcnl_cu_set_particle_records(sfcnl_cu_ctx* ctx, uint64_t n, const double* records, int ncols,
+                                  const char* const* fields, const sfcnl_box* box);
 /* Allocate the sorted slot for n particles with the named extra fields (contents
  * undefined) so ranks can fill it piecewise with write_sorted. Invalidates the
  * store. */

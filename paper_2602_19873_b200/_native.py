@@ -81,6 +81,7 @@ EXPORTS = [
     "sfcnl_make_evrard", "sfcnl_cu_build_store_range", "sfcnl_cu_alloc_sorted", "sfcnl_cu_write_sorted",
     "sfcnl_cu_read_sorted", "sfcnl_cu_read_order", "sfcnl_cu_set_keys", "sfcnl_cu_apply_order_into",
     "sfcnl_cu_node_geometry_range", "sfcnl_cu_halo_mark", "sfcnl_cu_device_array",
+    "sfcnl_cu_set_particle_records",
 ]
 
 _lib = None
@@ -141,6 +142,7 @@ def lib():
         "sfcnl_cu_node_geometry_range": (C.c_int, [P, u64, u64]),
         "sfcnl_cu_halo_mark": (C.c_int, [P, C.POINTER(BuildParamsC), u64, u64, C.POINTER(u64)]),
         "sfcnl_cu_device_array": (C.c_int, [P, C.c_char_p, C.POINTER(P), C.POINTER(u64)]),
+        "sfcnl_cu_set_particle_records": (C.c_int, [P, u64, P, C.c_int, C.POINTER(C.c_char_p), C.POINTER(Box)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

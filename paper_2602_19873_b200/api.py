@@ -397,6 +397,13 @@ class Context:
         for name, p in zip(names, ptr[4:]):
             self.check(self.L.sfcnl_cu_set_field(self.h, name.encode(), p))
 
+    def set_particle_records(self, n, rec, names, box: SimulationBox):
+        """Orig slot from a device row-major [n, 4 + len(names)] float64 tensor."""
+        b = box.c()
+        arr = (C.c_char_p * max(len(names), 1))(*[f.encode() for f in names])
+        self.check(self.L.sfcnl_cu_set_particle_records(self.h, int(n), int(rec.data_ptr()), int(rec.shape[1]), arr,
+                                                        C.byref(b)))
+
     def alloc_sorted(self, n, box: SimulationBox, fields):
         b = box.c()
         arr = (C.c_char_p * max(len(fields), 1))(*[f.encode() for f in fields])

@@ -60,6 +60,12 @@ void stage_end(sfcnl_cu_ctx* c, Stage s) {
     if (c->timing) cudaEventRecord(c->ev[2 * s + 1], c->stream);
 }
 
+// Row-major [n, ncols] records -> ncols SoA columns (one pass).
+__global__ void k_unpack_records(uint64_t n, int ncols, const double* __restrict__ rec, double* const* __restrict__ dst) {
+    for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n; k += uint64_t(gridDim.x) * blockDim.x)
+        for (int a = 0; a < ncols; ++a) dst[a][k] = rec[k * ncols + a];
+}
+
 }  // namespace sfcnl_cu
 
 namespace {
@@ -105,6 +111,8 @@ int set_slot(sfcnl_cu_ctx* c, Slot& s, uint64_t n, const double* x, const double
     s.valid = false;
     s.n = n;
     s.box = make_box(box);
+    // keep the field allocations for the next set_field of the same name (no cudaFree/cudaMalloc per step)
+    for (auto& f : s.fields) c->field_pool.push_back(std::move(f));
     s.fields.clear();
     drop_external(c);
     if (int rc = upload(c, s.x, x, n * 8)) return rc;
@@ -123,6 +131,12 @@ int set_slot_field(sfcnl_cu_ctx* c, Slot& s, const char* name, const double* v) 
         s.fields.emplace_back();
         f = &s.fields.back();
         f->name = name;
+        for (auto it = c->field_pool.begin(); it != c->field_pool.end(); ++it)
+            if (it->name == f->name) {
+                f->data = std::move(it->data);
+                c->field_pool.erase(it);
+                break;
+            }
     }
     return upload(c, f->data, v, s.n * 8);
 }
@@ -241,6 +255,43 @@ int sfcnl_cu_set_sorted_particles(sfcnl_cu_ctx* c, uint64_t n, const double* x, 
                                   const double* z, const double* h, const sfcnl_box* box) {
     CallScope scope(c);
     if (int rc = set_slot(c, c->sorted, n, x, y, z, h, box)) return rc;
+    return finish(c);
+}
+
+int sfcnl_cu_set_particle_records(sfcnl_cu_ctx* c, uint64_t n, const double* rec, int ncols,
+                                  const char* const* fields, const sfcnl_box* box) {
+    CallScope scope(c);
+    if (ncols < 4) return set_error(c, SFCNL_INPUT_ERROR, "set_particle_records: need x, y, z, h columns");
+    if (n && !rec) return set_error(c, SFCNL_INPUT_ERROR, "null particle array");
+    if (int rc = check_box(c, box)) return rc;
+    Slot& s = c->orig;
+    c->has_order = false;
+    s.valid = false;
+    s.n = n;
+    s.box = make_box(box);
+    drop_external(c);
+    SFCNL_CUDA_TRY(s.x.reserve(n * 8));
+    SFCNL_CUDA_TRY(s.y.reserve(n * 8));
+    SFCNL_CUDA_TRY(s.z.reserve(n * 8));
+    SFCNL_CUDA_TRY(s.h.reserve(n * 8));
+    std::vector<Field> nf(ncols - 4);
+    for (int k = 0; k < ncols - 4; ++k) {
+        if (!fields || !fields[k]) return set_error(c, SFCNL_INPUT_ERROR, "set_particle_records: null field name");
+        nf[k].name = fields[k];
+        if (Field* old = s.find(fields[k])) nf[k].data = std::move(old->data);
+        SFCNL_CUDA_TRY(nf[k].data.reserve(n * 8));
+    }
+    s.fields = std::move(nf);
+    std::vector<void*> host{s.x.p, s.y.p, s.z.p, s.h.p};
+    for (auto& f : s.fields) host.push_back(f.data.p);
+    SFCNL_CUDA_TRY(c->ptrs.reserve(ncols * sizeof(void*)));
+    SFCNL_CUDA_TRY(cudaMemcpyAsync(c->ptrs.p, host.data(), ncols * sizeof(void*), cudaMemcpyHostToDevice, c->stream));
+    if (n) {
+        const int grid = int(std::min<uint64_t>((n + 255) / 256, uint64_t(c->num_sms) * 16));
+        launch(c, k_unpack_records, dim3(grid), dim3(256), 0, n, ncols, rec, (double* const*)c->ptrs.as<void*>());
+        SFCNL_CUDA_TRY(cudaGetLastError());
+    }
+    s.valid = true;
     return finish(c);
 }
 

@@ -78,6 +78,7 @@ struct sfcnl_cu_ctx {
     int num_sms = 148;
 
     sfcnl_cu::Slot orig, sorted;
+    std::vector<sfcnl_cu::Field> field_pool;  // allocations of fields dropped by set_particles, reused by name
 
     // (1) order
     bool has_order = false;

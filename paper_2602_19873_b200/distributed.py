@@ -170,8 +170,7 @@ class CudaEngine:
     def own(self, recv, n_total, p0):
         torch = _torch()
         n = recv.shape[0]
-        cols = [recv[:, f].contiguous() for f in range(recv.shape[1])]
-        self.ctx.set_particles_device(n, cols, self.fields, self.box)
+        self.ctx.set_particle_records(n, recv.contiguous(), self.fields, self.box)
         self.ctx.sort(self.bits)
         self.ctx.alloc_sorted(n_total, self.box, self.fields)
         self.ctx.apply_order_into(p0)

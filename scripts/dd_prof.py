@@ -14,7 +14,7 @@ box = S.SimulationBox((0.0, 0.0, 0.0), (1.0, 1.0, 1.0), (True, True, True))
 E = CudaEngine(ctx, box, ["m"]); E.upload(ps)
 dd = DomainDecomposition(E, Comm(), S.BuildParams(S.ClusterParams(8, 8, 32), S.GATHER, True, 1.0),
                          [S.sph_density_kernel(), S.lj_kernel(1.0, 0.5 * (1.0 / n) ** (1 / 3))], S.PassConfig(1.0, S.MIXED))
-for it in range(3):
+for it in range(6):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     dd.run(download=False)
     torch.cuda.synchronize(); print("step wall ms", round((time.perf_counter() - t0) * 1e3, 1), flush=True)
