@@ -230,7 +230,9 @@ int sfcnl_cu_halo_mark(sfcnl_cu_ctx* ctx, const sfcnl_build_params* params, uint
                        uint64_t sc_end, uint64_t* num_jclusters);
 /* Device pointer + byte length of an internal array for zero-copy collectives:
  * "x","y","z","h", sorted fields by name, "keys","perm","nodes","node_geo",
- * "halo_flags","out0".."out3","count". Valid until the next call that resizes it. */
+ * "halo_flags","out0".."out3","count", the input slot "orig.x".."orig.h" and
+ * "orig.<field>", the store "store.counts","store.offsets","store.blob".
+ * Valid until the next call that resizes it. */
 int sfcnl_cu_device_array(sfcnl_cu_ctx* ctx, const char* name, void** ptr, uint64_t* bytes);
 
 /* ---- host-side codec (no device work) ----------------------------------------

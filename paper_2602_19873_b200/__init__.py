@@ -9,4 +9,4 @@ from .api import *  # noqa: F401,F403
 from .api import (BuildError, BuildParams, ClusterParams, Context, DecodeError, EvrardSpec,  # noqa: F401
                   InputError, NeighborStore, Octree, ParticleSet, PassConfig, ReduceResult,
                   SfcOrder, SimulationBox, UniformSpec)
-from .pipeline import Pipeline  # noqa: F401
+from .pipeline import Pipeline, StreamedPipeline  # noqa: F401

@@ -592,7 +592,19 @@ int sfcnl_cu_device_array(sfcnl_cu_ctx* c, const char* name, void** ptr, uint64_
     else if (nm.rfind("out", 0) == 0 && nm.size() == 4 && nm[3] >= '0' && nm[3] <= '3')
         b = &c->outs[nm[3] - '0'], len = pass_out_count(c) * 8;
     else if (nm == "count") b = &c->ncount, len = pass_out_count(c) * 4;
-    else if (c->sorted.valid && (b = sorted_array(c, name))) len = c->sorted.n * 8;
+    else if (nm == "store.counts" && c->has_store) b = &c->counts, len = c->num_sc * 4;
+    else if (nm == "store.offsets" && c->has_store) b = &c->offsets, len = (c->num_sc + 1) * 8;
+    else if (nm == "store.blob" && c->has_store) b = &c->blob, len = c->blob_bytes;
+    else if (nm.rfind("orig.", 0) == 0 && c->orig.valid) {
+        const std::string f = nm.substr(5);
+        Slot& o = c->orig;
+        if (f == "x") b = &o.x;
+        else if (f == "y") b = &o.y;
+        else if (f == "z") b = &o.z;
+        else if (f == "h") b = &o.h;
+        else if (Field* fl = o.find(f)) b = &fl->data;
+        len = o.n * 8;
+    } else if (c->sorted.valid && (b = sorted_array(c, name))) len = c->sorted.n * 8;
     if (!b || (len && len > b->bytes)) return set_error(c, SFCNL_INPUT_ERROR, "device_array: no such array: " + nm);
     *ptr = b->p;
     if (bytes) *bytes = len;
