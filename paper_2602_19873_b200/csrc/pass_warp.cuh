@@ -370,8 +370,10 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                         }
                         float ma = fset_lt(d2a, lo), mb = fset_lt(d2b, lo);
                         // special: inside the guard band [lo, hi], or (LJ) closer than close2
-                        const bool sa = (LJ && d2a < close2) || (!(d2a < lo) && d2a <= hi_t);
-                        const bool sb = (LJ && d2b < close2) || (!(d2b < lo) && d2b <= hi_t);
+                        // (bitwise, branch-free predicate logic; close2 < lo in every practical case,
+                        // and a close slot beyond lo is just routed to the reference path)
+                        const bool sa = (d2a <= hi_t) & ((LJ & (d2a < close2)) | !(d2a < lo));
+                        const bool sb = (d2b <= hi_t) & ((LJ & (d2b < close2)) | !(d2b < lo));
                         if (sa | sb) {
                             if (sa) special(e, 0, d2a), ma = 0.f;
                             if (sb) special(e, 1, d2b), mb = 0.f;
