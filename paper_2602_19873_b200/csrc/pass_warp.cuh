@@ -45,9 +45,9 @@ struct PwSmem {
     static constexpr bool LJ = (K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB);
     static constexpr int NO = nout<K>();
     static constexpr int kMinBlocks = LJ ? 4 : 6;  // CTAs of 4 warps per SM (registers: 128 / 85)
-    float sj[kPwChunk * 32];              // hi x,y,z + payload
-    float4 sl4[LJ ? kPwChunk * 4 : 1];    // lo (LJ) per (entry, j-quarter): {lx_a, lx_b, ly_a, ly_b}
-    float2 sl2[LJ ? kPwChunk * 4 : 1];    //                                  {lz_a, lz_b}
+    // per (entry, j-quarter): density/count 8 floats {x_a,x_b,y_a,y_b,z_a,z_b,m_a,m_b};
+    // LJ 12 floats {x_a,x_b,y_a,y_b, z_a,z_b,lx_a,lx_b, ly_a,ly_b,lz_a,lz_b} (hi, then lo)
+    float sj[kPwChunk * 4 * (LJ ? 12 : 8)];
     uint32_t idx[64];                     // decoded block
     float ix[64], iy[64], iz[64];
     float ilx[LJ ? 64 : 1], ily[LJ ? 64 : 1], ilz[LJ ? 64 : 1];
@@ -208,7 +208,6 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                         for (int u = 0; u < 4; ++u) {
                             const uint32_t e = uint32_t(k0 + u) * 4 + (lane >> 3), jj = lane & 7;
                             if (e >= n) continue;
-                            const uint32_t o = e * 32 + (jj & 3) * 8 + (jj >> 2);
                             float fx = kFar, fy = kFar, fz = kFar, fm = 0.f, lx = 0.f, ly = 0.f, lz = 0.f;
                             if (val[u]) {
                                 const double qx = rel(vx[u], ox, 0), qy = rel(vy[u], oy, 1), qz = rel(vz[u], oz, 2);
@@ -217,22 +216,14 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                                 if (LJ) lx = float(qx - double(fx)), ly = float(qy - double(fy)), lz = float(qz - double(fz));
                                 emax = fmaxf(emax, fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz))));
                             }
-                            if (jj < 4 || CJ == 8) {
-                                sj[o] = fx, sj[o + 2] = fy, sj[o + 4] = fz, sj[o + 6] = fm;
-                                if (LJ) {
-                                    float* l4 = reinterpret_cast<float*>(&S.sl4[e * 4 + (jj & 3)]) + (jj >> 2);
-                                    float* l2 = reinterpret_cast<float*>(&S.sl2[e * 4 + (jj & 3)]) + (jj >> 2);
-                                    l4[0] = lx, l4[2] = ly, l2[0] = lz;
-                                }
+                            const uint32_t q = jj & 3, hb = (jj < 4 || CJ == 8) ? (jj >> 2) : 1u;
+                            if (!(jj < 4 || CJ == 8)) fx = fy = fz = kFar, fm = 0.f, lx = ly = lz = 0.f;  // cj == 4: slot b is a far dummy
+                            if (LJ) {
+                                float* p = sj + (e * 4 + q) * 12 + hb;
+                                p[0] = fx, p[2] = fy, p[4] = fz, p[6] = lx, p[8] = ly, p[10] = lz;
                             } else {
-                                // cj == 4: slot b of every quarter is a far dummy
-                                const uint32_t ob = e * 32 + (jj & 3) * 8 + 1;
-                                sj[ob] = kFar, sj[ob + 2] = kFar, sj[ob + 4] = kFar, sj[ob + 6] = 0.f;
-                                if (LJ) {
-                                    float* l4 = reinterpret_cast<float*>(&S.sl4[e * 4 + (jj & 3)]) + 1;
-                                    float* l2 = reinterpret_cast<float*>(&S.sl2[e * 4 + (jj & 3)]) + 1;
-                                    l4[0] = 0.f, l4[2] = 0.f, l2[0] = 0.f;
-                                }
+                                float* p = sj + (e * 4 + q) * 8 + hb;
+                                p[0] = fx, p[2] = fy, p[4] = fz, p[6] = fm;
                             }
                         }
                     }
@@ -310,19 +301,20 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                     };
                     auto load = [&](uint32_t e) {
                         Ld L;
-                        const ulonglong2 P0 = reinterpret_cast<const ulonglong2*>(S.sj)[e * 8 + jq * 2];
-                        const ulonglong2 P1 = reinterpret_cast<const ulonglong2*>(S.sj)[e * 8 + jq * 2 + 1];
+                        const ulonglong2* pb = reinterpret_cast<const ulonglong2*>(S.sj + (e * 4 + jq) * (LJ ? 12 : 8));
+                        const ulonglong2 P0 = pb[0], P1 = pb[1];
                         L.dx = f2sub(xi2, P0.x);
                         L.dy = f2sub(yi2, P0.y);
                         L.dz = f2sub(zi2, P1.x);
                         if (LJ) {
-                            const ulonglong2 L0 = reinterpret_cast<const ulonglong2&>(S.sl4[e * 4 + jq]);
-                            const ulonglong2 L1 = make_ulonglong2(reinterpret_cast<const f2&>(S.sl2[e * 4 + jq]), 0ull);
-                            L.dx = f2add(L.dx, f2sub(lxi2, L0.x));
-                            L.dy = f2add(L.dy, f2sub(lyi2, L0.y));
-                            L.dz = f2add(L.dz, f2sub(lzi2, L1.x));
+                            const ulonglong2 P2 = pb[2];  // {ly, lz} pairs; lx pair is P1.y
+                            L.dx = f2add(L.dx, f2sub(lxi2, P1.y));
+                            L.dy = f2add(L.dy, f2sub(lyi2, P2.x));
+                            L.dz = f2add(L.dz, f2sub(lzi2, P2.y));
+                            L.pma = L.pmb = 0.f;
+                        } else {
+                            f2u(P1.y, L.pma, L.pmb);
                         }
-                        f2u(P1.y, L.pma, L.pmb);
                         f2u(f2fma(L.dz, L.dz, f2fma(L.dy, L.dy, f2mul(L.dx, L.dx))), L.d2a, L.d2b);
                         return L;
                     };
@@ -334,12 +326,10 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                         const uint64_t j = uint64_t(S.idx[h0 + e]) * CJ + jq + 4 * sl2;
                         if (j >= A.n) return;
                         if (LJ && d2 < lo) {
-                            const float* pj = S.sj + e * 32 + jq * 8;
-                            const float* pl = reinterpret_cast<const float*>(&S.sl4[e * 4 + jq]);
-                            const float* pz = reinterpret_cast<const float*>(&S.sl2[e * 4 + jq]);
-                            const double dx = (double(S.ix[li]) - double(pj[sl2])) + (double(S.ilx[li]) - double(pl[sl2]));
-                            const double dy = (double(S.iy[li]) - double(pj[2 + sl2])) + (double(S.ily[li]) - double(pl[2 + sl2]));
-                            const double dz = (double(S.iz[li]) - double(pj[4 + sl2])) + (double(S.ilz[li]) - double(pz[sl2]));
+                            const float* pj = S.sj + (e * 4 + jq) * 12 + sl2;
+                            const double dx = (double(S.ix[li]) - double(pj[0])) + (double(S.ilx[li]) - double(pj[6]));
+                            const double dy = (double(S.iy[li]) - double(pj[2])) + (double(S.ily[li]) - double(pj[8]));
+                            const double dz = (double(S.iz[li]) - double(pj[4])) + (double(S.ilz[li]) - double(pj[10]));
                             const double dd2 = dx * dx + dy * dy + dz * dz;
                             if (dd2 >= double(kLjTiny2) * sig2d) {
                                 const double inv2 = 1.0 / dd2;
