@@ -398,7 +398,7 @@ void launch_pass_item(sfcnl_cu_ctx* c, const PassArgs& A) {
 template <int K>
 void launch_pass(sfcnl_cu_ctx* c, const PassArgs& A, bool fast) {
     constexpr bool kLJ = K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB;
-    if (fast && kLJ && !getenv("SFCNL_PASS_ITEM_LJ")) {  // warp-per-SC lane = (i, j-quarter) layout (pass_warp.cuh)
+    if (fast && ((kLJ && !getenv("SFCNL_PASS_ITEM_LJ")) || (!kLJ && getenv("SFCNL_DENSITY_WARP")))) {  // warp-per-SC lane = (i, j-quarter) layout (pass_warp.cuh)
         if (A.cj == 8) launch_pass_warp<K, 8>(c, A);
         else launch_pass_warp<K, 4>(c, A);
     } else if (fast) {  // item-parallel layout (pass_item.cuh)
