@@ -1,6 +1,9 @@
-"""Full-size parity (BASELINE.json configs[1], C2: 2^26 uniform particles, 200
-neighbours, 8x8 gather compressed): the CUDA build and mixed pass at the bench
-size, checked on sampled super-cluster ranges against the plain-C restatement
+"""Full-size parity at the BASELINE.json configurations:
+C2 (2^26 uniform periodic particles, 200 neighbours), C3 (Evrard sphere, 2^24 particles,
+per-particle h, open box) and C4 (LJ fluid: 4M particles at density 100, 150 neighbours
+in the cutoff, Verlet skin 1.100642, sigma 0.2), 8x8 gather compressed: the CUDA build
+and mixed pass at the full size, checked on sampled super-cluster ranges against the
+plain-C restatement
 (oracle/sfcnl_oracle.c build_store_range / reduce_range, which follow
 neighbor_build.cpp:74-184 and reduce.hpp:38-231 and are pinned to the reference's
 golden fixtures by tests/test_oracle_golden.py).
@@ -10,7 +13,7 @@ golden fixtures by tests/test_oracle_golden.py).
 * LJ (mixed): neighbor_count exact, force error <= 1e-5 * sum_j |F_ij|, energy error
   <= 1e-5 * sum_j |E_ij| (same bar as tests/test_gpu_parity.py).
 
-SFCNL_SCALE_N overrides the particle count (default 2^26)."""
+SFCNL_SCALE_N overrides the C2 particle count (default 2^26)."""
 import os
 
 import numpy as np
@@ -24,30 +27,42 @@ P = Oracle("port")
 N = int(os.environ.get("SFCNL_SCALE_N", str(1 << 26)))
 
 
-@pytest.fixture(scope="module")
-def run():
+CONFIGS = {
+    # name: (generator, n, spec kwargs, build radius scale, LJ sigma)
+    "C2": ("uniform", N, dict(density=float(N), target_neighbors=200.0), 1.0, 0.5 * (1.0 / N) ** (1.0 / 3.0)),
+    "C3": ("evrard", 1 << 24, dict(target_neighbors=200.0), 1.0, 0.5 * (1.0 / (1 << 24)) ** (1.0 / 3.0)),
+    "C4": ("uniform", 4_000_000, dict(density=100.0, target_neighbors=150.0), 1.100642, 0.2),
+}
+
+
+@pytest.fixture(scope="module", params=sorted(CONFIGS))
+def run(request):
+    gen, n, kw, scale, sigma = CONFIGS[request.param]
     ctx = S.Context(0)
-    ps, box = S.make_uniform(S.UniformSpec(n=N, density=float(N), target_neighbors=200.0, seed=42))
-    bp = S.BuildParams(S.ClusterParams(8, 8, 32), S.GATHER, True, 1.0)
-    sigma = 0.5 * (1.0 / N) ** (1.0 / 3.0)
+    if gen == "uniform":
+        ps, box = S.make_uniform(S.UniformSpec(n=n, seed=42, **kw))
+    else:
+        ps, box = S.make_evrard(S.EvrardSpec(n=n, seed=42, **kw))
+    bp = S.BuildParams(S.ClusterParams(8, 8, 32), S.GATHER, True, scale)
     ctx.set_particles(ps, box)
     ctx.sort()
     ctx.apply_order()
     nn = ctx.octree(64)
     nsc, nb = ctx.build_store(bp)
-    store = ctx.get_store(bp, N, nsc, nb)
+    store = ctx.get_store(bp, n, nsc, nb)
     nodes = ctx.get_octree(nn)
     geo = ctx.node_geometry(nn)
-    rho = ctx.reduce(S.sph_density_kernel(), S.PassConfig(1.0, S.MIXED), N)
-    lj = ctx.reduce(S.lj_kernel(1.0, sigma), S.PassConfig(1.0, S.MIXED), N)
-    sp = Particles(*(ctx.get_sorted(f, N) for f in ("x", "y", "z", "h", "m")), np.zeros(N),
+    rho = ctx.reduce(S.sph_density_kernel(), S.PassConfig(1.0, S.MIXED), n)
+    lj = ctx.reduce(S.lj_kernel(1.0, sigma), S.PassConfig(1.0, S.MIXED), n)
+    sp = Particles(*(ctx.get_sorted(f, n) for f in ("x", "y", "z", "h", "m")), np.zeros(n),
                    np.array(list(box.lo) + list(box.hi)), tuple(int(v) for v in box.periodic))
     f = lambda k, dt: np.ascontiguousarray(nodes[k], dt)  # structured-array fields are strided views
     tree = Tree(f("key_first", np.uint64), f("key_last", np.uint64), f("particle_begin", np.uint32),
                 f("particle_end", np.uint32), f("first_child", np.int32), f("depth", np.uint8), 21)
     rng = np.random.default_rng(5)
     starts = sorted({0, nsc - 48} | set(int(v) for v in rng.integers(0, nsc - 48, 3)))
-    return dict(store=store, geo=geo, rho=rho, lj=lj, sp=sp, tree=tree, sigma=sigma, ranges=[(s, s + 48) for s in starts])
+    return dict(store=store, geo=geo, rho=rho, lj=lj, sp=sp, tree=tree, sigma=sigma, scale=scale,
+                ranges=[(s, s + 48) for s in starts])
 
 
 def _slice(store, sc0, sc1):
@@ -58,7 +73,7 @@ def _slice(store, sc0, sc1):
 def test_store_bit_exact_on_sampled_ranges(run):
     sp, tree, geo = run["sp"], run["tree"], run["geo"]
     for sc0, sc1 in run["ranges"]:
-        ref = P.build_store_range(sp, tree, geo, sc0, sc1, float(sp.h.max()))
+        ref = P.build_store_range(sp, tree, geo, sc0, sc1, float(sp.h.max()), scale=run["scale"])
         counts, blob = _slice(run["store"], sc0, sc1)
         assert np.array_equal(counts, ref.counts), (sc0, sc1)
         assert np.array_equal(blob, ref.blob), (sc0, sc1)
@@ -68,7 +83,7 @@ def _range_store(run, sc0, sc1):
     st = run["store"]
     counts, blob = _slice(st, sc0, sc1)
     offs = st.offsets[sc0:sc1 + 1] - st.offsets[sc0]
-    return Store(run["sp"].n, 8, 8, 32, 0, 1, 1.0, counts.copy(), offs.astype(np.uint64), blob.copy())
+    return Store(run["sp"].n, 8, 8, 32, 0, 1, run["scale"], counts.copy(), offs.astype(np.uint64), blob.copy())
 
 
 def test_density_mixed_on_sampled_ranges(run):
@@ -104,7 +119,8 @@ def test_lj_mixed_on_sampled_ranges(run):
                         continue
                     ii = np.arange(64 * (sc0 + s) + 8 * bit, min(64 * (sc0 + s) + 8 * bit + 8, sp.n))
                     d = pos[ii][:, None, :] - pos[js][None, :, :]
-                    d -= L * np.rint(d / L)
+                    per = np.array(sp.periodic, bool)
+                    d[..., per] -= L[per] * np.rint(d[..., per] / L[per])
                     d2 = (d * d).sum(2)
                     ok = (d2 <= (sp.h[ii] ** 2)[:, None]) & (js[None, :] != ii[:, None])
                     inv2 = np.where(ok, 1.0 / np.where(ok, d2, 1.0), 0.0)
