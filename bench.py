@@ -139,6 +139,26 @@ def peaks():
         return {"hbm_gbs": 6650.0}, "fallback"
 
 
+def composite_roofline(stage, n, pk, ms):
+    """sum over stages of the time the stage's binding resource needs for
+    its algorithmic work, over the measured step. Streaming stages are bound by HBM
+    (compulsory bytes per particle); the build and the passes by the FP32 lanes
+    (148 SMs x 128 lanes x 1.965 GHz = 37.2 T lane-ops/s; algorithmic lane-ops per
+    particle from the reference's measured work counters: build 464 pair tests x 9,
+    density 644 slots x 18 + 200 hits x 12, LJ 644 slots x 12 (hi+lo d2) + 200 hits x 16)."""
+    bw = pk["hbm_gbs"] * 1e9
+    lane_ops = 148 * 128 * 1.965e9
+    hbm_bytes = {"keygen": 36, "sort": 24 * ((3 * 21 + 7) // 8), "permute": 84, "octree": 11,
+                 "node_geometry": 14, "cluster_geometry": 46, "encode": 3.77}
+    alu_ops = {"build": 464 * 9, "pass_rho": 644 * 18 + 200 * 12, "pass_fx": 644 * 12 + 200 * 16}
+    floor = {k: v * n / bw * 1e3 for k, v in hbm_bytes.items() if k in stage}
+    floor.update({k: v * n / lane_ops * 1e3 for k, v in alu_ops.items() if k in stage})
+    tot = sum(floor.values())
+    return {"frac": round(tot / ms, 4), "floor_ms": round(tot, 2),
+            "stage_frac": {k: round(floor[k] / stage[k], 3) for k in floor if stage.get(k, 0) > 0},
+            "model": "HBM bytes for streaming stages, FP32 lane-ops for build/passes (bench.py composite_roofline)"}
+
+
 # ---------------------------------------------------------------- CPU reference
 def cpu_reference(n, target, steps=1):
     """The unmodified reference (oracle/_ref) on all host threads; every stage timed."""
@@ -320,6 +340,7 @@ def run_b200(args, ws, rank, local):
                      "peak_kind": pk_kind, "pipe_util_pct": pipe_util,
                      "note": "pass/build are FP32-pipe/latency bound (SURVEY §8(d)): the HBM fraction is per the "
                              "schema; pipe_util_pct = ncu FMA/ALU pipe and issue utilisation of this kernel"},
+        "roofline_composite": composite_roofline(stage, n, pk, ms_max),
         "clocks": clk.summary(),
     }
     if rank == 0 and not args.no_cpu_baseline:
