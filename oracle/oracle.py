@@ -186,7 +186,7 @@ class Oracle:
 
     # ---- store
     def build_store(self, ps: Particles, tree: Tree, ci=8, cj=8, w=32, mode=0, compress=1,
-                    scale=1.0, threads=1) -> Store:
+                    scale=1.0, threads=1, write_path=None) -> Store:
         per = (C.c_int * 3)(*ps.periodic)
         h = C.c_void_p()
         common = (U64(ps.n), _p(ps.x, D), _p(ps.y, D), _p(ps.z, D), _p(ps.h, D), _p(ps.box6, D), per,
@@ -207,6 +207,8 @@ class Oracle:
             offsets = np.empty(nsc.value + 1, np.uint64)
             blob = np.empty(max(nb.value, 1), np.uint8)
             self._f("store_copy")(h, _p(counts, U32), _p(offsets, U64), _p(blob, U8))
+            if write_path is not None:  # the reference's own SFNLSTOR writer (reference kind only)
+                self._check(self._f("store_write")(h, write_path.encode()))
             return Store(ps.n, ci, cj, w, mode, compress, scale, counts, offsets, blob[: nb.value])
         finally:
             self._f("store_free")(h)

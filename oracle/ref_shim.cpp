@@ -295,6 +295,11 @@ REF_API int ref_build_store_nodes(uint64_t n, const double* x, const double* y, 
     });
 }
 
+// write_store (neighbor_store.cpp:84-103) of a built store to `path` (SFNLSTOR v1).
+REF_API int ref_store_write(void* h, const char* path) {
+    return guarded([&] { sfcnl_ref::write_store(static_cast<RefStore*>(h)->s, std::string(path)); });
+}
+
 REF_API void ref_store_info(void* h, uint64_t* num_sc, uint64_t* blob_size) {
     const auto& s = static_cast<RefStore*>(h)->s;
     *num_sc = s.counts.size();

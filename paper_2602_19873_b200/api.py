@@ -24,6 +24,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import os
+import struct
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -193,6 +194,57 @@ class NeighborStore:
 class MemoryFootprint:
     total_bytes: int
     bytes_per_particle: float
+
+
+_STORE_MAGIC = b"SFNLSTOR"
+_STORE_HEAD = struct.Struct("<8sIBBHIIIIdQQQ")  # magic, version, mode, compress, reserved, ci, cj, sc, w, scale, n, nsc, nb
+
+
+def write_store(store: NeighborStore, path_or_file) -> None:
+    """write_store (neighbor_store.hpp:79-82, neighbor_store.cpp:84-103): the
+    "SFNLSTOR" v1 little-endian dump -- header, counts (u32), offsets (u64), blob."""
+    p = store.build.params
+    head = _STORE_HEAD.pack(_STORE_MAGIC, 1, int(store.build.mode), 1 if store.build.compress else 0, 0,
+                            p.ci, p.cj, p.sc_size, p.w, float(store.build.build_radius_scale), int(store.n),
+                            len(store.counts), len(store.blob))
+    body = [np.ascontiguousarray(store.counts, "<u4").tobytes(), np.ascontiguousarray(store.offsets, "<u8").tobytes(),
+            np.ascontiguousarray(store.blob, np.uint8).tobytes()]
+    if isinstance(path_or_file, (str, bytes, os.PathLike)):
+        with open(path_or_file, "wb") as f:
+            f.write(head), [f.write(b) for b in body]
+    else:
+        path_or_file.write(head), [path_or_file.write(b) for b in body]
+
+
+def read_store(path_or_file) -> NeighborStore:
+    """read_store (neighbor_store.hpp:83-86, neighbor_store.cpp:110-146), same errors:
+    DecodeError("bad store magic", 0), ("unsupported store version", 8),
+    ("unsupported super-cluster size", 0), ("store file truncated", offset)."""
+    if isinstance(path_or_file, (str, bytes, os.PathLike)):
+        with open(path_or_file, "rb") as f:
+            data = f.read()
+    else:
+        data = path_or_file.read()
+    if len(data) < 8 or data[:8] != _STORE_MAGIC:
+        raise DecodeError("bad store magic", 0)
+    if len(data) < 12:
+        raise DecodeError("store file truncated", len(data))
+    if struct.unpack_from("<I", data, 8)[0] != 1:
+        raise DecodeError("unsupported store version", 8)
+    if len(data) < _STORE_HEAD.size:
+        raise DecodeError("store file truncated", len(data))
+    _, _, mode, comp, _, ci, cj, sc, w, scale, n, nsc, nb = _STORE_HEAD.unpack_from(data, 0)
+    if sc != kSuperClusterSize:
+        raise DecodeError("unsupported super-cluster size", 0)
+    o = _STORE_HEAD.size
+    need = o + 4 * nsc + 8 * (nsc + 1) + nb
+    if len(data) < need:
+        raise DecodeError("store file truncated", len(data))
+    counts = np.frombuffer(data, "<u4", nsc, o).astype(np.uint32)
+    offsets = np.frombuffer(data, "<u8", nsc + 1, o + 4 * nsc).astype(np.uint64)
+    blob = np.frombuffer(data, np.uint8, nb, o + 4 * nsc + 8 * (nsc + 1)).copy()
+    bp = BuildParams(ClusterParams(ci, cj, w), GATHER if mode == 0 else SYMMETRIC, comp != 0, scale)
+    return NeighborStore(bp, n, counts, offsets, blob)
 
 
 def memory_footprint(store: NeighborStore) -> MemoryFootprint:

@@ -38,7 +38,9 @@ def make(name, spec, R):
     keys, perm = R.sort_by_sfc(ps)
     sp = ps.permuted(perm)
     tree, lo, hi, rad = R.node_geometry(keys, sp)
-    store = R.build_store(sp, tree, ci, cj, w, mode, comp, scale, threads=1)
+    # the reference's own SFNLSTOR v1 writer (neighbor_store.cpp:84-103) -> <name>.sfnl
+    store = R.build_store(sp, tree, ci, cj, w, mode, comp, scale, threads=1,
+                          write_path=os.path.join(HERE, name + ".sfnl"))
     sigma = 0.5 * (1.0 / (ga["density"] if gen == "uniform" else ga["n"])) ** (1.0 / 3.0)
     out = dict(x=ps.x, y=ps.y, z=ps.z, h=ps.h, m=ps.m, q=ps.q, box6=ps.box6,
                periodic=np.array(ps.periodic, np.int32), keys=keys, perm=perm,
