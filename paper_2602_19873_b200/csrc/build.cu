@@ -65,6 +65,9 @@ struct BuildArgs {
     const float4* frame;       // cluster-frame staging copy (frame.cu)
     const unsigned* frame_x;   // its max |offset| per axis (float bits)
     unsigned long long* prof;  // phase clocks (SFCNL_PHASE_PROF builds)
+    uint32_t* leaf_cache;      // accepted leaves per SC of [sc_lo, ...) (halo_mark -> range build), or null
+    uint32_t* leaf_count;      // their number per SC (~0u: not cached)
+    uint64_t leaf_sc0;         // first SC of the cache
     DevError* err;
 };
 
@@ -648,6 +651,11 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
     A.overflow_list = c->overflow_list.as<uint32_t>();
     A.err = c->derr.as<DevError>();
     A.btab = nullptr;
+    A.leaf_cache = nullptr, A.leaf_count = nullptr, A.leaf_sc0 = sc0;
+    if (c->leaf_cache_valid && c->jflags_valid && c->jflags_sc0 == sc0 && c->jflags_sc1 == sc1) {
+        // the halo marking of this range already ran the same traversal (build_warp.cuh)
+        A.leaf_cache = c->leaf_cache.as<uint32_t>(), A.leaf_count = c->leaf_count.as<uint32_t>();
+    }
     if (p.compress) {
         SFCNL_CUDA_TRY(c->btab.reserve(std::max<uint64_t>(num_sc, 1) * 16 * 2));
         A.btab = c->btab.as<uint16_t>() - sc0 * 16;
@@ -757,6 +765,7 @@ int run_halo_mark(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, ui
     SFCNL_CUDA_TRY(c->jflags.reserve(std::max<uint64_t>(nj, 1)));
     SFCNL_CUDA_TRY(cudaMemsetAsync(c->jflags.p, 0, std::max<uint64_t>(nj, 1), c->stream));
     c->jflags_valid = false;
+    c->leaf_cache_valid = false;
     if (sc1 > sc0) {
         const uint64_t p_lo = sc0 * 64, p_hi = tmin<uint64_t>(sc1 * 64, n);
         int rc = run_cluster_geometry(c, p.ci, p.ci, p_lo, p_hi);  // i-clusters of the range
@@ -780,6 +789,10 @@ int run_halo_mark(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, ui
         A.err = c->derr.as<DevError>();
         SFCNL_CUDA_TRY(c->work_ctr.reserve(8));
         SFCNL_CUDA_TRY(cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream));
+        // accepted leaves per SC, reused by the range build of the same range
+        SFCNL_CUDA_TRY(c->leaf_cache.reserve((sc1 - sc0) * kLeafCacheCap * 4));
+        SFCNL_CUDA_TRY(c->leaf_count.reserve((sc1 - sc0) * 4));
+        A.leaf_cache = c->leaf_cache.as<uint32_t>(), A.leaf_count = c->leaf_count.as<uint32_t>(), A.leaf_sc0 = sc0;
         const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((sc1 - sc0 + 7) / 8, uint64_t(c->num_sms) * 3)));
         launch(c, k_halo_warp, dim3(grid), dim3(256), 0, A, sc0, sc1, c->jflags.as<uint8_t>(),
                c->work_ctr.as<unsigned long long>());
@@ -798,6 +811,7 @@ int run_halo_mark(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, ui
         }
     }
     c->jflags_valid = true;
+    c->leaf_cache_valid = sc1 > sc0 && c->leaf_cache.bytes >= (sc1 - sc0) * kLeafCacheCap * 4;
     c->jflags_sc0 = sc0, c->jflags_sc1 = sc1, c->jflags_len = nj;
     return 0;
 }

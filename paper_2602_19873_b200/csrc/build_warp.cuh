@@ -34,6 +34,7 @@ constexpr int kBwWarps = 4;
 constexpr uint32_t kBwF = 512;   // frontier entries per buffer
 constexpr uint32_t kBwE = 384;   // entries per SC (~170 at 200 neighbours)
 constexpr uint32_t kBwBytes = 4096;  // encoded bytes (aliases the frontier)
+constexpr uint32_t kLeafCacheCap = 256;  // accepted leaves kept per SC by halo marking
 
 struct BwSmem {
     union {
@@ -214,7 +215,17 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
     PHASE(0);
     // ---- 2. ordered-frontier BFS (exact fp64 node test)
     uint32_t* fa;
-    const uint32_t nA = warp_bfs(A, scg, r2, S.u.t.fa, S.u.t.fb, &fa);
+    uint32_t nA = ~0u;
+    if (A.leaf_cache) {  // halo marking of this range already traversed (same BFS, same order)
+        const uint32_t cnt = A.leaf_count[sc - A.leaf_sc0];
+        if (cnt != ~0u) {
+            const uint32_t* src = A.leaf_cache + (sc - A.leaf_sc0) * kLeafCacheCap;
+            for (uint32_t k = lane; k < cnt; k += 32) S.u.t.fa[k] = src[k];
+            __syncwarp();
+            fa = S.u.t.fa, nA = cnt;
+        }
+    }
+    if (nA == ~0u) nA = warp_bfs(A, scg, r2, S.u.t.fa, S.u.t.fb, &fa);
     if (nA == ~0u) return false;
     uint32_t* fb = fa == S.u.t.fa ? S.u.t.fb : S.u.t.fa;
 
@@ -620,6 +631,7 @@ __global__ void __launch_bounds__(256) k_halo_warp(const __grid_constant__ Build
             if (lane == 0) {
                 const unsigned long long slot = atomicAdd(&A.ctl[1], 1ull);
                 A.overflow_list[slot] = uint32_t(sc);
+                if (A.leaf_count) A.leaf_count[sc - A.leaf_sc0] = ~0u;
             }
             __syncwarp();
             continue;
@@ -627,7 +639,9 @@ __global__ void __launch_bounds__(256) k_halo_warp(const __grid_constant__ Build
         for (uint32_t k = lane; k < nA; k += 32) {
             const Node nd = A.nodes[fa[k] & ~kTag];
             for (uint32_t j = nd.pbegin / A.cj; j <= (nd.pend - 1) / A.cj; ++j) jflags[j] = 1;
+            if (A.leaf_cache && nA <= kLeafCacheCap) A.leaf_cache[(sc - A.leaf_sc0) * kLeafCacheCap + k] = fa[k];
         }
+        if (A.leaf_count && lane == 0) A.leaf_count[sc - A.leaf_sc0] = nA <= kLeafCacheCap ? nA : ~0u;
         __syncwarp();
     }
 }

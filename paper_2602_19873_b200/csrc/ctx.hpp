@@ -122,6 +122,8 @@ struct sfcnl_cu_ctx {
     sfcnl_cu::DBuf jflags;  // halo: u8 per global j-cluster, set by run_halo_mark
     bool jflags_valid = false;
     uint64_t jflags_sc0 = 0, jflags_sc1 = 0, jflags_len = 0;
+    sfcnl_cu::DBuf leaf_cache, leaf_count;  // accepted leaves per SC from halo_mark (reused by the range build)
+    bool leaf_cache_valid = false;
     sfcnl_cu::DBuf sc_size, sc_scratch_off, scratch, build_ctl, overflow_list, fallback_ws;
 
     // (5) pass
@@ -176,6 +178,7 @@ int host_set_error(int code, const std::string& msg, uint64_t off = 0);
 inline void drop_external(sfcnl_cu_ctx* c) {
     c->node_geo_external = false;
     c->jflags_valid = false;
+    c->leaf_cache_valid = false;
 }
 
 // Particles covered by the current store's super-cluster range (outputs of a pass).
