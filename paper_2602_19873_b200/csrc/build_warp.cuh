@@ -260,6 +260,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
     PHASE(2);
     // ---- 4. masks, chunk by chunk; 5a. ordered compaction of mask != 0
     uint32_t nE = 0;
+    float Ej_run = -1.f;               // running max of the staged |coordinates| (guard bands)
     double pr_me = 0.0, pr2_me = 0.0;  // prefilter radius of i-cluster `lane` (neighbor_build.cpp:136)
     if (lane < nicl) pr_me = dmul(A.scale, A.igeo[icl_base + lane].maxh), pr2_me = dmul(pr_me, pr_me);
     const uint32_t il = lane >> 2, jq = lane & 3;
@@ -346,20 +347,25 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
             }
             Ej = warp_fmax(Ej);
             PHASE(6);
-            // coordinate errors: 2^-24 Ei (i side), 2^-23 (Ej + X) (cluster frame)
-            const double ecoord = 5.9604644775390625e-08 * double(Ei) + 1.1920928955078125e-07 * (double(Ej) + double(Xo));
+            // coordinate errors: 2^-24 Ei (i side), 2^-23 (Ej + X) (cluster frame). The band
+            // only widens with E, so thresholds computed for a running maximum of Ej stay
+            // valid for later chunks: they are recomputed only when a chunk raises it.
+            if (Ej > Ej_run) {
+                Ej_run = fmaxf(Ej, Ej_run * 1.0625f);  // a little headroom: fewer recomputations
+                const double ecoord = 5.9604644775390625e-08 * double(Ei) + 1.1920928955078125e-07 * (double(Ej_run) + double(Xo));
 #pragma unroll
-            for (int s = 0; s < 2; ++s) {
-                const uint32_t k = lane + 32u * s;
-                float lo = -1.f, hi = -1.f;
-                if (ri[s] >= 0.0) {
-                    const double rr2 = dmul(ri[s], ri[s]), g = guard_band(ri[s], rr2, ecoord);
-                    lo = __double2float_rd(rr2 - g);
-                    hi = __double2float_ru(rr2 + g);
+                for (int s = 0; s < 2; ++s) {
+                    const uint32_t k = lane + 32u * s;
+                    float lo = -1.f, hi = -1.f;
+                    if (ri[s] >= 0.0) {
+                        const double rr2 = dmul(ri[s], ri[s]), g = guard_band(ri[s], rr2, ecoord);
+                        lo = __double2float_rd(rr2 - g);
+                        hi = __double2float_ru(rr2 + g);
+                    }
+                    S.ia[(k & 7) * 8 + (k >> 3)].w = lo, S.ihi[(k & 7) * 8 + (k >> 3)] = hi;
                 }
-                S.ia[(k & 7) * 8 + (k >> 3)].w = lo, S.ihi[(k & 7) * 8 + (k >> 3)] = hi;
+                if (lane < nicl) S.pthr[lane] = __double2float_ru(pr2_me + guard_band(pr_me, pr2_me, ecoord));
             }
-            if (lane < nicl) S.pthr[lane] = __double2float_ru(pr2_me + guard_band(pr_me, pr2_me, ecoord));
             if (lane < 32) S.cmask[lane] = 0;
             __syncwarp();
             // conservative fp32 prefilter, lane = candidate
