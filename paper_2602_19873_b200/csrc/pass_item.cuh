@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : 5) k_pass_i
         __syncwarp();
 
         bool coincident = false;
+        float Ej_run = -1.f;  // running bound of the staged |coordinates| for the guard bands
         uint64_t pos = 0, running = 0;
         const uint32_t nicl = tmin<uint32_t>(8u, uint32_t((np + 7) / 8));
         for (uint32_t bb = 0; !bad && bb < count; bb += w) {
@@ -283,10 +284,13 @@ __global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : 5) k_pass_i
                 Ej = warp_fmax(Ej);
                 // per-i thresholds: coordinate errors <= 2^-24 Ei (i side) and
                 // 2^-24 Ej (fp64 staging) or 2^-23 (Ej + X) (cluster frame)
+                // (the band only widens with Ej: recomputed when a chunk raises the running bound)
+                const bool redo = Ej > Ej_run;
+                if (redo) Ej_run = fmaxf(Ej, Ej_run * 1.0625f);
                 const double ecoord = 5.9604644775390625e-08 * double(Ei) +
-                                      (LJ ? 5.9604644775390625e-08 * double(Ej) : 1.1920928955078125e-07 * (double(Ej) + double(Xo)));
+                                      (LJ ? 5.9604644775390625e-08 * double(Ej_run) : 1.1920928955078125e-07 * (double(Ej_run) + double(Xo)));
 #pragma unroll
-                for (int s = 0; s < 2; ++s) {
+                for (int s = 0; s < 2 && redo; ++s) {
                     const uint32_t k = lane + 32u * s;
                     const uint32_t slot = (k & 7) * 8 + (k >> 3);
                     const double r = S.ir[k];

@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
         __syncwarp();
 
         bool coincident = false;
+        float E_run = -1.f;  // running bound of the staged |coordinates| for the guard bands
         uint64_t pos = 0, running = 0;
         const uint32_t nicl = tmin<uint32_t>(8u, uint32_t((np + 7) / 8));
         for (uint32_t bb = 0; !bad && bb < count; bb += w) {
@@ -229,14 +230,15 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                     }
                 }
                 const float E = fmaxf(Ei, warp_fmax(emax));
-                if (!unsafe) {  // per-i thresholds for this chunk (guard band of pass.cu)
+                if (!unsafe && E > E_run) {  // per-i thresholds (guard band of pass.cu); the band only
+                    E_run = fmaxf(E, E_run * 1.0625f);  // widens with E: recomputed when a chunk raises it
 #pragma unroll
                     for (int s = 0; s < 2; ++s) {
                         const uint32_t k = lane + 32u * s;
                         float lo = -1.f, hi = -1.f;
                         if (k < np) {
                             const double r = dmul(A.qs, A.h[p0 + k]), r2 = dmul(r, r);
-                            const double ex = 1.1920928955078125e-07 * double(E) + 5.9604644775390625e-08 * r;
+                            const double ex = 1.1920928955078125e-07 * double(E_run) + 5.9604644775390625e-08 * r;
                             const double guard = 4.0 * (1.7881393432617188e-07 * r2 + 3.5 * r * ex + 3.0 * ex * ex) + 1e-300;
                             lo = __double2float_rd(r2 - guard);
                             hi = __double2float_ru(r2 + guard);
