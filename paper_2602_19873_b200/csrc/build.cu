@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_global(const __grid_con
         (reinterpret_cast<uintptr_t>(W.cand + ccap) + 15) & ~uintptr_t(15));
     W.ebuf = reinterpret_cast<uint8_t*>(W.cmask + ccap);
     W.fcap = fcap, W.ccap = ccap, W.ecap = ecap;
-    W.fast = false;  // exact mask loop
+    W.fast = true;  // global-memory workspaces; the fp32 guard-band masks still apply
     for (uint64_t t = blockIdx.x; t < count; t += gridDim.x) {
         const uint64_t sc = list[t];
         if (!build_sc(A, W, sc)) {
@@ -702,7 +702,7 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
             const uint32_t ecap = uint32_t(std::min<uint64_t>(uint64_t(ccap) * (A.mask_bytes + 10) + 64, 0xfffffff0ull));
             const uint64_t stride =
                 ((uint64_t(fcap) * 8 + uint64_t(ccap) * 4 + 16 + uint64_t(ccap) * 8 + ecap) + 255) & ~uint64_t(255);
-            const uint64_t nblk = std::min<uint64_t>(ctl[1], 8);
+            const uint64_t nblk = std::min<uint64_t>(ctl[1], 64);  // SCs too large for the warp slices
             SFCNL_CUDA_TRY(c->fallback_ws.reserve(stride * nblk));
             launch(c, k_build_global, dim3(unsigned(nblk)), dim3(kBuildThreads), 0, A,
                    (const uint32_t*)A.overflow_list, uint64_t(ctl[1]), c->fallback_ws.as<uint8_t>(), stride,
