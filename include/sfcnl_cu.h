@@ -170,6 +170,26 @@ int sfcnl_cu_set_store(sfcnl_cu_ctx* ctx, const sfcnl_build_params* params, uint
 int sfcnl_cu_reduce(sfcnl_cu_ctx* ctx, const sfcnl_pass_params* params, double* const* outs,
                     uint32_t* neighbor_count);
 
+/* ---- (5b) full Verlet list baseline -------------------------
+ * The classic per-particle CSR list the paper measures the compressed list
+ * against (baselines.hpp:27-38 FullVerletList, :42-44 build_full_list, :47-129
+ * reduce_full). build_full_list derives it on the device from the current
+ * whole-range GATHER store: for every i the j != i with
+ * |minimage(x_i - x_j)|^2 <= (build_scale h_i)^2 (periodic_delta, fp64), ascending
+ * j -- the same list as build_full_list(sorted, box, build_scale, gather) for any
+ * build_scale <= the store's build radius scale. num_pairs = offsets[n].
+ * get_full_list: offsets u64[n + 1], neighbors u32[num_pairs]. set_full_list
+ * uploads a list built elsewhere (mode 0 gather, 1 symmetric). reduce_full
+ * replaces reduce_full<Real,K>: precision 0 is bit-equal to reduce_full<double>
+ * (ascending j, thread per i); precision 1 evaluates the same pairs warp-per-i in
+ * fp64 with a tree sum. outs/count as in sfcnl_cu_reduce. */
+int sfcnl_cu_build_full_list(sfcnl_cu_ctx* ctx, double build_scale, uint64_t* num_pairs);
+int sfcnl_cu_get_full_list(sfcnl_cu_ctx* ctx, uint64_t* offsets, uint32_t* neighbors);
+int sfcnl_cu_set_full_list(sfcnl_cu_ctx* ctx, uint64_t n, int mode, double build_scale,
+                           const uint64_t* offsets, const uint32_t* neighbors, uint64_t num_pairs);
+int sfcnl_cu_reduce_full(sfcnl_cu_ctx* ctx, const sfcnl_pass_params* params, double* const* outs,
+                         uint32_t* neighbor_count);
+
 /* ---- (6) SFC domain decomposition -----------------------------
  * The reference is single-process; these entry points let one process per GPU
  * own a contiguous range of super-clusters of the GLOBAL sorted order while the
@@ -231,7 +251,8 @@ int sfcnl_cu_halo_mark(sfcnl_cu_ctx* ctx, const sfcnl_build_params* params, uint
 /* Device pointer + byte length of an internal array for zero-copy collectives:
  * "x","y","z","h", sorted fields by name, "keys","perm","nodes","node_geo",
  * "halo_flags","out0".."out3","count", the input slot "orig.x".."orig.h" and
- * "orig.<field>", the store "store.counts","store.offsets","store.blob".
+ * "orig.<field>", the store "store.counts","store.offsets","store.blob", the full
+ * list "full.offsets","full.neighbors".
  * Valid until the next call that resizes it. */
 int sfcnl_cu_device_array(sfcnl_cu_ctx* ctx, const char* name, void** ptr, uint64_t* bytes);
 

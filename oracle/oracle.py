@@ -307,6 +307,36 @@ class Oracle:
             _p(store.offsets, U64), _p(blob, U8), D(query_scale), D(eps), D(sigma), D(ck), optr, _p(cnt, U32)))
         return [o[:nloc] for o in outs], cnt[:nloc]
 
+    # ---- full Verlet list baseline (reference only: baselines.hpp:39-131)
+    def full_list(self, ps: Particles, build_scale=1.0, kernels=(), query_scale=1.0, eps=1.0, sigma=1.0, mode=0):
+        """build_full_list (cell grid, baselines.cpp:39-131) -> (offsets u64[n+1],
+        neighbors u32[]), plus reduce_full<double> (baselines.hpp:47-129) outputs for
+        each kernel name in `kernels`. mode 0 gather, 1 symmetric."""
+        assert self.kind == "reference"
+        per = (C.c_int * 3)(*ps.periodic)
+        h, npairs = C.c_void_p(), C.c_uint64()
+        self._check(self._f("full_list")(U64(ps.n), _p(ps.x, D), _p(ps.y, D), _p(ps.z, D), _p(ps.h, D),
+                                         _p(ps.box6, D), per, D(build_scale), C.c_int(mode), C.c_int(2),
+                                         C.byref(h), C.byref(npairs)))
+        try:
+            offsets = np.empty(ps.n + 1, np.uint64)
+            nbrs = np.empty(max(npairs.value, 1), np.uint32)
+            self._f("full_copy")(h, _p(offsets, U64), _p(nbrs, U32))
+            res = {}
+            for kern in kernels:
+                kid = KERNELS[kern]
+                nout = 4 if kid >= 2 else 1
+                outs = [np.zeros(ps.n) for _ in range(nout)]
+                optr = (C.POINTER(C.c_double) * 4)(*[_p(o, D) for o in outs])
+                cnt = np.zeros(ps.n, np.uint32)
+                self._check(self._f("reduce_full")(h, C.c_int(kid), U64(ps.n), _p(ps.x, D), _p(ps.y, D), _p(ps.z, D),
+                                                   _p(ps.h, D), _p(ps.m, D), _p(ps.q, D), _p(ps.box6, D), per,
+                                                   D(query_scale), D(eps), D(sigma), D(0.0), optr, _p(cnt, U32)))
+                res[kern] = (outs, cnt)
+            return offsets, nbrs[: npairs.value], res
+        finally:
+            self._f("full_free")(h)
+
     # ---- codec
     def encode(self, idx, w=32):
         idx = np.ascontiguousarray(idx, np.uint32)

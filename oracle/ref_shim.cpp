@@ -350,6 +350,55 @@ REF_API int ref_reduce(int kernel, int real, uint64_t n, const double* x, const 
     });
 }
 
+// ---- full Verlet list baseline (baselines.hpp:39-131) ----------------------------
+struct RefFull {
+    sfcnl_ref::FullVerletList l;
+};
+
+REF_API int ref_full_list(uint64_t n, const double* x, const double* y, const double* z, const double* h,
+                          const double* box6, const int* per, double build_scale, int mode, int method,
+                          void** out, uint64_t* num_pairs) {
+    return guarded([&] {
+        const auto ps = make_ps(n, x, y, z, h, nullptr, nullptr);
+        auto* r = new RefFull{sfcnl_ref::build_full_list(
+            ps, make_box(box6, per), build_scale, mode ? sfcnl_ref::ListMode::symmetric : sfcnl_ref::ListMode::gather,
+            sfcnl_ref::FullListMethod(method), ~size_t(0))};
+        *num_pairs = r->l.neighbors.size();
+        *out = r;
+    });
+}
+
+REF_API void ref_full_copy(void* h, uint64_t* offsets, uint32_t* neighbors) {
+    const auto& l = static_cast<RefFull*>(h)->l;
+    std::memcpy(offsets, l.offsets.data(), l.offsets.size() * 8);
+    if (!l.neighbors.empty()) std::memcpy(neighbors, l.neighbors.data(), l.neighbors.size() * 4);
+}
+
+REF_API int ref_reduce_full(void* hl, int kernel, uint64_t n, const double* x, const double* y, const double* z,
+                            const double* h, const double* m, const double* q, const double* box6, const int* per,
+                            double query_scale, double eps, double sigma, double ck, double** outs,
+                            uint32_t* ncount) {
+    return guarded([&] {
+        const auto ps = make_ps(n, x, y, z, h, m, q);
+        const auto box = make_box(box6, per);
+        const auto& l = static_cast<RefFull*>(hl)->l;
+        const sfcnl_ref::PassConfig cfg(query_scale, sfcnl_ref::Isa::scalar, 1);
+        auto finish = [&](const sfcnl_ref::ReduceResult<double>& r) {
+            for (size_t o = 0; o < r.outputs.size(); ++o)
+                for (uint64_t i = 0; i < n; ++i) outs[o][i] = r.outputs[o][i];
+            std::memcpy(ncount, r.neighbor_count.data(), n * 4);
+        };
+        switch (kernel) {
+            case 0: finish(sfcnl_ref::reduce_full<double>(ps, box, l, sfcnl_ref::count_kernel<double>(), cfg)); break;
+            case 1: finish(sfcnl_ref::reduce_full<double>(ps, box, l, sfcnl_ref::sph_density_kernel<double>(), cfg)); break;
+            case 2: finish(sfcnl_ref::reduce_full<double>(ps, box, l, sfcnl_ref::lj_kernel<double>(eps, sigma), cfg)); break;
+            default: throw sfcnl_ref::InputError("ref_reduce_full: unknown kernel id");
+        }
+    });
+}
+
+REF_API void ref_full_free(void* h) { delete static_cast<RefFull*>(h); }
+
 // ---- codec --------------------------------------------------------------------
 REF_API int ref_codec_encode(const uint32_t* idx, uint64_t count, int w, uint8_t* out,
                              uint64_t cap, uint64_t* len) {

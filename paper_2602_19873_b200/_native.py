@@ -81,7 +81,8 @@ EXPORTS = [
     "sfcnl_make_evrard", "sfcnl_cu_build_store_range", "sfcnl_cu_alloc_sorted", "sfcnl_cu_write_sorted",
     "sfcnl_cu_read_sorted", "sfcnl_cu_read_order", "sfcnl_cu_set_keys", "sfcnl_cu_apply_order_into",
     "sfcnl_cu_node_geometry_range", "sfcnl_cu_halo_mark", "sfcnl_cu_device_array",
-    "sfcnl_cu_set_particle_records",
+    "sfcnl_cu_set_particle_records", "sfcnl_cu_build_full_list", "sfcnl_cu_get_full_list",
+    "sfcnl_cu_set_full_list", "sfcnl_cu_reduce_full",
 ]
 
 _lib = None
@@ -143,6 +144,10 @@ def lib():
         "sfcnl_cu_halo_mark": (C.c_int, [P, C.POINTER(BuildParamsC), u64, u64, C.POINTER(u64)]),
         "sfcnl_cu_device_array": (C.c_int, [P, C.c_char_p, C.POINTER(P), C.POINTER(u64)]),
         "sfcnl_cu_set_particle_records": (C.c_int, [P, u64, P, C.c_int, C.POINTER(C.c_char_p), C.POINTER(Box)]),
+        "sfcnl_cu_build_full_list": (C.c_int, [P, C.c_double, C.POINTER(u64)]),
+        "sfcnl_cu_get_full_list": (C.c_int, [P, P, P]),
+        "sfcnl_cu_set_full_list": (C.c_int, [P, u64, C.c_int, C.c_double, P, P, u64]),
+        "sfcnl_cu_reduce_full": (C.c_int, [P, C.POINTER(PassParamsC), C.POINTER(P), P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -191,6 +191,18 @@ class NeighborStore:
 
 
 @dataclass
+class FullVerletList:
+    """baselines.hpp:27-38: classic per-particle Verlet list in CSR form, neighbors ascending."""
+    mode: int = GATHER
+    build_scale: float = 1.0
+    offsets: np.ndarray = field(default_factory=lambda: np.zeros(1, np.uint64))
+    neighbors: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
+
+    def memory_bytes(self):
+        return 8 * len(self.offsets) + 4 * len(self.neighbors)
+
+
+@dataclass
 class MemoryFootprint:
     total_bytes: int
     bytes_per_particle: float
@@ -440,6 +452,41 @@ class Context:
         self.check(self.L.sfcnl_cu_reduce(self.h, C.byref(pp), arr, _ptr(cnt)))
         return ReduceResult(list(kernel.names), outs, cnt)
 
+    # full Verlet list baseline (include/sfcnl_cu.h section (5b)) ----------
+    def build_full_list(self, build_scale):
+        """Full list of the current whole-range gather store's pairs; returns num_pairs."""
+        npairs = C.c_uint64()
+        self.check(self.L.sfcnl_cu_build_full_list(self.h, float(build_scale), C.byref(npairs)))
+        return npairs.value
+
+    def get_full_list(self, n, num_pairs, build_scale, mode=GATHER) -> FullVerletList:
+        offsets = np.empty(n + 1, np.uint64)
+        nbrs = np.empty(max(num_pairs, 1), np.uint32)
+        self.check(self.L.sfcnl_cu_get_full_list(self.h, _ptr(offsets), _ptr(nbrs)))
+        return FullVerletList(mode, float(build_scale), offsets, nbrs[:num_pairs])
+
+    def set_full_list(self, fl: FullVerletList):
+        offsets = np.ascontiguousarray(fl.offsets, np.uint64)
+        nbrs = np.ascontiguousarray(fl.neighbors, np.uint32)
+        if len(offsets) < 1:
+            raise InputError("reduce_full: list/particle-set mismatch")
+        buf = nbrs if nbrs.size else np.zeros(1, np.uint32)
+        self.check(self.L.sfcnl_cu_set_full_list(self.h, len(offsets) - 1, int(fl.mode), float(fl.build_scale),
+                                                 _ptr(offsets), _ptr(buf), len(nbrs)))
+
+    def reduce_full(self, kernel: Kernel, cfg: PassConfig, n, download=True):
+        pp = N.PassParamsC(kernel.kind, int(cfg.precision), float(cfg.query_scale), kernel.epsilon,
+                           kernel.sigma, kernel.coulomb_k)
+        nout = len(kernel.names)
+        if not download:
+            self.check(self.L.sfcnl_cu_reduce_full(self.h, C.byref(pp), None, None))
+            return None
+        outs = [np.empty(n) for _ in range(nout)]
+        cnt = np.empty(n, np.uint32)
+        arr = (C.c_void_p * 4)(*([o.ctypes.data for o in outs] + [None] * (4 - nout)))
+        self.check(self.L.sfcnl_cu_reduce_full(self.h, C.byref(pp), arr, _ptr(cnt)))
+        return ReduceResult(list(kernel.names), outs, cnt)
+
     # domain decomposition (include/sfcnl_cu.h section (6)) ----------------
     def set_particles_device(self, n, cols, names, box: SimulationBox):
         """Orig slot from device arrays: cols = [x, y, z, h, *fields] (torch CUDA tensors)."""
@@ -610,6 +657,57 @@ def reduce(ps: ParticleSet, box: SimulationBox, store: NeighborStore, kernel: Ke
     ctx.set_particles(ps, box, sorted_slot=True)
     ctx.set_store(store)
     return ctx.reduce(kernel, cfg, ps.size())
+
+
+def build_full_list(ps: ParticleSet, box: SimulationBox, build_scale: float, mode: int = GATHER,
+                    ctx=None) -> FullVerletList:
+    """build_full_list (baselines.hpp:42-44, baselines.cpp:39-131) on the GPU.
+
+    The list is derived from a compressed gather store built at `build_scale` over the
+    SFC-sorted copy of `ps` (K1-K4 of the hot path + pass_full.cuh). When `ps` is not
+    in SFC order, the sorted-index list is mapped back to `ps`'s numbering on the host
+    (rows by the permutation, each row re-sorted ascending). Gather mode only: a
+    symmetric full list (d <= scale max(h_i, h_j)) is not derivable from a gather
+    store at the same scale."""
+    if mode != GATHER:
+        raise InputError("build_full_list: only gather lists are built on the GPU")
+    if not (build_scale >= 0):
+        raise InputError("build_full_list: build_scale must be >= 0")
+    ctx = ctx or default_context()
+    n = ps.size()
+    ctx.set_particles(ParticleSet(ps.x, ps.y, ps.z, ps.h), box)
+    ctx.sort()
+    ctx.apply_order()
+    ctx.octree(64)
+    ctx.build_store(BuildParams(ClusterParams(8, 8, 32), GATHER, True, float(build_scale)))
+    pairs = ctx.build_full_list(build_scale)
+    fl = ctx.get_full_list(n, pairs, build_scale)
+    _, perm = ctx.get_order(n)
+    if n and not np.array_equal(perm, np.arange(n, dtype=np.uint32)):
+        cnt = np.diff(fl.offsets).astype(np.int64)
+        rows = np.repeat(perm.astype(np.int64), cnt)
+        cols = perm[fl.neighbors.astype(np.int64)].astype(np.int64)
+        o = np.lexsort((cols, rows))
+        per_row = np.bincount(rows, minlength=n)
+        offsets = np.zeros(n + 1, np.uint64)
+        np.cumsum(per_row, out=offsets[1:])
+        fl = FullVerletList(GATHER, float(build_scale), offsets, cols[o].astype(np.uint32))
+    return fl
+
+
+def reduce_full(ps: ParticleSet, box: SimulationBox, fl: FullVerletList, kernel: Kernel,
+                cfg: PassConfig = None, ctx=None) -> ReduceResult:
+    """reduce_full<Real,K> (baselines.hpp:47-129) on the GPU: precision F64 is
+    bit-equal to reduce_full<double>."""
+    cfg = cfg or PassConfig()
+    ctx = ctx or default_context()
+    if len(fl.offsets) != ps.size() + 1:
+        raise InputError("reduce_full: list/particle-set mismatch")
+    if cfg.query_scale > fl.build_scale:
+        raise InputError("reduce_full: query_scale exceeds the list's build scale")
+    ctx.set_particles(ps, box, sorted_slot=True)
+    ctx.set_full_list(fl)
+    return ctx.reduce_full(kernel, cfg, ps.size())
 
 
 # ----------------------------------------------------------------- store helpers (host)

@@ -459,6 +459,53 @@ int sfcnl_cu_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params* p, double* const* 
     return finish(c);
 }
 
+int sfcnl_cu_build_full_list(sfcnl_cu_ctx* c, double build_scale, uint64_t* num_pairs) {
+    CallScope scope(c);
+    if (int rc = run_build_full_list(c, build_scale)) return rc;
+    if (num_pairs) *num_pairs = c->full_pairs;
+    return finish(c);
+}
+
+int sfcnl_cu_get_full_list(sfcnl_cu_ctx* c, uint64_t* offsets, uint32_t* neighbors) {
+    CallScope scope(c);
+    if (!c->has_full) return set_error(c, SFCNL_INPUT_ERROR, "get_full_list: no full list");
+    if (int rc = download(c, offsets, c->full_off.p, (c->full_n + 1) * 8)) return rc;
+    if (int rc = download(c, neighbors, c->full_nbr.p, c->full_pairs * 4)) return rc;
+    return finish(c);
+}
+
+int sfcnl_cu_set_full_list(sfcnl_cu_ctx* c, uint64_t n, int mode, double build_scale, const uint64_t* offsets,
+                           const uint32_t* neighbors, uint64_t num_pairs) {
+    CallScope scope(c);
+    if (mode != 0 && mode != 1) return set_error(c, SFCNL_INPUT_ERROR, "set_full_list: unknown list mode");
+    if (!offsets) return set_error(c, SFCNL_INPUT_ERROR, "set_full_list: null offsets");
+    if (offsets[0] != 0 || offsets[n] != num_pairs)
+        return set_error(c, SFCNL_INPUT_ERROR, "set_full_list: offsets do not span the neighbor array");
+    for (uint64_t i = 0; i < n; ++i)
+        if (offsets[i + 1] < offsets[i]) return set_error(c, SFCNL_INPUT_ERROR, "set_full_list: offsets not monotone");
+    for (uint64_t k = 0; k < num_pairs; ++k)
+        if (neighbors[k] >= n) return set_error(c, SFCNL_INPUT_ERROR, "set_full_list: neighbor index out of range");
+    c->has_full = false;
+    if (int rc = upload(c, c->full_off, offsets, (n + 1) * 8)) return rc;
+    if (int rc = upload(c, c->full_nbr, neighbors, num_pairs * 4)) return rc;
+    c->full_n = n, c->full_pairs = num_pairs, c->full_scale = build_scale, c->full_mode = mode;
+    c->has_full = true;
+    return finish(c);
+}
+
+int sfcnl_cu_reduce_full(sfcnl_cu_ctx* c, const sfcnl_pass_params* p, double* const* outs, uint32_t* count) {
+    CallScope scope(c);
+    if (!p) return set_error(c, SFCNL_INPUT_ERROR, "null pass params");
+    if (int rc = run_reduce_full(c, *p)) return rc;
+    const int no = p->kernel >= 2 ? 4 : 1;
+    const uint64_t n = c->sorted.n;
+    if (outs)
+        for (int o = 0; o < no; ++o)
+            if (int rc = download(c, outs[o], c->outs[o].p, n * 8)) return rc;
+    if (int rc = download(c, count, c->ncount.p, n * 4)) return rc;
+    return finish(c);
+}
+
 int sfcnl_cu_build_store_range(sfcnl_cu_ctx* c, const sfcnl_build_params* p, uint64_t sc_begin, uint64_t sc_end,
                                double max_h, uint64_t* num_sc, uint64_t* blob_bytes) {
     CallScope scope(c);
@@ -595,6 +642,8 @@ int sfcnl_cu_device_array(sfcnl_cu_ctx* c, const char* name, void** ptr, uint64_
     else if (nm == "store.counts" && c->has_store) b = &c->counts, len = c->num_sc * 4;
     else if (nm == "store.offsets" && c->has_store) b = &c->offsets, len = (c->num_sc + 1) * 8;
     else if (nm == "store.blob" && c->has_store) b = &c->blob, len = c->blob_bytes;
+    else if (nm == "full.offsets" && c->has_full) b = &c->full_off, len = (c->full_n + 1) * 8;
+    else if (nm == "full.neighbors" && c->has_full) b = &c->full_nbr, len = c->full_pairs * 4;
     else if (nm.rfind("orig.", 0) == 0 && c->orig.valid) {
         const std::string f = nm.substr(5);
         Slot& o = c->orig;

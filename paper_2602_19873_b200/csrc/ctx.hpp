@@ -131,6 +131,13 @@ struct sfcnl_cu_ctx {
     sfcnl_cu::DBuf work_ctr;  // dynamic work counter of the warp-per-SC kernels
     sfcnl_cu::DBuf frame, frame_x;  // cluster-frame fp32 positions (+ payload), max |offset| per axis (frame.cu)
 
+    // full Verlet list baseline (pass_full.cuh): CSR offsets u64[n+1], neighbors u32
+    bool has_full = false;
+    uint64_t full_n = 0, full_pairs = 0;
+    double full_scale = 0;
+    int full_mode = 0;
+    sfcnl_cu::DBuf full_cnt, full_off, full_nbr;
+
     // errors
     sfcnl_cu::DBuf derr;  // DevError
     sfcnl_cu::DBuf ptrs;  // small pointer tables
@@ -164,6 +171,8 @@ int run_cluster_geometry(sfcnl_cu_ctx* c, uint32_t ci, uint32_t cj, uint64_t p0 
                          const uint8_t* jflags = nullptr);
 int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, uint64_t sc1, double max_h);
 int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p);
+int run_build_full_list(sfcnl_cu_ctx* c, double build_scale);
+int run_reduce_full(sfcnl_cu_ctx* c, const sfcnl_pass_params& p);
 // cluster-frame staging copy of the sorted positions (frame.cu); m = payload or null
 // clusters overlapping particles [p_lo, p_hi) plus those flagged in jflags (if non-null)
 int run_frame(sfcnl_cu_ctx* c, uint32_t cj, const double* m, uint64_t p_lo = 0, uint64_t p_hi = ~0ull,

@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "ctx.hpp"
+#include "scan.hpp"
 
 namespace sfcnl_cu {
 namespace {
@@ -343,6 +344,7 @@ __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& 
 #include "pass_ws.cuh"
 #include "pass_warp.cuh"
 #include "pass_item.cuh"
+#include "pass_full.cuh"
 
 // Device-side block-offset index of an uploaded store: warp per SC walks the codec
 // block headers (first kBtab blocks) and records where each block starts.
@@ -503,6 +505,122 @@ int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p) {
                                         "trailing bytes in index blob",
                                         "raw index blob length mismatch",
                                         "reduce: coincident particles"};
+    return check_dev_error(c, kMsgs);
+}
+
+// ------------------------------------------------------------ full Verlet list (f3)
+int run_build_full_list(sfcnl_cu_ctx* c, double build_scale) {
+    if (!c->sorted.valid) return set_error(c, 1, "build_full_list: no particles");
+    if (!c->has_store) return set_error(c, 1, "build_full_list: no neighbor store");
+    const uint64_t n = c->sorted.n;
+    if (c->store_n != n) return set_error(c, 1, "build_full_list: store/particle-set size mismatch");
+    if (c->sp.mode != 0) return set_error(c, 1, "build_full_list: the store must be a gather store");
+    if (c->sc_base != 0 || c->num_sc != (n + 63) / 64)
+        return set_error(c, 1, "build_full_list: the store must cover every super-cluster");
+    if (!(build_scale >= 0)) return set_error(c, 1, "build_full_list: build_scale must be >= 0");
+    if (build_scale > c->sp.build_radius_scale)
+        return set_error(c, 1, "build_full_list: build_scale exceeds the store's build radius scale");
+    if (n >= (1ull << 32)) return set_error(c, 1, "build_full_list: more than 2^32 particles");
+    PassArgs A{};
+    A.n = n;
+    A.box = c->sorted.box;
+    A.ci = c->sp.ci, A.cj = c->sp.cj, A.icl_per_sc = 64 / c->sp.ci, A.mask_bytes = (A.icl_per_sc + 7) / 8;
+    A.w = c->sp.w, A.compress = c->sp.compress;
+    A.sc_begin = 0, A.num_sc = c->num_sc, A.num_icl = (n + A.ci - 1) / A.ci;
+    A.counts = c->counts.as<uint32_t>(), A.offsets = c->offsets.as<uint64_t>(), A.blob = c->blob.as<uint8_t>();
+    A.x = c->sorted.x.as<double>(), A.y = c->sorted.y.as<double>(), A.z = c->sorted.z.as<double>();
+    A.h = c->sorted.h.as<double>();
+    A.qs = build_scale;
+    A.err = c->derr.as<DevError>();
+    SFCNL_CUDA_TRY(c->full_cnt.reserve((n + 1) * 4));
+    SFCNL_CUDA_TRY(c->full_off.reserve((n + 1) * 8));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(c->full_cnt.p, 0, (n + 1) * 4, c->stream));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(c->derr.p, 0xff, sizeof(DevError), c->stream));
+    c->has_full = false;
+    stage_begin(c, kPass);
+    const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(A.num_sc, uint64_t(c->num_sms) * 32)));
+    if (A.num_sc)
+        launch(c, k_full_list<false>, dim3(grid), dim3(kExactThreads), 0, A, c->full_cnt.as<uint32_t>(),
+               (const uint64_t*)nullptr, (uint32_t*)nullptr);
+    if (int rc = excl_scan(c, c->full_cnt.as<uint32_t>(), c->full_off.as<uint64_t>(), n + 1)) return rc;
+    uint64_t pairs = 0;
+    SFCNL_CUDA_TRY(cudaMemcpyAsync(&pairs, c->full_off.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, c->stream));
+    SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    SFCNL_CUDA_TRY(c->full_nbr.reserve(std::max<uint64_t>(pairs, 1) * 4));
+    if (A.num_sc)
+        launch(c, k_full_list<true>, dim3(grid), dim3(kExactThreads), 0, A, (uint32_t*)nullptr,
+               c->full_off.as<const uint64_t>(), c->full_nbr.as<uint32_t>());
+    SFCNL_CUDA_TRY(cudaGetLastError());
+    stage_end(c, kPass);
+    static const char* const kMsgs[] = {"",
+                                        "blob slice too short for bitmasks",
+                                        "truncated bitmask",
+                                        "truncated nibble stream",
+                                        "trailing bytes in index blob",
+                                        "raw index blob length mismatch",
+                                        ""};
+    if (int rc = check_dev_error(c, kMsgs)) return rc;
+    c->full_n = n, c->full_pairs = pairs, c->full_scale = build_scale, c->full_mode = 0;
+    c->has_full = true;
+    return 0;
+}
+
+int run_reduce_full(sfcnl_cu_ctx* c, const sfcnl_pass_params& p) {
+    if (!c->sorted.valid) return set_error(c, 1, "reduce_full: no particles");
+    if (!c->has_full) return set_error(c, 1, "reduce_full: no full list");
+    const uint64_t n = c->sorted.n;
+    if (c->full_n != n) return set_error(c, 1, "reduce_full: list/particle-set mismatch");
+    if (!(p.query_scale >= 0)) return set_error(c, 1, "PassConfig: query_scale must be >= 0");
+    if (p.query_scale > c->full_scale) return set_error(c, 1, "reduce_full: query_scale exceeds the list's build scale");
+    if (p.kernel < 0 || p.kernel > 3) return set_error(c, 1, "reduce_full: unknown kernel");
+    PassArgs A{};
+    if (p.kernel == SFCNL_KERNEL_DENSITY) {
+        auto* f = c->sorted.find("m");
+        if (!f) return set_error(c, 1, "ParticleSet: no such field: m");
+        A.m = f->data.as<double>();
+    }
+    if (p.kernel == SFCNL_KERNEL_LJ_COULOMB) {
+        auto* f = c->sorted.find("q");
+        if (!f) return set_error(c, 1, "ParticleSet: no such field: q");
+        A.q = f->data.as<double>();
+    }
+    const int no = p.kernel >= 2 ? 4 : 1;
+    for (int o = 0; o < no; ++o) SFCNL_CUDA_TRY(c->outs[o].reserve(std::max<uint64_t>(n, 1) * 8));
+    SFCNL_CUDA_TRY(c->ncount.reserve(std::max<uint64_t>(n, 1) * 4));
+    if (n == 0) return 0;
+    A.n = n;
+    A.box = c->sorted.box;
+    A.symmetric = c->full_mode != 0;
+    A.x = c->sorted.x.as<double>(), A.y = c->sorted.y.as<double>(), A.z = c->sorted.z.as<double>();
+    A.h = c->sorted.h.as<double>();
+    A.qs = p.query_scale, A.eps = p.epsilon, A.sigma = p.sigma, A.ck = p.coulomb_k;
+    for (int o = 0; o < 4; ++o) A.out[o] = c->outs[o].as<double>();
+    A.cnt = c->ncount.as<uint32_t>();
+    A.err = c->derr.as<DevError>();
+    SFCNL_CUDA_TRY(cudaMemsetAsync(c->derr.p, 0xff, sizeof(DevError), c->stream));
+    const uint64_t* off = c->full_off.as<const uint64_t>();
+    const uint32_t* nb = c->full_nbr.as<const uint32_t>();
+    stage_begin(c, kPass);
+    if (p.precision == 1) {
+        const unsigned grid = unsigned(std::min<uint64_t>((n + 7) / 8, uint64_t(c->num_sms) * 64));
+        switch (p.kernel) {
+            case 0: launch(c, k_reduce_full_warp<0>, dim3(grid), dim3(256), 0, A, off, nb); break;
+            case 1: launch(c, k_reduce_full_warp<1>, dim3(grid), dim3(256), 0, A, off, nb); break;
+            case 2: launch(c, k_reduce_full_warp<2>, dim3(grid), dim3(256), 0, A, off, nb); break;
+            default: launch(c, k_reduce_full_warp<3>, dim3(grid), dim3(256), 0, A, off, nb); break;
+        }
+    } else {
+        const unsigned grid = unsigned(std::min<uint64_t>((n + 127) / 128, uint64_t(c->num_sms) * 16));
+        switch (p.kernel) {
+            case 0: launch(c, k_reduce_full_exact<0>, dim3(grid), dim3(128), 0, A, off, nb); break;
+            case 1: launch(c, k_reduce_full_exact<1>, dim3(grid), dim3(128), 0, A, off, nb); break;
+            case 2: launch(c, k_reduce_full_exact<2>, dim3(grid), dim3(128), 0, A, off, nb); break;
+            default: launch(c, k_reduce_full_exact<3>, dim3(grid), dim3(128), 0, A, off, nb); break;
+        }
+    }
+    SFCNL_CUDA_TRY(cudaGetLastError());
+    stage_end(c, kPass);
+    static const char* const kMsgs[] = {"", "", "", "", "", "", "reduce_full: coincident particles"};
     return check_dev_error(c, kMsgs);
 }
 
