@@ -190,6 +190,11 @@ int sfcnl_cu_set_full_list(sfcnl_cu_ctx* ctx, uint64_t n, int mode, double build
 int sfcnl_cu_reduce_full(sfcnl_cu_ctx* ctx, const sfcnl_pass_params* params, double* const* outs,
                          uint32_t* neighbor_count);
 
+/* Numerator of cluster_overhead (bench.cpp:93-122) for the current gather store:
+ * the pair slots the pass evaluates, sum over entries and set mask bits of
+ * |i-cluster| * |j-cluster|. overhead = slots / true directed pairs. */
+int sfcnl_cu_cluster_slots(sfcnl_cu_ctx* ctx, uint64_t* slots);
+
 /* ---- (6) SFC domain decomposition -----------------------------
  * The reference is single-process; these entry points let one process per GPU
  * own a contiguous range of super-clusters of the GLOBAL sorted order while the

@@ -337,6 +337,16 @@ class Oracle:
         finally:
             self._f("full_free")(h)
 
+    def cluster_overhead(self, st: Store, true_pairs):
+        """bench::cluster_overhead (bench.cpp:93-122) of a gather store."""
+        assert self.kind == "reference"
+        out = D()
+        blob = st.blob if len(st.blob) else np.zeros(1, np.uint8)
+        self._check(self._f("cluster_overhead")(U64(st.n), U32(st.ci), U32(st.cj), C.c_int(st.w), C.c_int(st.compress),
+                                                U64(len(st.counts)), _p(st.counts, U32), _p(st.offsets, U64),
+                                                _p(blob, U8), U64(len(st.blob)), U64(int(true_pairs)), C.byref(out)))
+        return out.value
+
     # ---- codec
     def encode(self, idx, w=32):
         idx = np.ascontiguousarray(idx, np.uint32)

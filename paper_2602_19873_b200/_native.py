@@ -82,7 +82,7 @@ EXPORTS = [
     "sfcnl_cu_read_sorted", "sfcnl_cu_read_order", "sfcnl_cu_set_keys", "sfcnl_cu_apply_order_into",
     "sfcnl_cu_node_geometry_range", "sfcnl_cu_halo_mark", "sfcnl_cu_device_array",
     "sfcnl_cu_set_particle_records", "sfcnl_cu_build_full_list", "sfcnl_cu_get_full_list",
-    "sfcnl_cu_set_full_list", "sfcnl_cu_reduce_full",
+    "sfcnl_cu_set_full_list", "sfcnl_cu_reduce_full", "sfcnl_cu_cluster_slots",
 ]
 
 _lib = None
@@ -148,6 +148,7 @@ def lib():
         "sfcnl_cu_get_full_list": (C.c_int, [P, P, P]),
         "sfcnl_cu_set_full_list": (C.c_int, [P, u64, C.c_int, C.c_double, P, P, u64]),
         "sfcnl_cu_reduce_full": (C.c_int, [P, C.POINTER(PassParamsC), C.POINTER(P), P]),
+        "sfcnl_cu_cluster_slots": (C.c_int, [P, C.POINTER(u64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -487,6 +487,12 @@ class Context:
         self.check(self.L.sfcnl_cu_reduce_full(self.h, C.byref(pp), arr, _ptr(cnt)))
         return ReduceResult(list(kernel.names), outs, cnt)
 
+    def cluster_slots(self):
+        """Pair slots of the current gather store (cluster_overhead numerator)."""
+        v = C.c_uint64()
+        self.check(self.L.sfcnl_cu_cluster_slots(self.h, C.byref(v)))
+        return v.value
+
     # domain decomposition (include/sfcnl_cu.h section (6)) ----------------
     def set_particles_device(self, n, cols, names, box: SimulationBox):
         """Orig slot from device arrays: cols = [x, y, z, h, *fields] (torch CUDA tensors)."""
@@ -708,6 +714,18 @@ def reduce_full(ps: ParticleSet, box: SimulationBox, fl: FullVerletList, kernel:
     ctx.set_particles(ps, box, sorted_slot=True)
     ctx.set_full_list(fl)
     return ctx.reduce_full(kernel, cfg, ps.size())
+
+
+def cluster_overhead(store: NeighborStore, true_directed_pairs: int, ctx=None) -> float:
+    """bench::cluster_overhead (bench.cpp:93-122): evaluated pair slots / true directed
+    pairs; the slot count is a device pass over the store (k_cluster_slots)."""
+    if store.build.mode != GATHER:
+        raise InputError("cluster_overhead: requires a gather-mode store")
+    if true_directed_pairs == 0:
+        raise InputError("cluster_overhead: no in-range pairs")
+    ctx = ctx or default_context()
+    ctx.set_store(store)
+    return ctx.cluster_slots() / float(true_directed_pairs)
 
 
 # ----------------------------------------------------------------- store helpers (host)

@@ -58,7 +58,7 @@ struct BuildArgs {
     uint32_t* sizes;
     uint64_t* soff;
     uint8_t* scratch;
-    unsigned long long* ctl;  // [0] scratch top, [1] overflow count, [2] scratch overflow flag
+    unsigned long long* ctl;  // [0] scratch top, [1] overflow count, [2] scratch overflow flag, [3] max h bits, [4] medium-tier overflow count
     uint64_t scratch_cap;
     uint32_t* overflow_list;
     uint16_t* btab;  // device-side block-offset index for the pass (first 16 blocks per SC)
@@ -626,7 +626,7 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
     }
     SFCNL_CUDA_TRY(c->sc_size.reserve(num_sc * 4));
     SFCNL_CUDA_TRY(c->sc_scratch_off.reserve(num_sc * 8));
-    SFCNL_CUDA_TRY(c->overflow_list.reserve(num_sc * 4));
+    SFCNL_CUDA_TRY(c->overflow_list.reserve(num_sc * 8));  // main-tier list, then medium-tier list
     uint64_t scratch_cap = std::max<uint64_t>(c->scratch.bytes, (p_hi - p_lo) * 16 + (1 << 20));
 
     BuildArgs A;
@@ -661,12 +661,14 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
         A.btab = c->btab.as<uint16_t>() - sc0 * 16;
     }
 
-    unsigned long long ctl[3];
+    unsigned long long ctl[5];
     for (int attempt = 0; attempt < 3; ++attempt) {
+        const uint32_t* ovf_list = A.overflow_list;
+        unsigned long long ovf_count = 0;
         SFCNL_CUDA_TRY(c->scratch.reserve(scratch_cap));
         A.scratch = c->scratch.as<uint8_t>();
         A.scratch_cap = c->scratch.bytes;
-        SFCNL_CUDA_TRY(cudaMemsetAsync(c->build_ctl.p, 0, 3 * 8, c->stream));
+        SFCNL_CUDA_TRY(cudaMemsetAsync(c->build_ctl.p, 0, 5 * 8, c->stream));
         stage_begin(c, kBuild);
         if (p.ci == 8 && (p.cj == 8 || p.cj == 4) && p.mode == 0) {
             // warp-per-SC kernel (build_warp.cuh) on the cluster-frame staging copy
@@ -680,21 +682,40 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
             A.frame = c->frame.as<const float4>();
             A.frame_x = c->frame_x.as<const unsigned>();
             const size_t smem = size_t(kBwWarps) * sizeof(BwSmem);
-            cudaFuncSetAttribute(k_build_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            cudaFuncSetAttribute(k_build_warp<BwSmem, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             SFCNL_CUDA_TRY(c->work_ctr.reserve(8));
             SFCNL_CUDA_TRY(cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream));
             const unsigned grid = unsigned(std::max<uint64_t>(
                 1, std::min<uint64_t>((num_sc + kBwWarps - 1) / kBwWarps, uint64_t(c->num_sms) * 5)));
-            launch(c, k_build_warp, dim3(grid), dim3(kBwWarps * 32), smem, A, sc0, sc1,
-                   c->work_ctr.as<unsigned long long>());
+            launch(c, k_build_warp<BwSmem, 5>, dim3(grid), dim3(kBwWarps * 32), smem, A, sc0, sc1,
+                   c->work_ctr.as<unsigned long long>(), (const uint32_t*)nullptr, A.overflow_list, 1);
+            SFCNL_CUDA_TRY(cudaGetLastError());
+            SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
+            SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+            if (ctl[1]) {  // medium tier over the overflow list; what still overflows -> ctl[4]
+                const size_t smem_m = size_t(kBwWarps) * sizeof(BwSmemM);
+                cudaFuncSetAttribute(k_build_warp<BwSmemM, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_m));
+                SFCNL_CUDA_TRY(cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream));
+                const unsigned grid_m = unsigned(std::max<uint64_t>(
+                    1, std::min<uint64_t>((ctl[1] + kBwWarps - 1) / kBwWarps, uint64_t(c->num_sms) * 3)));
+                launch(c, k_build_warp<BwSmemM, 3>, dim3(grid_m), dim3(kBwWarps * 32), smem_m, A, uint64_t(0),
+                       uint64_t(ctl[1]), c->work_ctr.as<unsigned long long>(), (const uint32_t*)A.overflow_list,
+                       A.overflow_list + num_sc, 4);
+                SFCNL_CUDA_TRY(cudaGetLastError());
+                SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
+                SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+                ovf_list = A.overflow_list + num_sc;
+                ovf_count = ctl[4];
+            }
         } else {
             const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(num_sc, uint64_t(c->num_sms) * 64)));
             launch(c, k_build_smem, dim3(grid), dim3(kBuildThreads), 0, A, sc0, sc1);
+            SFCNL_CUDA_TRY(cudaGetLastError());
+            SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
+            SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+            ovf_count = ctl[1];
         }
-        SFCNL_CUDA_TRY(cudaGetLastError());
-        SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 3 * 8, cudaMemcpyDeviceToHost, c->stream));
-        SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
-        if (ctl[1]) {
+        if (ovf_count) {
             // capacity fallback in global memory: same code, big workspaces
             const uint64_t ncl = (n + p.cj - 1) / p.cj;
             const uint32_t fcap = uint32_t(std::min<uint64_t>(c->num_nodes + 8, 0xffffffffull));
@@ -702,13 +723,12 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
             const uint32_t ecap = uint32_t(std::min<uint64_t>(uint64_t(ccap) * (A.mask_bytes + 10) + 64, 0xfffffff0ull));
             const uint64_t stride =
                 ((uint64_t(fcap) * 8 + uint64_t(ccap) * 4 + 16 + uint64_t(ccap) * 8 + ecap) + 255) & ~uint64_t(255);
-            const uint64_t nblk = std::min<uint64_t>(ctl[1], 64);  // SCs too large for the warp slices
+            const uint64_t nblk = std::min<uint64_t>(ovf_count, 64);  // SCs too large for the warp slices
             SFCNL_CUDA_TRY(c->fallback_ws.reserve(stride * nblk));
-            launch(c, k_build_global, dim3(unsigned(nblk)), dim3(kBuildThreads), 0, A,
-                   (const uint32_t*)A.overflow_list, uint64_t(ctl[1]), c->fallback_ws.as<uint8_t>(), stride,
-                   fcap, ccap, ecap);
+            launch(c, k_build_global, dim3(unsigned(nblk)), dim3(kBuildThreads), 0, A, (const uint32_t*)ovf_list,
+                   uint64_t(ovf_count), c->fallback_ws.as<uint8_t>(), stride, fcap, ccap, ecap);
             SFCNL_CUDA_TRY(cudaGetLastError());
-            SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 3 * 8, cudaMemcpyDeviceToHost, c->stream));
+            SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
             SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
             static const char* const kMsgs[] = {"", "", "", "build_neighbor_store: workspace capacity exceeded"};
             const int rc = check_dev_error(c, kMsgs);

@@ -36,12 +36,18 @@ constexpr uint32_t kBwE = 384;   // entries per SC (~170 at 200 neighbours)
 constexpr uint32_t kBwBytes = 4096;  // encoded bytes (aliases the frontier)
 constexpr uint32_t kLeafCacheCap = 256;  // accepted leaves kept per SC by halo marking
 
-struct BwSmem {
+// Per-warp shared-memory slice. Two capacity tiers: the main kernel runs every SC with
+// the small one (5 CTAs x 4 warps per SM); SCs that exceed it (dense lists, wide skins,
+// 8x4 clusters at high neighbour counts) are re-run from the overflow list with the
+// medium one (3 CTAs x 4 warps per SM); only SCs beyond that go to k_build_global.
+template <uint32_t F, uint32_t E, uint32_t B>
+struct BwSmemT {
+    static constexpr uint32_t kF = F, kE = E, kB = B;
     union {
         struct {
-            uint32_t fa[kBwF], fb[kBwF];  // traversal frontier, then per-leaf candidate prefix
+            uint32_t fa[F], fb[F];  // traversal frontier, then per-leaf candidate prefix
         } t;
-        uint8_t ebuf[kBwBytes];  // encoder output (after the masks: the frontier is dead)
+        uint8_t ebuf[B];  // encoder output (after the masks: the frontier is dead)
     } u;
     float4 sa[4][32];  // staged j pairs [p][candidate]: {x_2p, x_2p+1, y_2p, y_2p+1}
     float2 sz[4][32];  //                                 {z_2p, z_2p+1}
@@ -51,9 +57,11 @@ struct BwSmem {
     float pthr[8];
     uint32_t cmask[32];
     uint8_t items[256];
-    uint32_t eidx[kBwE];
-    uint8_t emsk[kBwE];
+    uint32_t eidx[E];
+    uint8_t emsk[E];
 };
+using BwSmem = BwSmemT<kBwF, kBwE, kBwBytes>;
+using BwSmemM = BwSmemT<1024, 1024, 8192>;
 
 // Guard band on a squared distance near r^2 when every coordinate difference carries
 // an absolute error <= ecoord + 2^-24 r (see pass.cu); factor 4 margin.
@@ -74,7 +82,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // up in key order in *out (one of the two buffers). Returns their number, or ~0u
 // when the frontier exceeds kBwF.
 __device__ __forceinline__ uint32_t warp_bfs(const BuildArgs& A, const Geo& scg, double r2, uint32_t* fa,
-                                             uint32_t* fb, uint32_t** out) {
+                                             uint32_t* fb, uint32_t** out, uint32_t cap = kBwF) {
     const unsigned lane = lane_id();
     if (lane == 0) fa[0] = 0;
     uint32_t nA = 1;
@@ -103,7 +111,7 @@ __device__ __forceinline__ uint32_t warp_bfs(const BuildArgs& A, const Geo& scg,
             }
             const uint32_t inc = warp_incl_scan(emit);
             const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
-            if (nB + tot > kBwF) return ~0u;
+            if (nB + tot > cap) return ~0u;
             const uint32_t at = nB + inc - emit;
             if (emit == 1) fb[at] = e | kTag;
             if (emit == 8) {
@@ -150,7 +158,8 @@ __device__ __forceinline__ void sc_box(const BuildArgs& A, uint64_t icl_base, ui
     } while (0)
 #endif
 
-__device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
+template <class Sm>
+__device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
     const unsigned lane = lane_id();
 #ifdef SFCNL_PHASE_PROF
     long long _tprev = clock64();
@@ -225,7 +234,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
             fa = S.u.t.fa, nA = cnt;
         }
     }
-    if (nA == ~0u) nA = warp_bfs(A, scg, r2, S.u.t.fa, S.u.t.fb, &fa);
+    if (nA == ~0u) nA = warp_bfs(A, scg, r2, S.u.t.fa, S.u.t.fb, &fa, Sm::kF);
     if (nA == ~0u) return false;
     uint32_t* fb = fa == S.u.t.fa ? S.u.t.fb : S.u.t.fa;
 
@@ -486,7 +495,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
         // ordered compaction of the chunk's entries with mask != 0
         const bool keep = valid && mask != 0;
         const unsigned kb = __ballot_sync(0xffffffffu, keep);
-        if (nE + __popc(kb) > kBwE) return false;
+        if (nE + __popc(kb) > Sm::kE) return false;
         if (keep) {
             const uint32_t at = nE + __popc(kb & lanemask_lt());
             S.eidx[at] = cand, S.emsk[at] = uint8_t(mask);
@@ -500,11 +509,11 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
     // ---- 5b. serialization (neighbor_build.cpp:164-182): masks, then the index list
     uint8_t* ebuf = S.u.ebuf;
     const uint32_t mbytes = nE;  // one mask byte per entry (ci == 8)
-    if (mbytes + 4 > kBwBytes) return false;
+    if (mbytes + 4 > Sm::kB) return false;
     for (uint32_t k = lane; k < nE; k += 32) ebuf[k] = S.emsk[k];
     uint32_t pos = mbytes;
     if (!A.compress) {
-        if (mbytes + 4 * nE > kBwBytes) return false;
+        if (mbytes + 4 * nE > Sm::kB) return false;
         for (uint32_t k = lane; k < nE; k += 32) {
             const uint32_t v = S.eidx[k];
 #pragma unroll
@@ -537,7 +546,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
             const uint32_t inc1 = warp_incl_scan(nd[1]);
             const uint32_t nib = ninfo + tot0 + __shfl_sync(0xffffffffu, inc1, 31);
             const uint32_t bsize = w / 8 + (nib + 1) / 2;
-            if (pos + bsize > kBwBytes) return false;
+            if (pos + bsize > Sm::kB) return false;
             const unsigned long long bm = (unsigned long long)m0 | ((unsigned long long)m1 << 32);
             if (lane < w / 8) ebuf[pos + lane] = uint8_t(bm >> (8 * lane));
             if (lane == 0 && A.btab && bb / w < 16) A.btab[sc * 16 + bb / w] = uint16_t(pos - mbytes);
@@ -592,20 +601,26 @@ __device__ bool build_sc_warp(const BuildArgs& A, BwSmem& S, uint64_t sc) {
     return true;
 }
 
-__global__ void __launch_bounds__(kBwWarps * 32, 5) k_build_warp(const __grid_constant__ BuildArgs A, uint64_t sc_begin,
-                                                                  uint64_t sc_end, unsigned long long* __restrict__ work) {
+// list == nullptr: SCs [sc_begin, sc_end) (main tier); else the `count` SCs of list
+// (overflow re-run). SCs beyond this tier's capacity go to overflow_out / ctl[ctl_slot].
+template <class Sm, int MINB>
+__global__ void __launch_bounds__(kBwWarps * 32, MINB) k_build_warp(const __grid_constant__ BuildArgs A, uint64_t sc_begin,
+                                                                     uint64_t sc_end, unsigned long long* __restrict__ work,
+                                                                     const uint32_t* __restrict__ list,
+                                                                     uint32_t* __restrict__ overflow_out, int ctl_slot) {
     extern __shared__ __align__(16) unsigned char dsm[];
-    BwSmem& S = reinterpret_cast<BwSmem*>(dsm)[threadIdx.x >> 5];
+    Sm& S = reinterpret_cast<Sm*>(dsm)[threadIdx.x >> 5];
     const unsigned lane = lane_id();
     for (;;) {
         unsigned long long t = 0;
         if (lane == 0) t = atomicAdd(work, 1ull);
-        const uint64_t sc = sc_begin + __shfl_sync(0xffffffffu, t, 0);
-        if (sc >= sc_end) break;
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (sc_begin + t >= sc_end) break;
+        const uint64_t sc = list ? uint64_t(list[t]) : sc_begin + t;
         if (!build_sc_warp(A, S, sc)) {
             if (lane == 0) {
-                const unsigned long long slot = atomicAdd(&A.ctl[1], 1ull);
-                A.overflow_list[slot] = uint32_t(sc);
+                const unsigned long long slot = atomicAdd(&A.ctl[ctl_slot], 1ull);
+                overflow_out[slot] = uint32_t(sc);
                 A.counts[sc] = 0, A.sizes[sc] = 0, A.soff[sc] = 0;
             }
         }

@@ -506,6 +506,14 @@ int sfcnl_cu_reduce_full(sfcnl_cu_ctx* c, const sfcnl_pass_params* p, double* co
     return finish(c);
 }
 
+int sfcnl_cu_cluster_slots(sfcnl_cu_ctx* c, uint64_t* slots) {
+    CallScope scope(c);
+    uint64_t v = 0;
+    if (int rc = run_cluster_slots(c, &v)) return rc;
+    if (slots) *slots = v;
+    return finish(c);
+}
+
 int sfcnl_cu_build_store_range(sfcnl_cu_ctx* c, const sfcnl_build_params* p, uint64_t sc_begin, uint64_t sc_end,
                                double max_h, uint64_t* num_sc, uint64_t* blob_bytes) {
     CallScope scope(c);

@@ -173,6 +173,7 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
 int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p);
 int run_build_full_list(sfcnl_cu_ctx* c, double build_scale);
 int run_reduce_full(sfcnl_cu_ctx* c, const sfcnl_pass_params& p);
+int run_cluster_slots(sfcnl_cu_ctx* c, uint64_t* slots);
 // cluster-frame staging copy of the sorted positions (frame.cu); m = payload or null
 // clusters overlapping particles [p_lo, p_hi) plus those flagged in jflags (if non-null)
 int run_frame(sfcnl_cu_ctx* c, uint32_t cj, const double* m, uint64_t p_lo = 0, uint64_t p_hi = ~0ull,

@@ -624,4 +624,37 @@ int run_reduce_full(sfcnl_cu_ctx* c, const sfcnl_pass_params& p) {
     return check_dev_error(c, kMsgs);
 }
 
+int run_cluster_slots(sfcnl_cu_ctx* c, uint64_t* slots) {
+    if (!c->has_store) return set_error(c, 1, "cluster_overhead: no neighbor store");
+    if (c->sp.mode != 0) return set_error(c, 1, "cluster_overhead: requires a gather-mode store");
+    const uint64_t n = c->store_n;
+    PassArgs A{};
+    A.n = n;
+    A.ci = c->sp.ci, A.cj = c->sp.cj, A.icl_per_sc = 64 / c->sp.ci, A.mask_bytes = (A.icl_per_sc + 7) / 8;
+    A.w = c->sp.w, A.compress = c->sp.compress;
+    A.sc_begin = c->sc_base, A.num_sc = c->sc_base + c->num_sc, A.num_icl = (n + A.ci - 1) / A.ci;
+    A.counts = c->counts.as<uint32_t>() - c->sc_base, A.offsets = c->offsets.as<uint64_t>() - c->sc_base;
+    A.blob = c->blob.as<uint8_t>();
+    A.err = c->derr.as<DevError>();
+    SFCNL_CUDA_TRY(c->work_ctr.reserve(8));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(c->derr.p, 0xff, sizeof(DevError), c->stream));
+    if (c->num_sc) {
+        const unsigned grid = unsigned(std::min<uint64_t>(c->num_sc, uint64_t(c->num_sms) * 32));
+        launch(c, k_cluster_slots, dim3(grid), dim3(kExactThreads), 0, A, c->work_ctr.as<unsigned long long>());
+    }
+    SFCNL_CUDA_TRY(cudaGetLastError());
+    static const char* const kMsgs[] = {"",
+                                        "blob slice too short for bitmasks",
+                                        "truncated bitmask",
+                                        "truncated nibble stream",
+                                        "trailing bytes in index blob",
+                                        "raw index blob length mismatch",
+                                        ""};
+    if (int rc = check_dev_error(c, kMsgs)) return rc;
+    SFCNL_CUDA_TRY(cudaMemcpyAsync(slots, c->work_ctr.p, 8, cudaMemcpyDeviceToHost, c->stream));
+    SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
 }  // namespace sfcnl_cu

@@ -133,3 +133,36 @@ __global__ void __launch_bounds__(256) k_reduce_full_warp(const __grid_constant_
         }
     }
 }
+
+// cluster_overhead numerator (bench.cpp:93-122): pair slots of a gather store --
+// for every entry and set mask bit b, |i-cluster b| * |j-cluster| (trailing partial
+// clusters counted at their size). One CTA per SC, thread per entry of a block.
+__global__ void __launch_bounds__(kExactThreads) k_cluster_slots(const __grid_constant__ PassArgs A,
+                                                                 unsigned long long* __restrict__ slots) {
+    __shared__ uint32_t s_idx[64];
+    __shared__ unsigned long long s_msk[64];
+    __shared__ int s_len;
+    const uint32_t t = threadIdx.x;
+    unsigned long long acc = 0;
+    for (uint64_t sc = A.sc_begin + blockIdx.x; sc < A.num_sc; sc += gridDim.x) {
+        ScStream st;
+        if (!open_sc(A, sc, st)) continue;
+        for (uint32_t first = 0; first < st.count; first += uint32_t(A.w)) {
+            const int len = next_block(A, sc, st, first, s_idx, s_msk, &s_len);
+            if (len < 0) break;
+            if (int(t) >= len) continue;
+            const uint64_t jb = uint64_t(s_idx[t]) * A.cj, je = tmin<uint64_t>(jb + A.cj, A.n);
+            const uint64_t cj_eff = je > jb ? je - jb : 0;
+            const unsigned long long m = s_msk[t];
+            for (uint32_t b = 0; b < A.icl_per_sc; ++b) {
+                if (!((m >> b) & 1ull)) continue;
+                const uint64_t gi = sc * A.icl_per_sc + b;
+                if (gi >= A.num_icl) continue;
+                const uint64_t ib = gi * A.ci, ie = tmin<uint64_t>(ib + A.ci, A.n);
+                acc += (ie - ib) * cj_eff;
+            }
+        }
+    }
+    for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+    if (lane_id() == 0 && acc) atomicAdd(slots, acc);
+}

@@ -3,7 +3,9 @@ UNMODIFIED reference's build_full_list (cell grid, baselines.cpp:39-131) and
 reduce_full<double> (baselines.hpp:47-129) through oracle/_ref on the particles of
 every tests/golden/*.npz fixture (SFC order and original order) and writes
 tests/golden/full_lists.npz: per case and order the pair count, the SHA-256 of
-offsets||neighbors, and the reduce_full<double> outputs of count / density / LJ.
+offsets||neighbors, the reduce_full<double> outputs of count / density / LJ, and
+(gather stores) bench::cluster_overhead of the fixture's store against the
+in-range pair count of the full list at query scale.
 Run in the build container:
 
     make -C oracle ref && python tests/golden/make_full_golden.py
@@ -54,6 +56,10 @@ def main():
                     assert np.array_equal(res[kern][1], g[f"{kern}_double_count"]), (name, kern)
                     for o in range(len(res[kern][0])):
                         assert np.array_equal(res[kern][0][o], g[f"{kern}_double_{o}"]), (name, kern, o)
+            if order == "sorted" and mode == 0:
+                from conftest import oracle_store
+                pairs_q = int(res["count"][1].astype(np.int64).sum())
+                out[name + ".overhead"] = np.array([R.cluster_overhead(oracle_store(g), pairs_q)])
             print(name, order, len(nb))
     np.savez_compressed(os.path.join(HERE, "full_lists.npz"), **out)
 

@@ -142,3 +142,27 @@ def test_gpu_reduce_full_symmetric_uploaded_list(ctx):
     bad = S.FullVerletList(S.GATHER, scale, off[:-1], nb)
     with pytest.raises(S.InputError, match="list/particle-set mismatch"):
         S.reduce_full(ps, box, bad, S.count_kernel(), ctx=ctx)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", GATHER_CASES)
+def test_gpu_cluster_overhead_matches_reference(ctx, name):
+    """bench::cluster_overhead (bench.cpp:93-122) from the device slot count."""
+    import paper_2602_19873_b200 as S
+    g = load_golden(name)
+    ci, cj, w, mode, comp = (int(v) for v in g["params"])
+    store = S.NeighborStore(S.BuildParams(S.ClusterParams(ci, cj, w), mode, bool(comp), float(g["scale"][0])),
+                            len(g["x"]), g["counts"], g["offsets"], g["blob"])
+    pairs = int(FULL[f"{name}.sorted.count.count"].astype(np.int64).sum())
+    assert S.cluster_overhead(store, pairs, ctx=ctx) == float(FULL[name + ".overhead"][0])
+    with pytest.raises(S.InputError, match="no in-range pairs"):
+        S.cluster_overhead(store, 0, ctx=ctx)
+
+
+def test_cluster_overhead_rejects_symmetric_store():
+    import paper_2602_19873_b200 as S
+    g = load_golden("uniform_symmetric")
+    store = S.NeighborStore(S.BuildParams(S.ClusterParams(8, 8, 32), S.SYMMETRIC, True, 1.0), len(g["x"]),
+                            g["counts"], g["offsets"], g["blob"])
+    with pytest.raises(S.InputError, match="requires a gather-mode store"):
+        S.cluster_overhead(store, 1)

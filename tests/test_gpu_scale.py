@@ -28,22 +28,25 @@ N = int(os.environ.get("SFCNL_SCALE_N", str(1 << 26)))
 
 
 CONFIGS = {
-    # name: (generator, n, spec kwargs, build radius scale, LJ sigma)
-    "C2": ("uniform", N, dict(density=float(N), target_neighbors=200.0), 1.0, 0.5 * (1.0 / N) ** (1.0 / 3.0)),
-    "C3": ("evrard", 1 << 24, dict(target_neighbors=200.0), 1.0, 0.5 * (1.0 / (1 << 24)) ** (1.0 / 3.0)),
-    "C4": ("uniform", 4_000_000, dict(density=100.0, target_neighbors=150.0), 1.100642, 0.2),
+    # name: (generator, n, spec kwargs, build radius scale, LJ sigma, (ci, cj, w))
+    "C2": ("uniform", N, dict(density=float(N), target_neighbors=200.0), 1.0, 0.5 * (1.0 / N) ** (1.0 / 3.0), (8, 8, 32)),
+    "C3": ("evrard", 1 << 24, dict(target_neighbors=200.0), 1.0, 0.5 * (1.0 / (1 << 24)) ** (1.0 / 3.0), (8, 8, 32)),
+    "C4": ("uniform", 4_000_000, dict(density=100.0, target_neighbors=150.0), 1.100642, 0.2, (8, 8, 32)),
+    # dense 8x4 lists (C4 sweep end): SCs beyond the small warp-build tier
+    # run the medium tier (and the global-memory fallback beyond that)
+    "C4-8x4-t400": ("uniform", 1 << 20, dict(density=100.0, target_neighbors=400.0), 1.100642, 0.2, (8, 4, 64)),
 }
 
 
 @pytest.fixture(scope="module", params=sorted(CONFIGS))
 def run(request):
-    gen, n, kw, scale, sigma = CONFIGS[request.param]
+    gen, n, kw, scale, sigma, (ci, cj, w) = CONFIGS[request.param]
     ctx = S.Context(0)
     if gen == "uniform":
         ps, box = S.make_uniform(S.UniformSpec(n=n, seed=42, **kw))
     else:
         ps, box = S.make_evrard(S.EvrardSpec(n=n, seed=42, **kw))
-    bp = S.BuildParams(S.ClusterParams(8, 8, 32), S.GATHER, True, scale)
+    bp = S.BuildParams(S.ClusterParams(ci, cj, w), S.GATHER, True, scale)
     ctx.set_particles(ps, box)
     ctx.sort()
     ctx.apply_order()
@@ -62,7 +65,7 @@ def run(request):
     rng = np.random.default_rng(5)
     starts = sorted({0, nsc - 48} | set(int(v) for v in rng.integers(0, nsc - 48, 3)))
     return dict(store=store, geo=geo, rho=rho, lj=lj, sp=sp, tree=tree, sigma=sigma, scale=scale,
-                ranges=[(s, s + 48) for s in starts])
+                ranges=[(s, s + 48) for s in starts], cp=(ci, cj, w))
 
 
 def _slice(store, sc0, sc1):
@@ -73,7 +76,8 @@ def _slice(store, sc0, sc1):
 def test_store_bit_exact_on_sampled_ranges(run):
     sp, tree, geo = run["sp"], run["tree"], run["geo"]
     for sc0, sc1 in run["ranges"]:
-        ref = P.build_store_range(sp, tree, geo, sc0, sc1, float(sp.h.max()), scale=run["scale"])
+        ci, cj, w = run["cp"]
+        ref = P.build_store_range(sp, tree, geo, sc0, sc1, float(sp.h.max()), scale=run["scale"], ci=ci, cj=cj, w=w)
         counts, blob = _slice(run["store"], sc0, sc1)
         assert np.array_equal(counts, ref.counts), (sc0, sc1)
         assert np.array_equal(blob, ref.blob), (sc0, sc1)
@@ -83,7 +87,8 @@ def _range_store(run, sc0, sc1):
     st = run["store"]
     counts, blob = _slice(st, sc0, sc1)
     offs = st.offsets[sc0:sc1 + 1] - st.offsets[sc0]
-    return Store(run["sp"].n, 8, 8, 32, 0, 1, run["scale"], counts.copy(), offs.astype(np.uint64), blob.copy())
+    ci, cj, w = run["cp"]
+    return Store(run["sp"].n, ci, cj, w, 0, 1, run["scale"], counts.copy(), offs.astype(np.uint64), blob.copy())
 
 
 def test_density_mixed_on_sampled_ranges(run):
@@ -110,10 +115,11 @@ def test_lj_mixed_on_sampled_ranges(run):
             if not c:
                 continue
             b, e = int(rs.offsets[s]), int(rs.offsets[s + 1])
-            idx, _ = P.decode(rs.blob[b + c:e], c, 32)
+            ci, cj, w = run["cp"]
+            idx, _ = P.decode(rs.blob[b + c:e], c, w)
             for k, jc in enumerate(idx):
                 mask = int(rs.blob[b + k])
-                js = np.arange(int(jc) * 8, min(int(jc) * 8 + 8, sp.n))
+                js = np.arange(int(jc) * cj, min(int(jc) * cj + cj, sp.n))
                 for bit in range(8):
                     if not (mask >> bit) & 1:
                         continue
