@@ -137,6 +137,9 @@ struct sfcnl_cu_ctx {
     double full_scale = 0;
     int full_mode = 0;
     sfcnl_cu::DBuf full_cnt, full_off, full_nbr;
+    // symmetric pass (pass_sym.cuh): entry base, j-side accumulators/counts, entry
+    // j-cluster/SC, transposed entry lists per j-cluster
+    sfcnl_cu::DBuf sym[8];
 
     // errors
     sfcnl_cu::DBuf derr;  // DevError

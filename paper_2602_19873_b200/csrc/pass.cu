@@ -345,6 +345,7 @@ __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& 
 #include "pass_warp.cuh"
 #include "pass_item.cuh"
 #include "pass_full.cuh"
+#include "pass_sym.cuh"
 
 // Device-side block-offset index of an uploaded store: warp per SC walks the codec
 // block headers (first kBtab blocks) and records where each block starts.
@@ -410,6 +411,50 @@ void launch_pass(sfcnl_cu_ctx* c, const PassArgs& A, bool fast) {
         const unsigned grid = unsigned(std::min<uint64_t>(A.num_sc - A.sc_begin, uint64_t(c->num_sms) * 32));
         launch(c, k_pass_exact<K>, dim3(grid), dim3(kExactThreads), 0, A);
     }
+}
+
+// Symmetric stores: the three-step deterministic pass of pass_sym.cuh.
+template <int K>
+int launch_sym(sfcnl_cu_ctx* c, const PassArgs& A) {
+    constexpr int NO = nout<K>();
+    const uint64_t num_sc = A.num_sc - A.sc_begin;
+    if (num_sc == 0) return 0;
+    auto& ebase = c->sym[0];
+    SFCNL_CUDA_TRY(ebase.reserve((num_sc + 1) * 8));
+    if (int rc = excl_scan(c, A.counts + A.sc_begin, ebase.as<uint64_t>(), num_sc)) return rc;
+    uint64_t last[2] = {0, 0};
+    uint32_t lastc = 0;
+    SFCNL_CUDA_TRY(cudaMemcpyAsync(last, ebase.as<uint64_t>() + num_sc - 1, 8, cudaMemcpyDeviceToHost, c->stream));
+    SFCNL_CUDA_TRY(cudaMemcpyAsync(&lastc, A.counts + A.num_sc - 1, 4, cudaMemcpyDeviceToHost, c->stream));
+    SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const uint64_t num_e = last[0] + lastc;
+    const uint64_t ncl = (A.n + A.cj - 1) / A.cj;
+    auto &jacc = c->sym[1], &jcnt = c->sym[2], &ejcl = c->sym[3], &esc = c->sym[4];
+    auto &tcnt = c->sym[5], &tstart = c->sym[6], &tlist = c->sym[7];
+    SFCNL_CUDA_TRY(jacc.reserve(std::max<uint64_t>(num_e, 1) * NO * A.cj * 8));
+    SFCNL_CUDA_TRY(jcnt.reserve(std::max<uint64_t>(num_e, 1) * A.cj * 4));
+    SFCNL_CUDA_TRY(ejcl.reserve(std::max<uint64_t>(num_e, 1) * 4));
+    SFCNL_CUDA_TRY(esc.reserve(std::max<uint64_t>(num_e, 1) * 4));
+    SFCNL_CUDA_TRY(tcnt.reserve((ncl + 1) * 4));
+    SFCNL_CUDA_TRY(tstart.reserve((ncl + 1) * 8));
+    SFCNL_CUDA_TRY(tlist.reserve(std::max<uint64_t>(num_e, 1) * 4));
+    const unsigned grid_sc = unsigned(std::min<uint64_t>(num_sc, uint64_t(c->num_sms) * 32));
+    // ebase is indexed by global SC: A.sc_begin == 0 for symmetric stores (whole range)
+    launch(c, k_sym_jside<K>, dim3(grid_sc), dim3(kExactThreads), 0, A, ebase.as<const uint64_t>(), jacc.as<double>(),
+           jcnt.as<uint32_t>(), ejcl.as<uint32_t>(), esc.as<uint32_t>());
+    const unsigned grid_e = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((num_e + 255) / 256, uint64_t(c->num_sms) * 16)));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(tcnt.p, 0, (ncl + 1) * 4, c->stream));
+    if (num_e) launch(c, k_sym_tcount, dim3(grid_e), dim3(256), 0, num_e, ejcl.as<const uint32_t>(), tcnt.as<uint32_t>());
+    if (int rc = excl_scan(c, tcnt.as<uint32_t>(), tstart.as<uint64_t>(), ncl + 1)) return rc;
+    SFCNL_CUDA_TRY(cudaMemsetAsync(tcnt.p, 0, (ncl + 1) * 4, c->stream));
+    if (num_e)
+        launch(c, k_sym_tfill, dim3(grid_e), dim3(256), 0, num_e, ejcl.as<const uint32_t>(), tstart.as<const uint64_t>(),
+               tcnt.as<uint32_t>(), tlist.as<uint32_t>());
+    launch(c, k_sym_tsort, dim3(unsigned(std::min<uint64_t>((ncl + 255) / 256, uint64_t(c->num_sms) * 16))), dim3(256), 0,
+           ncl, tstart.as<const uint64_t>(), tlist.as<uint32_t>());
+    launch(c, k_sym_final<K>, dim3(grid_sc), dim3(kExactThreads), 0, A, jacc.as<const double>(), jcnt.as<const uint32_t>(),
+           esc.as<const uint32_t>(), tstart.as<const uint64_t>(), tlist.as<const uint32_t>());
+    return 0;
 }
 
 }  // namespace
@@ -490,11 +535,22 @@ int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p) {
     A.cnt = c->ncount.as<uint32_t>() - p0;
     A.err = c->derr.as<DevError>();
     stage_begin(c, kPass);
-    switch (p.kernel) {
-        case 0: launch_pass<0>(c, A, fast); break;
-        case 1: launch_pass<1>(c, A, fast); break;
-        case 2: launch_pass<2>(c, A, fast); break;
-        default: launch_pass<3>(c, A, fast); break;
+    if (symmetric) {
+        int rc = 0;
+        switch (p.kernel) {
+            case 0: rc = launch_sym<0>(c, A); break;
+            case 1: rc = launch_sym<1>(c, A); break;
+            case 2: rc = launch_sym<2>(c, A); break;
+            default: rc = launch_sym<3>(c, A); break;
+        }
+        if (rc) return rc;
+    } else {
+        switch (p.kernel) {
+            case 0: launch_pass<0>(c, A, fast); break;
+            case 1: launch_pass<1>(c, A, fast); break;
+            case 2: launch_pass<2>(c, A, fast); break;
+            default: launch_pass<3>(c, A, fast); break;
+        }
     }
     SFCNL_CUDA_TRY(cudaGetLastError());
     stage_end(c, kPass);
