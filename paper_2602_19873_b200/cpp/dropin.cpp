@@ -3,12 +3,15 @@
 // libsfcnl.a for callers of the build-and-query path: same declarations, same
 // results, GPU-resident hot path. Host-only utilities (codec, store I/O,
 // generators, single-key helpers) are plain C++ here.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <memory>
 #include <mutex>
 
+#include "sfcnl/baselines.hpp"
+#include "sfcnl/bench.hpp"
 #include "sfcnl/builtin_kernels.hpp"
 #include "sfcnl/generators.hpp"
 #include "sfcnl/hilbert.hpp"
@@ -278,6 +281,91 @@ void gpu::run_pass(const ParticleSet& ps, const SimulationBox& box, const Neighb
     for (int o = 0; o < no; ++o) outs[o] = outputs[o].data();
     const sfcnl_pass_params pp{req.kind, req.precision, req.query_scale, req.epsilon, req.sigma, req.coulomb_k};
     D.check(sfcnl_cu_reduce(D.ctx, &pp, outs, neighbor_count.data()));
+}
+
+// ------------------------------------------------------------------ full Verlet list
+FullVerletList build_full_list(const ParticleSet& ps, const SimulationBox& box, double build_scale, ListMode mode,
+                               FullListMethod /*method*/, std::size_t /*cap*/) {
+    if (mode != ListMode::gather) throw InputError("build_full_list: only gather lists are built on the GPU");
+    if (!(build_scale >= 0)) throw InputError("build_full_list: build_scale must be >= 0");
+    check_lengths(ps);
+    Device& D = device();
+    std::lock_guard<std::mutex> lock(D.mu);
+    const std::size_t n = ps.size();
+    upload(D, ps, box, false, false);
+    D.check(sfcnl_cu_sort_by_sfc(D.ctx, kDefaultSfcBits));
+    D.check(sfcnl_cu_apply_order(D.ctx));
+    std::uint64_t nn = 0, nsc = 0, nb = 0, pairs = 0;
+    D.check(sfcnl_cu_build_octree(D.ctx, 64, &nn));
+    sfcnl_build_params p{8, 8, 32, 0, 1, build_scale};
+    D.check(sfcnl_cu_build_store(D.ctx, &p, &nsc, &nb));
+    D.check(sfcnl_cu_build_full_list(D.ctx, build_scale, &pairs));
+    FullVerletList sl;
+    sl.mode = ListMode::gather;
+    sl.build_scale = build_scale;
+    sl.offsets.resize(n + 1);
+    sl.neighbors.resize(pairs);
+    D.check(sfcnl_cu_get_full_list(D.ctx, sl.offsets.data(), sl.neighbors.data()));
+    std::vector<std::uint64_t> keys(n);
+    std::vector<std::uint32_t> perm(n);
+    D.check(sfcnl_cu_get_order(D.ctx, keys.data(), perm.data()));
+    bool identity = true;
+    for (std::size_t k = 0; k < n && identity; ++k) identity = perm[k] == k;
+    if (identity) return sl;
+    // sorted-index list -> the caller's numbering: row perm[s] holds perm[neighbors of s], ascending
+    FullVerletList out;
+    out.mode = ListMode::gather;
+    out.build_scale = build_scale;
+    out.offsets.assign(n + 1, 0);
+    for (std::size_t s = 0; s < n; ++s) out.offsets[perm[s] + 1] = sl.offsets[s + 1] - sl.offsets[s];
+    for (std::size_t i = 0; i < n; ++i) out.offsets[i + 1] += out.offsets[i];
+    out.neighbors.resize(pairs);
+    for (std::size_t s = 0; s < n; ++s) {
+        std::uint32_t* row = out.neighbors.data() + out.offsets[perm[s]];
+        const std::uint64_t b = sl.offsets[s], e = sl.offsets[s + 1];
+        for (std::uint64_t k = b; k < e; ++k) row[k - b] = perm[sl.neighbors[k]];
+        std::sort(row, row + (e - b));
+    }
+    return out;
+}
+
+void gpu::run_pass_full(const ParticleSet& ps, const SimulationBox& box, const FullVerletList& list,
+                        const PassRequest& req, std::vector<std::vector<double>>& outputs,
+                        std::vector<std::uint32_t>& neighbor_count) {
+    const std::size_t n = ps.size();
+    if (list.offsets.size() != n + 1) throw InputError("reduce_full: list/particle-set mismatch");
+    if (req.query_scale > list.build_scale) throw InputError("reduce_full: query_scale exceeds the list's build scale");
+    Device& D = device();
+    std::lock_guard<std::mutex> lock(D.mu);
+    check_lengths(ps);
+    upload(D, ps, box, true, false);
+    if (req.kind == 1) D.check(sfcnl_cu_set_sorted_field(D.ctx, "m", ps.field("m").data()));
+    if (req.kind == 3) D.check(sfcnl_cu_set_sorted_field(D.ctx, "q", ps.field("q").data()));
+    const std::uint32_t dummy = 0;
+    D.check(sfcnl_cu_set_full_list(D.ctx, n, list.mode == ListMode::symmetric ? 1 : 0, list.build_scale,
+                                   list.offsets.data(), list.neighbors.empty() ? &dummy : list.neighbors.data(),
+                                   list.neighbors.size()));
+    const int no = req.kind >= 2 ? 4 : 1;
+    outputs.assign(no, std::vector<double>(n));
+    neighbor_count.assign(n, 0);
+    double* outs[4] = {nullptr, nullptr, nullptr, nullptr};
+    for (int o = 0; o < no; ++o) outs[o] = outputs[o].data();
+    const sfcnl_pass_params pp{req.kind, req.precision, req.query_scale, req.epsilon, req.sigma, req.coulomb_k};
+    D.check(sfcnl_cu_reduce_full(D.ctx, &pp, outs, neighbor_count.data()));
+}
+
+double bench::cluster_overhead(const NeighborStore& store, std::uint64_t true_directed_pairs) {
+    if (store.build.mode != ListMode::gather) throw InputError("cluster_overhead: requires a gather-mode store");
+    if (true_directed_pairs == 0) throw InputError("cluster_overhead: no in-range pairs");
+    Device& D = device();
+    std::lock_guard<std::mutex> lock(D.mu);
+    const sfcnl_build_params p = to_params(store.build);
+    const std::uint8_t dummy = 0;
+    D.check(sfcnl_cu_set_store(D.ctx, &p, store.n, store.counts.size(), store.counts.data(), store.offsets.data(),
+                               store.blob.empty() ? &dummy : store.blob.data(), store.blob.size()));
+    std::uint64_t slots = 0;
+    D.check(sfcnl_cu_cluster_slots(D.ctx, &slots));
+    return double(slots) / double(true_directed_pairs);
 }
 
 // ------------------------------------------------------------------ store helpers

@@ -5,7 +5,8 @@ from /root/reference); the binaries travel with the tree.
 
 test_cluster / test_codec exercise host-side API only and run on CPU;
 test_hilbert / test_octree call sort_by_sfc / build_octree / compute_node_aabbs,
-which run on the GPU."""
+which run on the GPU. test_dropin_baselines (tests/cpp, built by `make all`) checks the
+drop-in's full-list / reduce_full / cluster_overhead C++ API on the GPU."""
 import os
 import subprocess
 
@@ -29,6 +30,6 @@ def test_reference_host_suites(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["test_hilbert", "test_octree"])
+@pytest.mark.parametrize("name", ["test_hilbert", "test_octree", "test_dropin_baselines"])
 def test_reference_gpu_suites(name):
     _run(name)
