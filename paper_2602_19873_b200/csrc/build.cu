@@ -117,7 +117,7 @@ __device__ __forceinline__ double d2_guard(double r, double r2, float E) {
 // Exact pair test of one (i, j) in reference arithmetic (neighbor_build.cpp:140-155).
 __device__ __noinline__ bool exact_hit(const BuildArgs& A, double xi, double yi, double zi, double hi,
                                        uint64_t j) {
-    const double rr = dmul(A.scale, hi);
+    const double rr = dmul(A.scale, A.symmetric ? smax(hi, A.h[j]) : hi);
     const double d2 = pair_d2_exact(xi, yi, zi, A.x[j], A.y[j], A.z[j], A.box, nullptr, nullptr, nullptr);
     return d2 <= dmul(rr, rr);
 }
@@ -550,6 +550,41 @@ __global__ void k_validate(uint64_t n, const double* __restrict__ x, const doubl
     if (lane_id() == 0 && local) atomicMax(maxh_bits, local);
 }
 
+// Main warp-build tier over [sc0, sc1), then the medium tier over its overflow list;
+// SCs beyond both are returned in (*ovf_list, *ovf_count) for k_build_global.
+template <class Sm, class SmM>
+int launch_build_warp(sfcnl_cu_ctx* c, const BuildArgs& A, uint64_t sc0, uint64_t sc1, uint64_t num_sc,
+                      unsigned long long* ctl, const uint32_t** ovf_list, unsigned long long* ovf_count) {
+    constexpr int kMinMain = sizeof(Sm) * kBwWarps * 5 <= 227 * 1024 ? 5 : 4;
+    const size_t smem = size_t(kBwWarps) * sizeof(Sm);
+    cudaFuncSetAttribute(k_build_warp<Sm, kMinMain>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream));
+    const unsigned grid = unsigned(std::max<uint64_t>(
+        1, std::min<uint64_t>((num_sc + kBwWarps - 1) / kBwWarps, uint64_t(c->num_sms) * kMinMain)));
+    launch(c, k_build_warp<Sm, kMinMain>, dim3(grid), dim3(kBwWarps * 32), smem, A, sc0, sc1,
+           c->work_ctr.as<unsigned long long>(), (const uint32_t*)nullptr, A.overflow_list, 1);
+    SFCNL_CUDA_TRY(cudaGetLastError());
+    SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
+    SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    *ovf_list = A.overflow_list;
+    *ovf_count = 0;
+    if (ctl[1]) {  // medium tier over the overflow list; what still overflows -> ctl[4]
+        const size_t smem_m = size_t(kBwWarps) * sizeof(SmM);
+        cudaFuncSetAttribute(k_build_warp<SmM, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_m));
+        SFCNL_CUDA_TRY(cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream));
+        const unsigned grid_m = unsigned(std::max<uint64_t>(
+            1, std::min<uint64_t>((ctl[1] + kBwWarps - 1) / kBwWarps, uint64_t(c->num_sms) * 3)));
+        launch(c, k_build_warp<SmM, 3>, dim3(grid_m), dim3(kBwWarps * 32), smem_m, A, uint64_t(0), uint64_t(ctl[1]),
+               c->work_ctr.as<unsigned long long>(), (const uint32_t*)A.overflow_list, A.overflow_list + num_sc, 4);
+        SFCNL_CUDA_TRY(cudaGetLastError());
+        SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
+        SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        *ovf_list = A.overflow_list + num_sc;
+        *ovf_count = ctl[4];
+    }
+    return 0;
+}
+
 }  // namespace
 
 int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, uint64_t sc1, double max_h_in) {
@@ -670,7 +705,7 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
         A.scratch_cap = c->scratch.bytes;
         SFCNL_CUDA_TRY(cudaMemsetAsync(c->build_ctl.p, 0, 5 * 8, c->stream));
         stage_begin(c, kBuild);
-        if (p.ci == 8 && (p.cj == 8 || p.cj == 4) && p.mode == 0) {
+        if (p.ci == 8 && (p.cj == 8 || p.cj == 4)) {
             // warp-per-SC kernel (build_warp.cuh) on the cluster-frame staging copy
             {
                 const bool whole = sc0 == 0 && sc1 == total_sc;
@@ -681,32 +716,11 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
             }
             A.frame = c->frame.as<const float4>();
             A.frame_x = c->frame_x.as<const unsigned>();
-            const size_t smem = size_t(kBwWarps) * sizeof(BwSmem);
-            cudaFuncSetAttribute(k_build_warp<BwSmem, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             SFCNL_CUDA_TRY(c->work_ctr.reserve(8));
-            SFCNL_CUDA_TRY(cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream));
-            const unsigned grid = unsigned(std::max<uint64_t>(
-                1, std::min<uint64_t>((num_sc + kBwWarps - 1) / kBwWarps, uint64_t(c->num_sms) * 5)));
-            launch(c, k_build_warp<BwSmem, 5>, dim3(grid), dim3(kBwWarps * 32), smem, A, sc0, sc1,
-                   c->work_ctr.as<unsigned long long>(), (const uint32_t*)nullptr, A.overflow_list, 1);
-            SFCNL_CUDA_TRY(cudaGetLastError());
-            SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
-            SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
-            if (ctl[1]) {  // medium tier over the overflow list; what still overflows -> ctl[4]
-                const size_t smem_m = size_t(kBwWarps) * sizeof(BwSmemM);
-                cudaFuncSetAttribute(k_build_warp<BwSmemM, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_m));
-                SFCNL_CUDA_TRY(cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream));
-                const unsigned grid_m = unsigned(std::max<uint64_t>(
-                    1, std::min<uint64_t>((ctl[1] + kBwWarps - 1) / kBwWarps, uint64_t(c->num_sms) * 3)));
-                launch(c, k_build_warp<BwSmemM, 3>, dim3(grid_m), dim3(kBwWarps * 32), smem_m, A, uint64_t(0),
-                       uint64_t(ctl[1]), c->work_ctr.as<unsigned long long>(), (const uint32_t*)A.overflow_list,
-                       A.overflow_list + num_sc, 4);
-                SFCNL_CUDA_TRY(cudaGetLastError());
-                SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
-                SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
-                ovf_list = A.overflow_list + num_sc;
-                ovf_count = ctl[4];
-            }
+            const int rc = p.mode == 0 ? launch_build_warp<BwSmem, BwSmemM>(c, A, sc0, sc1, num_sc, ctl, &ovf_list, &ovf_count)
+                                       : launch_build_warp<BwSmemSym, BwSmemMSym>(c, A, sc0, sc1, num_sc, ctl, &ovf_list,
+                                                                                &ovf_count);
+            if (rc) return rc;
         } else {
             const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(num_sc, uint64_t(c->num_sms) * 64)));
             launch(c, k_build_smem, dim3(grid), dim3(kBuildThreads), 0, A, sc0, sc1);

@@ -40,9 +40,18 @@ constexpr uint32_t kLeafCacheCap = 256;  // accepted leaves kept per SC by halo 
 // the small one (5 CTAs x 4 warps per SM); SCs that exceed it (dense lists, wide skins,
 // 8x4 clusters at high neighbour counts) are re-run from the overflow list with the
 // medium one (3 CTAs x 4 warps per SM); only SCs beyond that go to k_build_global.
-template <uint32_t F, uint32_t E, uint32_t B>
+// symmetric mode: per-j guard-band thresholds of the staged chunk ([p][candidate] pairs)
+template <bool SYM>
+struct BwSymJ {
+    float2 slo[4][32], shi[4][32];
+};
+template <>
+struct BwSymJ<false> {};
+
+template <uint32_t F, uint32_t E, uint32_t B, bool SYM = false>
 struct BwSmemT {
     static constexpr uint32_t kF = F, kE = E, kB = B;
+    static constexpr bool kSym = SYM;
     union {
         struct {
             uint32_t fa[F], fb[F];  // traversal frontier, then per-leaf candidate prefix
@@ -59,9 +68,12 @@ struct BwSmemT {
     uint8_t items[256];
     uint32_t eidx[E];
     uint8_t emsk[E];
+    BwSymJ<SYM> sy;
 };
 using BwSmem = BwSmemT<kBwF, kBwE, kBwBytes>;
 using BwSmemM = BwSmemT<1024, 1024, 8192>;
+using BwSmemSym = BwSmemT<kBwF, kBwE, kBwBytes, true>;
+using BwSmemMSym = BwSmemT<1024, 1024, 8192, true>;
 
 // Guard band on a squared distance near r^2 when every coordinate difference carries
 // an absolute error <= ecoord + 2^-24 r (see pass.cu); factor 4 margin.
@@ -102,7 +114,12 @@ __device__ __forceinline__ uint32_t warp_bfs(const BuildArgs& A, const Geo& scg,
                     const Node nd = A.nodes[e];
                     if (nd.pend > nd.pbegin) {
                         const Geo ng = A.ngeo[e];
-                        if (!(aabb_dist_sq(scg, ng, A.box) > r2)) {
+                        double rr2 = r2;
+                        if (A.symmetric) {  // scale * max(sc_maxh, node_maxh) (neighbor_build.cpp:122-125)
+                            const double rr = dmul(A.scale, smax(scg.maxh, ng.maxh));
+                            rr2 = dmul(rr, rr);
+                        }
+                        if (!(aabb_dist_sq(scg, ng, A.box) > rr2)) {
                             fc = nd.first_child;
                             emit = fc < 0 ? 1 : 8;
                         }
@@ -160,6 +177,7 @@ __device__ __forceinline__ void sc_box(const BuildArgs& A, uint64_t icl_base, ui
 
 template <class Sm>
 __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
+    constexpr bool SYM = Sm::kSym;
     const unsigned lane = lane_id();
 #ifdef SFCNL_PHASE_PROF
     long long _tprev = clock64();
@@ -225,7 +243,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
     // ---- 2. ordered-frontier BFS (exact fp64 node test)
     uint32_t* fa;
     uint32_t nA = ~0u;
-    if (A.leaf_cache) {  // halo marking of this range already traversed (same BFS, same order)
+    if (!SYM && A.leaf_cache) {  // halo marking of this range already traversed (same BFS, same order)
         const uint32_t cnt = A.leaf_count[sc - A.leaf_sc0];
         if (cnt != ~0u) {
             const uint32_t* src = A.leaf_cache + (sc - A.leaf_sc0) * kLeafCacheCap;
@@ -270,6 +288,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
     // ---- 4. masks, chunk by chunk; 5a. ordered compaction of mask != 0
     uint32_t nE = 0;
     float Ej_run = -1.f;               // running max of the staged |coordinates| (guard bands)
+    double ecoord_cur = 0.0;           // coordinate error bound of the current thresholds
     double pr_me = 0.0, pr2_me = 0.0;  // prefilter radius of i-cluster `lane` (neighbor_build.cpp:136)
     if (lane < nicl) pr_me = dmul(A.scale, A.igeo[icl_base + lane].maxh), pr2_me = dmul(pr_me, pr_me);
     const uint32_t il = lane >> 2, jq = lane & 3;
@@ -296,8 +315,9 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
                 const Geo jg = A.jgeo[cand];
                 const uint64_t jb = uint64_t(cand) * cj, je = tmin<uint64_t>(jb + cj, A.n);
                 for (uint32_t b = 0; b < nicl; ++b) {
+                    if (SYM && (icl_base + b) * 8 > jb) continue;  // half-list rule (neighbor_build.cpp:133)
                     const Geo ig = A.igeo[icl_base + b];
-                    const double pre_r = dmul(A.scale, ig.maxh);
+                    const double pre_r = dmul(A.scale, SYM ? smax(ig.maxh, jg.maxh) : ig.maxh);
                     if (aabb_dist_sq(ig, jg, A.box) > dmul(pre_r, pre_r)) continue;
                     const uint64_t ib = (icl_base + b) * 8, ie = tmin<uint64_t>(ib + 8, A.n);
                     bool hit = false;
@@ -307,7 +327,8 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
                         for (uint64_t j = jb; j < je; ++j) {
                             if (i == j) continue;
                             const double d2 = pair_d2_exact(xi, yi, zi, A.x[j], A.y[j], A.z[j], A.box, nullptr, nullptr, nullptr);
-                            if (d2 <= dmul(rr, rr)) {
+                            const double rs = SYM ? dmul(A.scale, smax(A.h[i], A.h[j])) : rr;
+                            if (d2 <= dmul(rs, rs)) {
                                 hit = true;
                                 break;
                             }
@@ -374,6 +395,33 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
                     S.ia[(k & 7) * 8 + (k >> 3)].w = lo, S.ihi[(k & 7) * 8 + (k >> 3)] = hi;
                 }
                 if (lane < nicl) S.pthr[lane] = __double2float_ru(pr2_me + guard_band(pr_me, pr2_me, ecoord));
+                ecoord_cur = ecoord;
+            }
+            // symmetric: the pair radius is scale * max(h_i, h_j) = max(r_i, r_j) and the
+            // prefilter radius scale * max(imaxh, jmaxh); lo/hi/thresholds are monotone in r,
+            // so per-pair thresholds are the max of the per-particle ones
+            float pthr_c = 0.f;
+            if constexpr (SYM) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t e = uint32_t(u) * 4 + (lane >> 3), jj = lane & 7;
+                    const uint32_t ce = __shfl_sync(0xffffffffu, cand, e);
+                    const uint64_t j = uint64_t(ce) * cj + jj;
+                    float lo = -1.f, hi = -1.f;
+                    if (e < n && jj < cj && j < A.n) {
+                        const double r = dmul(A.scale, A.h[j]), rr2 = dmul(r, r), g = guard_band(r, rr2, ecoord_cur);
+                        lo = __double2float_rd(rr2 - g);
+                        hi = __double2float_ru(rr2 + g);
+                    }
+                    if (e < n) {
+                        reinterpret_cast<float*>(&S.sy.slo[jj >> 1][e])[jj & 1] = lo;
+                        reinterpret_cast<float*>(&S.sy.shi[jj >> 1][e])[jj & 1] = hi;
+                    }
+                }
+                if (valid) {
+                    const double pr = dmul(A.scale, A.jgeo[cand].maxh), pr2 = dmul(pr, pr);
+                    pthr_c = __double2float_ru(pr2 + guard_band(pr, pr2, ecoord_cur));
+                }
             }
             if (lane < 32) S.cmask[lane] = 0;
             __syncwarp();
@@ -397,13 +445,16 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
                     }
                 }
                 for (uint32_t b = 0; b < nicl; ++b) {
+                    // half-list rule: the pair lives on the side whose i-cluster starts first (:133)
+                    if (SYM && (icl_base + b) * 8 > uint64_t(cand) * cj) continue;
                     float s2 = 0.f;
 #pragma unroll
                     for (int d = 0; d < 3; ++d) {
                         const float g = fmaxf(fmaxf(S.iab[b][d], jlo[d]) - fminf(S.iab[b][3 + d], jhi[d]), 0.f);
                         s2 = fmaf(g, g, s2);
                     }
-                    if (!(s2 > S.pthr[b])) pm |= 1u << b;
+                    const float thr = SYM ? fmaxf(S.pthr[b], pthr_c) : S.pthr[b];
+                    if (!(s2 > thr)) pm |= 1u << b;
                 }
             }
             // items (b << 5 | c), candidate-major (one warp scan places each lane's set bits);
@@ -432,10 +483,12 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
                 const bool self = iv && j0 >= -7 && j0 < kSC;
                 ulonglong2 Ja[4];
                 f2 Jz[4];
+                float2 Jlo[4], Jhi[4];
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
                     Ja[p] = reinterpret_cast<const ulonglong2&>(S.sa[p][c]);
                     Jz[p] = reinterpret_cast<const f2&>(S.sz[p][c]);
+                    if constexpr (SYM) Jlo[p] = S.sy.slo[p][c], Jhi[p] = S.sy.shi[p][c];
                 }
                 bool hit = false;
                 uint32_t band_rows = 0;
@@ -446,7 +499,8 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
                         const float4 I = S.ia[ii * 8 + b];
                         const f2 xi2 = f2p(I.x, I.x), yi2 = f2p(I.y, I.y), zi2 = f2p(I.z, I.z);
                         const int iself = kSelf && self ? int(b * 8 + ii) - j0 : -1;
-                        float mn = 3.0e38f;
+                        float mn = 3.0e38f, mh = 3.0e38f;
+                        const float hii = S.ihi[ii * 8 + b];
 #pragma unroll
                         for (int p = 0; p < 4; ++p) {
                             const f2 dx = f2sub(xi2, Ja[p].x), dy = f2sub(yi2, Ja[p].y), dz = f2sub(zi2, Jz[p]);
@@ -456,10 +510,20 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
                                 if (iself == 2 * p) d2a = 3.0e38f;
                                 if (iself == 2 * p + 1) d2b = 3.0e38f;
                             }
-                            mn = fminf(mn, fminf(d2a, d2b));
+                            if (SYM) {  // margins to the per-pair thresholds max(lo_i, lo_j), max(hi_i, hi_j)
+                                mn = fminf(mn, fminf(d2a - fmaxf(I.w, Jlo[p].x), d2b - fmaxf(I.w, Jlo[p].y)));
+                                mh = fminf(mh, fminf(d2a - fmaxf(hii, Jhi[p].x), d2b - fmaxf(hii, Jhi[p].y)));
+                            } else {
+                                mn = fminf(mn, fminf(d2a, d2b));
+                            }
                         }
-                        if (mn < I.w) hit = true;
-                        else if (mn <= S.ihi[ii * 8 + b]) band_rows |= 1u << ii;
+                        if (SYM) {
+                            if (mn < 0.f) hit = true;
+                            else if (mh <= 0.f) band_rows |= 1u << ii;
+                        } else {
+                            if (mn < I.w) hit = true;
+                            else if (mn <= hii) band_rows |= 1u << ii;
+                        }
                     }
                 };
                 if (__any_sync(0xffffffffu, self)) rows(BoolC<true>());
@@ -482,7 +546,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
                     }
                     if (ex) {
                         const Geo ig = A.igeo[icl_base + b];
-                        const double pr = dmul(A.scale, ig.maxh);
+                        const double pr = dmul(A.scale, SYM ? smax(ig.maxh, A.jgeo[cc].maxh) : ig.maxh);
                         hit = !(aabb_dist_sq(ig, A.jgeo[cc], A.box) > dmul(pr, pr));
                     }
                 }

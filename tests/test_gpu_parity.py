@@ -148,6 +148,10 @@ def _pairs_from_store(st, n):
     ("evrard", 40000, (8, 8, 32, 0, 1, 1.0)),
     ("uniform", 20011, (8, 4, 64, 0, 1, 1.0)),
     ("uniform", 12345, (8, 8, 32, 1, 1, 1.0)),
+    # symmetric on the warp build: jittered h (per-pair radii), Evrard, 8x4 with a skin
+    ("uniform", 60000, (8, 8, 32, 1, 1, 1.0)),
+    ("evrard", 40000, (8, 8, 32, 1, 1, 1.0)),
+    ("uniform", 30011, (8, 4, 64, 1, 1, 1.1)),
     ("uniform", 30000, (8, 8, 32, 0, 0, 1.15)),
     ("uniform", 3001, (1, 1, 32, 0, 1, 1.0)),
 ])
