@@ -139,7 +139,7 @@ struct sfcnl_cu_ctx {
     sfcnl_cu::DBuf full_cnt, full_off, full_nbr;
     // symmetric pass (pass_sym.cuh): entry base, j-side accumulators/counts, entry
     // j-cluster/SC, transposed entry lists per j-cluster
-    sfcnl_cu::DBuf sym[8];
+    sfcnl_cu::DBuf sym[9];  // [8]: deferred special-slot queues of the symmetric fast pass
 
     // errors
     sfcnl_cu::DBuf derr;  // DevError

@@ -29,6 +29,7 @@
 //   lane and are combined in fp64.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "ctx.hpp"
@@ -36,6 +37,12 @@
 
 namespace sfcnl_cu {
 namespace {
+
+inline double __longlong_as_double_host(unsigned long long b) {
+    double d;
+    std::memcpy(&d, &b, 8);
+    return d;
+}
 
 struct PassArgs {
     uint64_t n;
@@ -54,6 +61,7 @@ struct PassArgs {
     const double* m;
     const double* q;
     double qs, eps, sigma, ck;
+    double maxh;      // max h over the particles (symmetric fast pass: image-safety bound)
     float lj_close2;  // LJ pairs with d2 < lj_close2 * sigma^2 take the fp64 path
     float sig2f;      // float(sigma^2)
     const float4* frame;     // cluster-frame staging copy (frame.cu), density/count
@@ -346,6 +354,7 @@ __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& 
 #include "pass_item.cuh"
 #include "pass_full.cuh"
 #include "pass_sym.cuh"
+#include "pass_symf.cuh"
 
 // Device-side block-offset index of an uploaded store: warp per SC walks the codec
 // block headers (first kBtab blocks) and records where each block starts.
@@ -413,47 +422,109 @@ void launch_pass(sfcnl_cu_ctx* c, const PassArgs& A, bool fast) {
     }
 }
 
-// Symmetric stores: the three-step deterministic pass of pass_sym.cuh.
+// Entries per j-cluster in ascending entry order (count, scan, fill, per-cluster sort).
+int sym_transpose(sfcnl_cu_ctx* c, uint64_t num_e, uint64_t ncl, const uint32_t* ejcl) {
+    auto &tcnt = c->sym[5], &tstart = c->sym[6], &tlist = c->sym[7];
+    SFCNL_CUDA_TRY(tcnt.reserve((ncl + 1) * 4));
+    SFCNL_CUDA_TRY(tstart.reserve((ncl + 1) * 8));
+    SFCNL_CUDA_TRY(tlist.reserve(std::max<uint64_t>(num_e, 1) * 4));
+    const unsigned grid_e = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((num_e + 255) / 256, uint64_t(c->num_sms) * 16)));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(tcnt.p, 0, (ncl + 1) * 4, c->stream));
+    if (num_e) launch(c, k_sym_tcount, dim3(grid_e), dim3(256), 0, num_e, ejcl, tcnt.as<uint32_t>());
+    if (int rc = excl_scan(c, tcnt.as<uint32_t>(), tstart.as<uint64_t>(), ncl + 1)) return rc;
+    SFCNL_CUDA_TRY(cudaMemsetAsync(tcnt.p, 0, (ncl + 1) * 4, c->stream));
+    if (num_e)
+        launch(c, k_sym_tfill, dim3(grid_e), dim3(256), 0, num_e, ejcl, tstart.as<const uint64_t>(), tcnt.as<uint32_t>(),
+               tlist.as<uint32_t>());
+    launch(c, k_sym_tsort, dim3(unsigned(std::max<uint64_t>(1, std::min<uint64_t>((ncl + 255) / 256, uint64_t(c->num_sms) * 16)))),
+           dim3(256), 0, ncl, tstart.as<const uint64_t>(), tlist.as<uint32_t>());
+    return 0;
+}
+
+// Global entry base per SC (exclusive scan of the counts) and the total entry count.
+int sym_entry_base(sfcnl_cu_ctx* c, const PassArgs& A, uint64_t num_sc, uint64_t* num_e) {
+    auto& ebase = c->sym[0];
+    SFCNL_CUDA_TRY(ebase.reserve((num_sc + 1) * 8));
+    if (int rc = excl_scan(c, A.counts + A.sc_begin, ebase.as<uint64_t>(), num_sc)) return rc;
+    uint64_t last = 0;
+    uint32_t lastc = 0;
+    SFCNL_CUDA_TRY(cudaMemcpyAsync(&last, ebase.as<uint64_t>() + num_sc - 1, 8, cudaMemcpyDeviceToHost, c->stream));
+    SFCNL_CUDA_TRY(cudaMemcpyAsync(&lastc, A.counts + A.num_sc - 1, 4, cudaMemcpyDeviceToHost, c->stream));
+    SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    *num_e = last + lastc;
+    return 0;
+}
+
+// Symmetric stores, precision 0: the three-step deterministic pass of pass_sym.cuh.
 template <int K>
 int launch_sym(sfcnl_cu_ctx* c, const PassArgs& A) {
     constexpr int NO = nout<K>();
     const uint64_t num_sc = A.num_sc - A.sc_begin;
     if (num_sc == 0) return 0;
-    auto& ebase = c->sym[0];
-    SFCNL_CUDA_TRY(ebase.reserve((num_sc + 1) * 8));
-    if (int rc = excl_scan(c, A.counts + A.sc_begin, ebase.as<uint64_t>(), num_sc)) return rc;
-    uint64_t last[2] = {0, 0};
-    uint32_t lastc = 0;
-    SFCNL_CUDA_TRY(cudaMemcpyAsync(last, ebase.as<uint64_t>() + num_sc - 1, 8, cudaMemcpyDeviceToHost, c->stream));
-    SFCNL_CUDA_TRY(cudaMemcpyAsync(&lastc, A.counts + A.num_sc - 1, 4, cudaMemcpyDeviceToHost, c->stream));
-    SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
-    const uint64_t num_e = last[0] + lastc;
+    uint64_t num_e = 0;
+    if (int rc = sym_entry_base(c, A, num_sc, &num_e)) return rc;
     const uint64_t ncl = (A.n + A.cj - 1) / A.cj;
-    auto &jacc = c->sym[1], &jcnt = c->sym[2], &ejcl = c->sym[3], &esc = c->sym[4];
-    auto &tcnt = c->sym[5], &tstart = c->sym[6], &tlist = c->sym[7];
+    auto &ebase = c->sym[0], &jacc = c->sym[1], &jcnt = c->sym[2], &ejcl = c->sym[3], &esc = c->sym[4];
     SFCNL_CUDA_TRY(jacc.reserve(std::max<uint64_t>(num_e, 1) * NO * A.cj * 8));
     SFCNL_CUDA_TRY(jcnt.reserve(std::max<uint64_t>(num_e, 1) * A.cj * 4));
     SFCNL_CUDA_TRY(ejcl.reserve(std::max<uint64_t>(num_e, 1) * 4));
     SFCNL_CUDA_TRY(esc.reserve(std::max<uint64_t>(num_e, 1) * 4));
-    SFCNL_CUDA_TRY(tcnt.reserve((ncl + 1) * 4));
-    SFCNL_CUDA_TRY(tstart.reserve((ncl + 1) * 8));
-    SFCNL_CUDA_TRY(tlist.reserve(std::max<uint64_t>(num_e, 1) * 4));
     const unsigned grid_sc = unsigned(std::min<uint64_t>(num_sc, uint64_t(c->num_sms) * 32));
     // ebase is indexed by global SC: A.sc_begin == 0 for symmetric stores (whole range)
     launch(c, k_sym_jside<K>, dim3(grid_sc), dim3(kExactThreads), 0, A, ebase.as<const uint64_t>(), jacc.as<double>(),
            jcnt.as<uint32_t>(), ejcl.as<uint32_t>(), esc.as<uint32_t>());
-    const unsigned grid_e = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((num_e + 255) / 256, uint64_t(c->num_sms) * 16)));
-    SFCNL_CUDA_TRY(cudaMemsetAsync(tcnt.p, 0, (ncl + 1) * 4, c->stream));
-    if (num_e) launch(c, k_sym_tcount, dim3(grid_e), dim3(256), 0, num_e, ejcl.as<const uint32_t>(), tcnt.as<uint32_t>());
-    if (int rc = excl_scan(c, tcnt.as<uint32_t>(), tstart.as<uint64_t>(), ncl + 1)) return rc;
-    SFCNL_CUDA_TRY(cudaMemsetAsync(tcnt.p, 0, (ncl + 1) * 4, c->stream));
-    if (num_e)
-        launch(c, k_sym_tfill, dim3(grid_e), dim3(256), 0, num_e, ejcl.as<const uint32_t>(), tstart.as<const uint64_t>(),
-               tcnt.as<uint32_t>(), tlist.as<uint32_t>());
-    launch(c, k_sym_tsort, dim3(unsigned(std::min<uint64_t>((ncl + 255) / 256, uint64_t(c->num_sms) * 16))), dim3(256), 0,
-           ncl, tstart.as<const uint64_t>(), tlist.as<uint32_t>());
+    if (int rc = sym_transpose(c, num_e, ncl, ejcl.as<const uint32_t>())) return rc;
     launch(c, k_sym_final<K>, dim3(grid_sc), dim3(kExactThreads), 0, A, jacc.as<const double>(), jcnt.as<const uint32_t>(),
-           esc.as<const uint32_t>(), tstart.as<const uint64_t>(), tlist.as<const uint32_t>());
+           esc.as<const uint32_t>(), c->sym[6].as<const uint64_t>(), c->sym[7].as<const uint32_t>());
+    return 0;
+}
+
+__global__ void k_max_h(uint64_t n, const double* __restrict__ h, unsigned long long* out) {
+    double m = 0.0;
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n; p += uint64_t(gridDim.x) * blockDim.x)
+        m = smax(m, h[p]);
+    for (int s = 16; s > 0; s >>= 1) m = smax(m, __shfl_xor_sync(0xffffffffu, m, s));
+    if (lane_id() == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));  // h > 0: bits order like values
+}
+
+// Symmetric stores, precision 1: one evaluation per stored pair (pass_symf.cuh).
+template <int K>
+int launch_sym_fast(sfcnl_cu_ctx* c, PassArgs A) {
+    constexpr int NO = nout<K>();
+    const uint64_t num_sc = A.num_sc - A.sc_begin;
+    if (num_sc == 0) return 0;
+    uint64_t num_e = 0;
+    if (int rc = sym_entry_base(c, A, num_sc, &num_e)) return rc;
+    const uint64_t ncl = (A.n + A.cj - 1) / A.cj;
+    {
+        SFCNL_CUDA_TRY(c->small_host_dev.reserve(16));
+        SFCNL_CUDA_TRY(cudaMemsetAsync(c->small_host_dev.p, 0, 8, c->stream));
+        launch(c, k_max_h, dim3(unsigned(std::min<uint64_t>((A.n + 255) / 256, uint64_t(c->num_sms) * 8))), dim3(256), 0, A.n,
+               A.h, c->small_host_dev.as<unsigned long long>());
+        unsigned long long bits = 0;
+        SFCNL_CUDA_TRY(cudaMemcpyAsync(&bits, c->small_host_dev.p, 8, cudaMemcpyDeviceToHost, c->stream));
+        SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        A.maxh = __longlong_as_double_host(bits);
+    }
+    auto &ebase = c->sym[0], &jacc = c->sym[1], &jcnt = c->sym[2], &ejcl = c->sym[3];
+    SFCNL_CUDA_TRY(jacc.reserve(std::max<uint64_t>(num_e, 1) * NO * A.cj * 4));
+    SFCNL_CUDA_TRY(jcnt.reserve(std::max<uint64_t>(num_e, 1) * A.cj * 4));
+    SFCNL_CUDA_TRY(ejcl.reserve(std::max<uint64_t>(num_e, 1) * 4));
+    const size_t smem = ps_smem<K>();
+    auto kern = A.cj == 8 ? k_pass_symw<K, 8> : k_pass_symw<K, 4>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPwWarps * 32, smem);
+    const unsigned grid = unsigned(std::max<uint64_t>(
+        1, std::min<uint64_t>((num_sc + kPwWarps - 1) / kPwWarps, uint64_t(c->num_sms) * std::max(per_sm, 1))));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream));
+    SFCNL_CUDA_TRY(c->sym[8].reserve(uint64_t(grid) * kPwWarps * kSqCap * 4));
+    launch(c, kern, dim3(grid), dim3(kPwWarps * 32), smem, A, c->work_ctr.as<unsigned long long>(),
+           ebase.as<const uint64_t>(), jacc.as<float>(), jcnt.as<uint32_t>(), ejcl.as<uint32_t>(), c->sym[8].as<uint32_t>());
+    if (int rc = sym_transpose(c, num_e, ncl, ejcl.as<const uint32_t>())) return rc;
+    launch(c, k_sym_fgather<K>, dim3(unsigned(std::min<uint64_t>((A.n + 255) / 256, uint64_t(c->num_sms) * 16))), dim3(256), 0,
+           A.n, uint32_t(A.cj), jacc.as<const float>(), jcnt.as<const uint32_t>(), c->sym[6].as<const uint64_t>(),
+           c->sym[7].as<const uint32_t>(), A.out[0], A.out[1], A.out[2], A.out[3], A.cnt);
     return 0;
 }
 
@@ -536,12 +607,14 @@ int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p) {
     A.err = c->derr.as<DevError>();
     stage_begin(c, kPass);
     if (symmetric) {
+        const bool sym_fast = p.precision == 1 && c->sp.ci == 8 && (c->sp.cj == 8 || c->sp.cj == 4) &&
+                              !getenv("SFCNL_SYM_EXACT");
         int rc = 0;
         switch (p.kernel) {
-            case 0: rc = launch_sym<0>(c, A); break;
-            case 1: rc = launch_sym<1>(c, A); break;
-            case 2: rc = launch_sym<2>(c, A); break;
-            default: rc = launch_sym<3>(c, A); break;
+            case 0: rc = sym_fast ? launch_sym_fast<0>(c, A) : launch_sym<0>(c, A); break;
+            case 1: rc = sym_fast ? launch_sym_fast<1>(c, A) : launch_sym<1>(c, A); break;
+            case 2: rc = sym_fast ? launch_sym_fast<2>(c, A) : launch_sym<2>(c, A); break;
+            default: rc = sym_fast ? launch_sym_fast<3>(c, A) : launch_sym<3>(c, A); break;
         }
         if (rc) return rc;
     } else {
