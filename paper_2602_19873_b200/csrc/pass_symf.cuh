@@ -20,12 +20,14 @@
 // evaluated (i == j never; mirror_stored, reduce.hpp:16-21, holds for every i > j
 // there). Unsafe SCs evaluate every slot through the reference fp64 predicate.
 
+constexpr int kPsChunk = 16;  // entries staged at a time (smaller than k_pass_warp's: more per-warp state)
+
 template <int K>
 struct PsSmem {
     static constexpr bool LJ = (K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB);
     static constexpr int NO = nout<K>();
-    float sj[kPwChunk * 4 * (LJ ? 12 : 8)];  // as PwSmem
-    float2 jlo[kPwChunk * 4], jhi[kPwChunk * 4];  // per (entry, quarter): thresholds of slots {a, b}
+    float sj[kPsChunk * 4 * (LJ ? 12 : 8)];  // as PwSmem
+    float2 jlo[kPsChunk * 4], jhi[kPsChunk * 4];  // per (entry, quarter): thresholds of slots {a, b}
     uint32_t idx[64];
     float ix[64], iy[64], iz[64];
     float ilx[LJ ? 64 : 1], ily[LJ ? 64 : 1], ilz[LJ ? 64 : 1];
@@ -34,11 +36,13 @@ struct PsSmem {
     double acc[64][NO];
     uint32_t cnt[64];
     float ilo[64], ihi[64];
-    float jside[kPwChunk][8][NO];  // the chunk's j-side sums (folded scale) per (entry, j)
-    uint32_t jsc[kPwChunk][8];
+    float jside[kPsChunk][8][NO];  // the chunk's j-side sums (folded scale) per (entry, j)
+    uint32_t jsc[kPsChunk][8];
+    float ip[64][4][NO];  // the chunk's i-side partial sums per (i, j-quarter lane): lane-private
+    float ipc[64][4];
 };
 
-constexpr uint32_t kSqCap = kPwChunk * 8 * 64;  // deferred special slots per warp and chunk (worst case)
+constexpr uint32_t kSqCap = kPsChunk * 8 * 64;  // deferred special slots per warp and chunk (worst case)
 
 template <int K>
 constexpr size_t ps_smem() {
@@ -147,8 +151,14 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
             if (LJ) S.ilx[k] = float(qx - double(fx)), S.ily[k] = float(qy - double(fy)), S.ilz[k] = float(qz - double(fz));
             if (K == SFCNL_KERNEL_DENSITY) S.iscale[k] = float(8.0 / (kPi * hk * hk * hk)), S.iinvh[k] = float(1.0 / hk);
 #pragma unroll
-            for (int o = 0; o < NO; ++o) S.acc[k][o] = 0.0;
+            for (int o = 0; o < NO; ++o) {
+                S.acc[k][o] = 0.0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) S.ip[k][q][o] = 0.f;
+            }
             S.cnt[k] = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) S.ipc[k][q] = 0.f;
         }
         eax = warp_fmax(eax), eay = warp_fmax(eay), eaz = warp_fmax(eaz);
         // the j side's radius can exceed the i side's: use the global max h for the image test
@@ -188,8 +198,8 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
                 }
             }
             __syncwarp();
-            for (uint32_t h0 = 0; h0 < len; h0 += kPwChunk) {
-                const uint32_t n = tmin<uint32_t>(kPwChunk, len - h0);
+            for (uint32_t h0 = 0; h0 < len; h0 += kPsChunk) {
+                const uint32_t n = tmin<uint32_t>(kPsChunk, len - h0);
                 const bool have = lane < n;
                 const uint32_t my_idx = have ? S.idx[h0 + lane] : 0u;
                 const uint32_t my_msk = have ? uint32_t(rec[bb + h0 + lane]) : 0u;
@@ -197,7 +207,7 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
                 float emax = 0.f;
                 if (!unsafe) {
 #pragma unroll
-                    for (int k0 = 0; k0 < 8; k0 += 4) {
+                    for (int k0 = 0; k0 < kPsChunk / 4; k0 += 4) {
                         double vx[4], vy[4], vz[4], vm[4];
                         bool val[4];
 #pragma unroll
@@ -255,7 +265,7 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
                 }
                 if (!unsafe) {  // per-j thresholds with the same bound (monotone in r: max with the i side's)
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
+                    for (int u = 0; u < kPsChunk / 4; ++u) {
                         const uint32_t e = uint32_t(u) * 4 + (lane >> 3), jj = lane & 7;
                         const uint32_t ie = __shfl_sync(0xffffffffu, my_idx, e);
                         const uint64_t j = uint64_t(ie) * CJ + jj;
@@ -413,19 +423,12 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
                             for (int o = 0; o < NO; ++o) {
                                 float a, c;
                                 f2u(vals[o], a, c);
-                                float v = a + c;
-                                v += __shfl_xor_sync(0xffffffffu, v, 1);
-                                v += __shfl_xor_sync(0xffffffffu, v, 2);
-                                if (jq == 0 && act) S.acc[li][o] += double(v) * double(fscale[o]);
+                                if (act) S.ip[li][jq][o] += a + c;
                                 // j side: signed (odd outputs negated), over the bits of the entry
                                 jv[o] = (NO == 4 && o < 3) ? f2sub(jv[o], vals[o]) : f2add(jv[o], vals[o]);
                             }
-                            float c = cnt_a + cnt_b;
-                            c += __shfl_xor_sync(0xffffffffu, c, 1);
-                            c += __shfl_xor_sync(0xffffffffu, c, 2);
-                            if (jq == 0 && act) S.cnt[li] += uint32_t(c);
+                            if (act) S.ipc[li][jq] += cnt_a + cnt_b;
                             jc0 += cnt_a, jc1 += cnt_b;
-                            __syncwarp();
                         }
                     }
                     // j side of the entry: reduce over the eight i lanes, write [entry][j][o]
@@ -493,6 +496,20 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
                     atomicAdd(&S.jsc[e][jj], 1u);
                 }
                 qn = 0;
+                __syncwarp();  // special-slot atomics done
+                // the chunk's i-side partials into the per-i fp64 sums (j-quarter order)
+#pragma unroll
+                for (int s = 0; s < 2; ++s) {
+                    const uint32_t k = lane + 32u * s;
+#pragma unroll
+                    for (int o = 0; o < NO; ++o) {
+                        const float v = (S.ip[k][0][o] + S.ip[k][1][o]) + (S.ip[k][2][o] + S.ip[k][3][o]);
+                        S.ip[k][0][o] = S.ip[k][1][o] = S.ip[k][2][o] = S.ip[k][3][o] = 0.f;
+                        S.acc[k][o] += double(v) * double(fscale[o]);
+                    }
+                    S.cnt[k] += uint32_t((S.ipc[k][0] + S.ipc[k][1]) + (S.ipc[k][2] + S.ipc[k][3]));
+                    S.ipc[k][0] = S.ipc[k][1] = S.ipc[k][2] = S.ipc[k][3] = 0.f;
+                }
                 __syncwarp();
                 // the chunk's j side to global: jacc[entry][j][o] (eps factors applied)
                 for (uint32_t k = lane; k < n * CJ; k += 32) {
