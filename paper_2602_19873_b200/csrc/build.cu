@@ -124,6 +124,7 @@ __device__ __noinline__ bool exact_hit(const BuildArgs& A, double xi, double yi,
 
 #include "build_fast.cuh"
 #include "build_warp.cuh"
+#include "build_p1.cuh"
 
 // Ordered-frontier BFS over the octree for one SC (collect_candidates,
 // neighbor_build.cpp:43-65). Leaves the accepted leaves (tagged, key order) in
@@ -721,6 +722,23 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
                                        : launch_build_warp<BwSmemSym, BwSmemMSym>(c, A, sc0, sc1, num_sc, ctl, &ovf_list,
                                                                                 &ovf_count);
             if (rc) return rc;
+        } else if (p.ci == 1 && p.cj == 1 && p.mode == 0 && !getenv("SFCNL_P1_GENERIC")) {
+            // point clusters: warp per SC (build_p1.cuh), per-warp global workspaces
+            constexpr uint32_t kCap = 16384;
+            const uint64_t wstride = (uint64_t(kCap) * 25 + 1024 + 255) & ~uint64_t(255);
+            const size_t smem = size_t(kBwWarps) * sizeof(P1Smem);
+            cudaFuncSetAttribute(k_build_p1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            const unsigned grid = unsigned(std::max<uint64_t>(
+                1, std::min<uint64_t>((num_sc + kBwWarps - 1) / kBwWarps, uint64_t(c->num_sms) * 4)));
+            SFCNL_CUDA_TRY(c->fallback_ws.reserve(uint64_t(grid) * kBwWarps * wstride));
+            SFCNL_CUDA_TRY(c->work_ctr.reserve(8));
+            SFCNL_CUDA_TRY(cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream));
+            launch(c, k_build_p1, dim3(grid), dim3(kBwWarps * 32), smem, A, sc0, sc1, c->work_ctr.as<unsigned long long>(),
+                   c->fallback_ws.as<uint8_t>(), wstride, kCap);
+            SFCNL_CUDA_TRY(cudaGetLastError());
+            SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
+            SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+            ovf_count = ctl[1];
         } else {
             const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(num_sc, uint64_t(c->num_sms) * 64)));
             launch(c, k_build_smem, dim3(grid), dim3(kBuildThreads), 0, A, sc0, sc1);

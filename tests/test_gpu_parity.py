@@ -178,6 +178,10 @@ def _pairs_from_store(st, n):
     ("uniform", 30011, (8, 4, 64, 1, 1, 1.1)),
     ("uniform", 30000, (8, 8, 32, 0, 0, 1.15)),
     ("uniform", 3001, (1, 1, 32, 0, 1, 1.0)),
+    # point clusters on the warp build (build_p1.cuh): skin, Evrard (open box), w64, raw
+    ("uniform", 20000, (1, 1, 32, 0, 1, 1.1)),
+    ("evrard", 20000, (1, 1, 64, 0, 1, 1.0)),
+    ("uniform", 9000, (1, 1, 32, 0, 0, 1.0)),
 ])
 def test_pipeline_vs_restatement(ctx, gen, n, cfg):
     ci, cj, w, mode, comp, scale = cfg
