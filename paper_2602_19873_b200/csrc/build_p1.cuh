@@ -19,7 +19,7 @@
 // SCs with more candidates than the workspace holds go to the global-memory fallback.
 constexpr uint32_t kP1F = 1024;  // frontier entries per buffer (point clusters accept more leaves)
 
-struct P1Smem {
+struct alignas(16) P1Smem {
     uint32_t fa[kP1F], fb[kP1F];  // traversal frontier, then per-leaf candidate prefix
     float ix[64], iy[64], iz[64], ilo[64], ihi[64];
 };

@@ -151,6 +151,12 @@ __device__ __forceinline__ float warp_fmax(float v) {
     return v;
 }
 
+__device__ __forceinline__ float warp_fmin(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
 // Block-wide exclusive scan of one uint32 per thread (blockDim.x <= 1024).
 // `scratch` must hold 33 uint32. Returns the exclusive prefix; *total = block sum.
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* scratch,

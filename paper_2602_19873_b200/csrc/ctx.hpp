@@ -139,7 +139,9 @@ struct sfcnl_cu_ctx {
     sfcnl_cu::DBuf full_cnt, full_off, full_nbr;
     // symmetric pass (pass_sym.cuh): entry base, j-side accumulators/counts, entry
     // j-cluster/SC, transposed entry lists per j-cluster
-    sfcnl_cu::DBuf sym[9];  // [8]: deferred special-slot queues of the symmetric fast pass
+    sfcnl_cu::DBuf sym[9];
+    sfcnl_cu::DBuf sym_aux;  // symmetric mixed density: per-particle error-bound weights (+ flag counter)
+    uint64_t last_redo = 0;  // particles / SCs handed to fp64 by the last mixed pass's error bound  // [8]: deferred special-slot queues of the symmetric fast pass
 
     // errors
     sfcnl_cu::DBuf derr;  // DevError

@@ -506,8 +506,11 @@ int launch_sym_fast(sfcnl_cu_ctx* c, PassArgs A) {
         SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
         A.maxh = __longlong_as_double_host(bits);
     }
+    constexpr int NE = PsSmem<K>::NE;
     auto &ebase = c->sym[0], &jacc = c->sym[1], &jcnt = c->sym[2], &ejcl = c->sym[3];
-    SFCNL_CUDA_TRY(jacc.reserve(std::max<uint64_t>(num_e, 1) * NO * A.cj * 4));
+    SFCNL_CUDA_TRY(jacc.reserve(std::max<uint64_t>(num_e, 1) * NE * A.cj * 4));
+    SFCNL_CUDA_TRY(c->sym_aux.reserve(std::max<uint64_t>(A.n, 1) * 8 + 8));
+    double* aux = c->sym_aux.as<double>();
     SFCNL_CUDA_TRY(jcnt.reserve(std::max<uint64_t>(num_e, 1) * A.cj * 4));
     SFCNL_CUDA_TRY(ejcl.reserve(std::max<uint64_t>(num_e, 1) * 4));
     const size_t smem = ps_smem<K>();
@@ -520,11 +523,22 @@ int launch_sym_fast(sfcnl_cu_ctx* c, PassArgs A) {
     SFCNL_CUDA_TRY(cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream));
     SFCNL_CUDA_TRY(c->sym[8].reserve(uint64_t(grid) * kPwWarps * kSqCap * 4));
     launch(c, kern, dim3(grid), dim3(kPwWarps * 32), smem, A, c->work_ctr.as<unsigned long long>(),
-           ebase.as<const uint64_t>(), jacc.as<float>(), jcnt.as<uint32_t>(), ejcl.as<uint32_t>(), c->sym[8].as<uint32_t>());
+           ebase.as<const uint64_t>(), jacc.as<float>(), jcnt.as<uint32_t>(), ejcl.as<uint32_t>(), c->sym[8].as<uint32_t>(), aux);
     if (int rc = sym_transpose(c, num_e, ncl, ejcl.as<const uint32_t>())) return rc;
     launch(c, k_sym_fgather<K>, dim3(unsigned(std::min<uint64_t>((A.n + 255) / 256, uint64_t(c->num_sms) * 16))), dim3(256), 0,
            A.n, uint32_t(A.cj), jacc.as<const float>(), jcnt.as<const uint32_t>(), c->sym[6].as<const uint64_t>(),
-           c->sym[7].as<const uint32_t>(), A.out[0], A.out[1], A.out[2], A.out[3], A.cnt);
+           c->sym[7].as<const uint32_t>(), A.out[0], A.out[1], A.out[2], A.out[3], A.cnt, aux);
+    if (K == SFCNL_KERNEL_DENSITY) {  // particles whose error bound exceeds the bar: the whole pass in fp64
+        unsigned long long* flagged = reinterpret_cast<unsigned long long*>(aux + A.n);
+        SFCNL_CUDA_TRY(cudaMemsetAsync(flagged, 0, 8, c->stream));
+        launch(c, k_sym_check, dim3(unsigned(std::min<uint64_t>((A.n + 255) / 256, uint64_t(c->num_sms) * 16))), dim3(256), 0,
+               A.n, A.qs, (const double*)A.out[0], (const double*)aux, flagged);
+        unsigned long long nf = 0;
+        SFCNL_CUDA_TRY(cudaMemcpyAsync(&nf, flagged, 8, cudaMemcpyDeviceToHost, c->stream));
+        SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        c->last_redo = nf;
+        if (nf) return launch_sym<K>(c, A);
+    }
     return 0;
 }
 

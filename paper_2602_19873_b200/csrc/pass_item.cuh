@@ -30,6 +30,7 @@
 // SCs whose periodic images are ambiguous in the SC frame ("unsafe") evaluate every
 // slot through rare_slot.
 constexpr int kPiWarps = 4;
+constexpr double kPiDensityDq = 2.0e-6;  // max staged-distance error / h of a density SC on the fp32 path
 
 template <int K>
 struct PiSmem {
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : 5) k_pass_i
             }
             return r;
         };
-        float eax = 0.f, eay = 0.f, eaz = 0.f, er = 0.f;
+        float eax = 0.f, eay = 0.f, eaz = 0.f, er = 0.f, hmin = 3.0e38f;
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
             const uint32_t k = lane + 32u * s;
@@ -135,6 +136,7 @@ __global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : 5) k_pass_i
                 r = dmul(A.qs, hk);
                 eax = fmaxf(eax, float(fabs(qx))), eay = fmaxf(eay, float(fabs(qy))), eaz = fmaxf(eaz, float(fabs(qz)));
                 er = fmaxf(er, float(r));
+                hmin = fminf(hmin, float(hk));
             }
             S.ia[slot] = make_float4(fx, fy, fz, float(1.0 / hk));
             if (LJ) {
@@ -150,10 +152,19 @@ __global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : 5) k_pass_i
         eax = warp_fmax(eax), eay = warp_fmax(eay), eaz = warp_fmax(eaz), er = warp_fmax(er);
         // per-particle / per-cluster images against the SC origin are exact for every
         // in-range pair when max|rel_i| + max r (+ X for the cluster frame) < 0.49 L
-        const bool unsafe = (A.box.per[0] && double(eax) + double(er) + double(Xax[0]) >= 0.49 * A.box.len[0]) ||
-                            (A.box.per[1] && double(eay) + double(er) + double(Xax[1]) >= 0.49 * A.box.len[1]) ||
-                            (A.box.per[2] && double(eaz) + double(er) + double(Xax[2]) >= 0.49 * A.box.len[2]);
+        bool unsafe = (A.box.per[0] && double(eax) + double(er) + double(Xax[0]) >= 0.49 * A.box.len[0]) ||
+                      (A.box.per[1] && double(eay) + double(er) + double(Xax[1]) >= 0.49 * A.box.len[1]) ||
+                      (A.box.per[2] && double(eaz) + double(er) + double(Xax[2]) >= 0.49 * A.box.len[2]);
         const float Ei = fmaxf(eax, fmaxf(eay, eaz));
+        if (K == SFCNL_KERNEL_DENSITY) {
+            // W(q) near the support edge amplifies the distance error (|dW/dq| / W ~ 3 / (1 - q)):
+            // SCs whose staged coordinates are coarse relative to their smallest h (far
+            // candidates of a tiny-h cluster; error of an in-range pair <= 2^-24 E_i +
+            // 2^-23 (E_i + r + X), frame.cu) take the fp64 path for every slot
+            hmin = warp_fmin(hmin);
+            const double ec = 5.9604644775390625e-08 * double(Ei) + 1.1920928955078125e-07 * (double(Ei) + double(er) + double(X));
+            unsafe |= 1.7320508075688772 * ec > kPiDensityDq * double(hmin);
+        }
         __syncwarp();
 
         bool coincident = false;

@@ -23,22 +23,28 @@
 constexpr int kPsChunk = 16;  // entries staged at a time (smaller than k_pass_warp's: more per-warp state)
 
 template <int K>
-struct PsSmem {
+struct alignas(16) PsSmem {
     static constexpr bool LJ = (K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB);
     static constexpr int NO = nout<K>();
-    float sj[kPsChunk * 4 * (LJ ? 12 : 8)];  // as PwSmem
+    // density: one more channel, the slot's weight in the error bound of the fp32 spline
+    static constexpr int NE = NO + (K == SFCNL_KERNEL_DENSITY ? 1 : 0);
+    // hi + lo staging for LJ and density (the density spline's edge amplifies distance
+    // errors by 3 / (1 - q); the few-neighbour side of a half list cannot average them)
+    static constexpr bool HL = LJ || K == SFCNL_KERNEL_DENSITY;
+    float sj[kPsChunk * 4 * (HL ? 12 : 8)];  // as PwSmem (LJ layout when HL)
+    float2 sm[K == SFCNL_KERNEL_DENSITY ? kPsChunk * 4 : 1];  // density: m of slots {a, b}
     float2 jlo[kPsChunk * 4], jhi[kPsChunk * 4];  // per (entry, quarter): thresholds of slots {a, b}
     uint32_t idx[64];
     float ix[64], iy[64], iz[64];
-    float ilx[LJ ? 64 : 1], ily[LJ ? 64 : 1], ilz[LJ ? 64 : 1];
+    float ilx[HL ? 64 : 1], ily[HL ? 64 : 1], ilz[HL ? 64 : 1];
     float iscale[64];  // density: 8 / (pi h^3)
     float iinvh[64];
-    double acc[64][NO];
+    double acc[64][NE];
     uint32_t cnt[64];
     float ilo[64], ihi[64];
-    float jside[kPsChunk][8][NO];  // the chunk's j-side sums (folded scale) per (entry, j)
+    float jside[kPsChunk][8][NE];  // the chunk's j-side sums (folded scale) per (entry, j)
     uint32_t jsc[kPsChunk][8];
-    float ip[64][4][NO];  // the chunk's i-side partial sums per (i, j-quarter lane): lane-private
+    float ip[64][4][NE];  // the chunk's i-side partial sums per (i, j-quarter lane): lane-private
     float ipc[64][4];
 };
 
@@ -75,9 +81,11 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
                                                                 unsigned long long* __restrict__ work,
                                                                 const uint64_t* __restrict__ ebase, float* __restrict__ jacc,
                                                                 uint32_t* __restrict__ jcnt, uint32_t* __restrict__ ejcl,
-                                                                uint32_t* __restrict__ squeue) {
+                                                                uint32_t* __restrict__ squeue, double* __restrict__ aux) {
     constexpr bool LJ = PsSmem<K>::LJ;
+    constexpr bool HL = PsSmem<K>::HL;
     constexpr int NO = nout<K>();
+    constexpr int NE = PsSmem<K>::NE;
     extern __shared__ __align__(16) unsigned char dsm[];
     PsSmem<K>& S = reinterpret_cast<PsSmem<K>*>(dsm)[threadIdx.x >> 5];
     const unsigned lane = lane_id();
@@ -148,10 +156,10 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
                 er = fmaxf(er, float(r));
             }
             S.ix[k] = fx, S.iy[k] = fy, S.iz[k] = fz;
-            if (LJ) S.ilx[k] = float(qx - double(fx)), S.ily[k] = float(qy - double(fy)), S.ilz[k] = float(qz - double(fz));
+            if (HL) S.ilx[k] = float(qx - double(fx)), S.ily[k] = float(qy - double(fy)), S.ilz[k] = float(qz - double(fz));
             if (K == SFCNL_KERNEL_DENSITY) S.iscale[k] = float(8.0 / (kPi * hk * hk * hk)), S.iinvh[k] = float(1.0 / hk);
 #pragma unroll
-            for (int o = 0; o < NO; ++o) {
+            for (int o = 0; o < NE; ++o) {
                 S.acc[k][o] = 0.0;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) S.ip[k][q][o] = 0.f;
@@ -231,14 +239,15 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
                                 const double qx = rel(vx[u], ox, 0), qy = rel(vy[u], oy, 1), qz = rel(vz[u], oz, 2);
                                 fx = float(qx), fy = float(qy), fz = float(qz);
                                 fm = float(vm[u]);
-                                if (LJ) lx = float(qx - double(fx)), ly = float(qy - double(fy)), lz = float(qz - double(fz));
+                                if (HL) lx = float(qx - double(fx)), ly = float(qy - double(fy)), lz = float(qz - double(fz));
                                 emax = fmaxf(emax, fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz))));
                             }
                             const uint32_t q = jj & 3, hb = (jj < 4 || CJ == 8) ? (jj >> 2) : 1u;
                             if (!(jj < 4 || CJ == 8)) fx = fy = fz = kFar, fm = 0.f, lx = ly = lz = 0.f;
-                            if (LJ) {
+                            if (HL) {
                                 float* p = S.sj + (e * 4 + q) * 12 + hb;
                                 p[0] = fx, p[2] = fy, p[4] = fz, p[6] = lx, p[8] = ly, p[10] = lz;
+                                if constexpr (K == SFCNL_KERNEL_DENSITY) reinterpret_cast<float*>(&S.sm[e * 4 + q])[hb] = fm;
                             } else {
                                 float* p = S.sj + (e * 4 + q) * 8 + hb;
                                 p[0] = fx, p[2] = fy, p[4] = fz, p[6] = fm;
@@ -342,10 +351,10 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
                         }
                     } else {
                         // the lane's staged j pair record and thresholds
-                        const ulonglong2* pb = reinterpret_cast<const ulonglong2*>(S.sj + (e * 4 + jq) * (LJ ? 12 : 8));
+                        const ulonglong2* pb = reinterpret_cast<const ulonglong2*>(S.sj + (e * 4 + jq) * (HL ? 12 : 8));
                         const ulonglong2 P0 = pb[0], P1 = pb[1];
                         ulonglong2 P2 = {0, 0};
-                        if (LJ) P2 = pb[2];
+                        if (HL) P2 = pb[2];
                         const float2 JL = S.jlo[e * 4 + jq], JH = S.jhi[e * 4 + jq];
                         for (uint32_t bits = m; bits; bits &= bits - 1) {
                             const uint32_t b = __ffs(bits) - 1;
@@ -355,7 +364,7 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
                             const float lo_i = S.ilo[li], hi_i = S.ihi[li];
                             const float fxi = S.ix[li], fyi = S.iy[li], fzi = S.iz[li];
                             f2 dx = f2sub(f2p(fxi, fxi), P0.x), dy = f2sub(f2p(fyi, fyi), P0.y), dz = f2sub(f2p(fzi, fzi), P1.x);
-                            if (LJ) {
+                            if (HL) {
                                 const float lxi = S.ilx[li], lyi = S.ily[li], lzi = S.ilz[li];
                                 dx = f2add(dx, f2sub(f2p(lxi, lxi), P1.y));
                                 dy = f2add(dy, f2sub(f2p(lyi, lyi), P2.x));
@@ -381,12 +390,21 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
                                 f2u(q, q0, q1);
                                 const f2 tt = f2p(fmaxf(1.f - q0, 0.f), fmaxf(1.f - q1, 0.f));
                                 const f2 uu = f2p(fmaxf(0.5f - q0, 0.f), fmaxf(0.5f - q1, 0.f));
-                                const f2 t3 = f2mul(f2mul(tt, tt), tt), u3 = f2mul(f2mul(uu, uu), uu);
+                                const f2 tt2 = f2mul(tt, tt), uu2 = f2mul(uu, uu);
+                                const f2 t3 = f2mul(tt2, tt), u3 = f2mul(uu2, uu);
                                 const f2 wv = f2fma(f2p(-4.f, -4.f), u3, t3);  // W / (2 sigma)
                                 float pma, pmb;
-                                f2u(P1.y, pma, pmb);
+                                if constexpr (HL) {
+                                    const float2 mm = S.sm[e * 4 + jq];
+                                    pma = mm.x, pmb = mm.y;
+                                } else {
+                                    f2u(P1.y, pma, pmb);
+                                }
                                 const float sgi = 2.f * S.iscale[li];
-                                vals[0] = f2mul(f2mul(f2p(pma * sgi, pmb * sgi), m2), wv);
+                                const f2 mw = f2mul(f2p(pma * sgi, pmb * sgi), m2);
+                                vals[0] = f2mul(mw, wv);
+                                // |dW/dq| <= 2 sigma 3 (t^2 + 4 u^2): the bound is 3 dq sum of this channel
+                                vals[1] = f2mul(mw, f2fma(f2p(4.f, 4.f), uu2, tt2));
                             } else if (LJ) {
                                 const f2 inv2 = f2mul(f2p(rcp_ftz(d2a), rcp_ftz(d2b)), m2);
                                 const f2 s2 = f2mul(f2p(sig2, sig2), inv2);
@@ -420,7 +438,7 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
                             }
                             // i side: the two slots, then the four j-quarter lanes; fp64 sums in smem
 #pragma unroll
-                            for (int o = 0; o < NO; ++o) {
+                            for (int o = 0; o < NE; ++o) {
                                 float a, c;
                                 f2u(vals[o], a, c);
                                 if (act) S.ip[li][jq][o] += a + c;
@@ -433,7 +451,7 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
                     }
                     // j side of the entry: reduce over the eight i lanes, write [entry][j][o]
 #pragma unroll
-                    for (int o = 0; o < NO; ++o) {
+                    for (int o = 0; o < NE; ++o) {
                         float a, c;
                         f2u(jv[o], a, c);
 #pragma unroll
@@ -502,7 +520,7 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
                 for (int s = 0; s < 2; ++s) {
                     const uint32_t k = lane + 32u * s;
 #pragma unroll
-                    for (int o = 0; o < NO; ++o) {
+                    for (int o = 0; o < NE; ++o) {
                         const float v = (S.ip[k][0][o] + S.ip[k][1][o]) + (S.ip[k][2][o] + S.ip[k][3][o]);
                         S.ip[k][0][o] = S.ip[k][1][o] = S.ip[k][2][o] = S.ip[k][3][o] = 0.f;
                         S.acc[k][o] += double(v) * double(fscale[o]);
@@ -516,7 +534,7 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
                     const uint32_t e = k / CJ, jj = k % CJ;
                     const uint64_t g = gE0 + bb + h0 + e;
 #pragma unroll
-                    for (int o = 0; o < NO; ++o) jacc[(g * CJ + jj) * NO + o] = S.jside[e][jj][o] * fscale[o];
+                    for (int o = 0; o < NE; ++o) jacc[(g * CJ + jj) * NE + o] = S.jside[e][jj][o] * fscale[o];
                     jcnt[g * CJ + jj] = S.jsc[e][jj];
                 }
                 __syncwarp();  // the chunk's staging is consumed
@@ -531,6 +549,7 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
                 if (k < np) {
 #pragma unroll
                     for (int o = 0; o < NO; ++o) A.out[o][p0 + k] = (K == SFCNL_KERNEL_COUNT) ? double(S.cnt[k]) : S.acc[k][o];
+                    if (NE > NO) aux[p0 + k] = S.acc[k][NE - 1];
                     A.cnt[p0 + k] = S.cnt[k];
                 }
             }
@@ -543,8 +562,9 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
 template <int K>
 __global__ void k_sym_fgather(uint64_t n, uint32_t cj, const float* __restrict__ jacc, const uint32_t* __restrict__ jcnt,
                               const uint64_t* __restrict__ tstart, const uint32_t* __restrict__ tlist, double* o0,
-                              double* o1, double* o2, double* o3, uint32_t* __restrict__ cnt) {
+                              double* o1, double* o2, double* o3, uint32_t* __restrict__ cnt, double* __restrict__ aux) {
     constexpr int NO = nout<K>();
+    constexpr int NE = PsSmem<K>::NE;
     for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n; p += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t c = p / cj, lane = p % cj;
         double acc[4] = {0, 0, 0, 0};
@@ -552,7 +572,7 @@ __global__ void k_sym_fgather(uint64_t n, uint32_t cj, const float* __restrict__
         for (uint64_t t = tstart[c]; t < tstart[c + 1]; ++t) {
             const uint64_t g = tlist[t];
 #pragma unroll
-            for (int o = 0; o < NO; ++o) acc[o] += double(jacc[(g * cj + lane) * NO + o]);
+            for (int o = 0; o < NE; ++o) acc[o] += double(jacc[(g * cj + lane) * NE + o]);
             k += jcnt[g * cj + lane];
         }
         double* outs[4] = {o0, o1, o2, o3};
@@ -562,6 +582,20 @@ __global__ void k_sym_fgather(uint64_t n, uint32_t cj, const float* __restrict__
 #pragma unroll
             for (int o = 0; o < NO; ++o) outs[o][p] += acc[o];
         }
+        if (NE > NO) aux[p] += acc[NE - 1];
         cnt[p] += k;
     }
+}
+
+// The mixed symmetric density's a-posteriori error bound: 3 dq sum_j w_ij (spline slope
+// weights, both sides) + 8 ulp rho, dq = 6 ulp qs (hi + lo staging: fp32 arithmetic only).
+// Counts the particles that might miss the 1e-5 bar (sparse, edge-dominated neighbourhoods).
+__global__ void k_sym_check(uint64_t n, double qs, const double* __restrict__ rho, const double* __restrict__ aux,
+                            unsigned long long* __restrict__ flagged) {
+    const double dq = 3.5762786865234375e-07 * qs;
+    unsigned c = 0;
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n; p += uint64_t(gridDim.x) * blockDim.x)
+        c += 3.0 * dq * aux[p] + 4.76837158203125e-07 * rho[p] > 1.0e-5 * rho[p];
+    for (int s = 16; s > 0; s >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s);
+    if (lane_id() == 0 && c) atomicAdd(flagged, (unsigned long long)c);
 }

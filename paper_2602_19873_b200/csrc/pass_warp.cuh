@@ -41,7 +41,7 @@ constexpr bool kTwo = false;
 constexpr bool kTwoDensityOff = true;
 
 template <int K>
-struct PwSmem {
+struct alignas(16) PwSmem {
     static constexpr bool LJ = (K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB);
     static constexpr int NO = nout<K>();
     static constexpr int kMinBlocks = LJ ? 4 : 6;  // CTAs of 4 warps per SM (registers: 128 / 85)
