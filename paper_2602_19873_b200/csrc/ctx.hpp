@@ -140,7 +140,7 @@ struct sfcnl_cu_ctx {
     // symmetric pass (pass_sym.cuh): entry base, j-side accumulators/counts, entry
     // j-cluster/SC, transposed entry lists per j-cluster
     sfcnl_cu::DBuf sym[9];
-    sfcnl_cu::DBuf sym_aux;  // symmetric mixed density: per-particle error-bound weights (+ flag counter)
+    sfcnl_cu::DBuf sym_aux, sym_spec;  // + fp64 j-side sums of the deferred special slots  // symmetric mixed density: per-particle error-bound weights (+ flag counter)
     uint64_t last_redo = 0;  // particles / SCs handed to fp64 by the last mixed pass's error bound  // [8]: deferred special-slot queues of the symmetric fast pass
 
     // errors

@@ -511,6 +511,9 @@ int launch_sym_fast(sfcnl_cu_ctx* c, PassArgs A) {
     SFCNL_CUDA_TRY(jacc.reserve(std::max<uint64_t>(num_e, 1) * NE * A.cj * 4));
     SFCNL_CUDA_TRY(c->sym_aux.reserve(std::max<uint64_t>(A.n, 1) * 8 + 8));
     double* aux = c->sym_aux.as<double>();
+    SFCNL_CUDA_TRY(c->sym_spec.reserve(std::max<uint64_t>(A.n, 1) * NO * 8));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(c->sym_spec.p, 0, A.n * NO * 8, c->stream));
+    double* jspec = c->sym_spec.as<double>();
     SFCNL_CUDA_TRY(jcnt.reserve(std::max<uint64_t>(num_e, 1) * A.cj * 4));
     SFCNL_CUDA_TRY(ejcl.reserve(std::max<uint64_t>(num_e, 1) * 4));
     const size_t smem = ps_smem<K>();
@@ -523,11 +526,11 @@ int launch_sym_fast(sfcnl_cu_ctx* c, PassArgs A) {
     SFCNL_CUDA_TRY(cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream));
     SFCNL_CUDA_TRY(c->sym[8].reserve(uint64_t(grid) * kPwWarps * kSqCap * 4));
     launch(c, kern, dim3(grid), dim3(kPwWarps * 32), smem, A, c->work_ctr.as<unsigned long long>(),
-           ebase.as<const uint64_t>(), jacc.as<float>(), jcnt.as<uint32_t>(), ejcl.as<uint32_t>(), c->sym[8].as<uint32_t>(), aux);
+           ebase.as<const uint64_t>(), jacc.as<float>(), jcnt.as<uint32_t>(), ejcl.as<uint32_t>(), c->sym[8].as<uint32_t>(), aux, jspec);
     if (int rc = sym_transpose(c, num_e, ncl, ejcl.as<const uint32_t>())) return rc;
     launch(c, k_sym_fgather<K>, dim3(unsigned(std::min<uint64_t>((A.n + 255) / 256, uint64_t(c->num_sms) * 16))), dim3(256), 0,
            A.n, uint32_t(A.cj), jacc.as<const float>(), jcnt.as<const uint32_t>(), c->sym[6].as<const uint64_t>(),
-           c->sym[7].as<const uint32_t>(), A.out[0], A.out[1], A.out[2], A.out[3], A.cnt, aux);
+           c->sym[7].as<const uint32_t>(), A.out[0], A.out[1], A.out[2], A.out[3], A.cnt, aux, (const double*)jspec);
     if (K == SFCNL_KERNEL_DENSITY) {  // particles whose error bound exceeds the bar: the whole pass in fp64
         unsigned long long* flagged = reinterpret_cast<unsigned long long*>(aux + A.n);
         SFCNL_CUDA_TRY(cudaMemsetAsync(flagged, 0, 8, c->stream));

@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
                                                                 unsigned long long* __restrict__ work,
                                                                 const uint64_t* __restrict__ ebase, float* __restrict__ jacc,
                                                                 uint32_t* __restrict__ jcnt, uint32_t* __restrict__ ejcl,
-                                                                uint32_t* __restrict__ squeue, double* __restrict__ aux) {
+                                                                uint32_t* __restrict__ squeue, double* __restrict__ aux,
+                                                                double* __restrict__ jspec) {
     constexpr bool LJ = PsSmem<K>::LJ;
     constexpr bool HL = PsSmem<K>::HL;
     constexpr int NO = nout<K>();
@@ -508,7 +509,8 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
 #pragma unroll
                     for (int o = 0; o < NO; ++o) {
                         atomicAdd(&S.acc[li][o], v[o]);
-                        atomicAdd(&S.jside[e][jj][o], float(((NO == 4 && o < 3) ? -v[o] : v[o]) / double(fscale[o])));
+                        // fp64 straight to the j particle (close LJ pairs can exceed the fp32 range)
+                        atomicAdd(jspec + j * NO + o, (NO == 4 && o < 3) ? -v[o] : v[o]);
                     }
                     atomicAdd(&S.cnt[li], 1u);
                     atomicAdd(&S.jsc[e][jj], 1u);
@@ -562,7 +564,8 @@ __global__ void __launch_bounds__(kPwWarps * 32, ps_min_blocks<K>()) k_pass_symw
 template <int K>
 __global__ void k_sym_fgather(uint64_t n, uint32_t cj, const float* __restrict__ jacc, const uint32_t* __restrict__ jcnt,
                               const uint64_t* __restrict__ tstart, const uint32_t* __restrict__ tlist, double* o0,
-                              double* o1, double* o2, double* o3, uint32_t* __restrict__ cnt, double* __restrict__ aux) {
+                              double* o1, double* o2, double* o3, uint32_t* __restrict__ cnt, double* __restrict__ aux,
+                              const double* __restrict__ jspec) {
     constexpr int NO = nout<K>();
     constexpr int NE = PsSmem<K>::NE;
     for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n; p += uint64_t(gridDim.x) * blockDim.x) {
@@ -580,7 +583,7 @@ __global__ void k_sym_fgather(uint64_t n, uint32_t cj, const float* __restrict__
             o0[p] += double(k);
         } else {
 #pragma unroll
-            for (int o = 0; o < NO; ++o) outs[o][p] += acc[o];
+            for (int o = 0; o < NO; ++o) outs[o][p] += acc[o] + jspec[p * NO + o];
         }
         if (NE > NO) aux[p] += acc[NE - 1];
         cnt[p] += k;

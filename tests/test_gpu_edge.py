@@ -4,14 +4,15 @@ i-/j-clusters and super-clusters), duplicated positions (stable-sort ties, d = 0
 the LJ coincidence error), a periodic box barely twice the cutoff (every SC takes the
 exact "unsafe" paths), positions exactly on the box faces (wrap), and a strongly
 clustered set (deep octree, per-particle h over two decades). For each: SFC keys/perm,
-store bytes bit-exact; fp64 density bit-exact; mixed density exact counts and within
-1e-5; for 8x8 / 8x4 gather, 8x8 symmetric and 1x1 geometries."""
+store bytes bit-exact; fp64 density and LJ bit-exact; mixed density exact counts and
+within 1e-5; mixed LJ exact counts, force / energy error <= 1e-5 x sum_j |term_ij|; for
+8x8 / 8x4 gather, 8x8 symmetric and 1x1 geometries."""
 import zlib
 
 import numpy as np
 import pytest
 
-from oracle.oracle import Oracle, Particles
+from oracle.oracle import Oracle, OracleError, Particles
 
 pytestmark = pytest.mark.gpu
 P = Oracle("port")
@@ -55,6 +56,27 @@ def _case(name):
     raise KeyError(name)
 
 
+def _abs_lj(sp, sigma, mode):
+    """sum_j |F_ij| and sum_j |E_ij| over the neighbourhood (gather: d <= h_i; symmetric:
+    d <= max(h_i, h_j)), brute force."""
+    pos = np.stack([sp.x, sp.y, sp.z], 1)
+    L = sp.box6[3:] - sp.box6[:3]
+    per = np.array(sp.periodic, bool)
+    absf, abse = np.zeros(sp.n), np.zeros(sp.n)
+    for i in range(sp.n):
+        d = pos[i] - pos
+        d[:, per] -= L[per] * np.rint(d[:, per] / L[per])
+        d2 = (d * d).sum(1)
+        r = np.maximum(sp.h[i], sp.h) if mode else sp.h[i]
+        ok = d2 <= r * r
+        ok[i] = False
+        inv2 = 1.0 / d2[ok]
+        s6 = (sigma * sigma * inv2) ** 3
+        absf[i] = np.sum(np.abs(24.0 * inv2 * (2 * s6 * s6 - s6)) * np.sqrt(d2[ok]))
+        abse[i] = np.sum(np.abs(4.0 * (s6 * s6 - s6)))
+    return absf, abse
+
+
 CASES = [f"tiny-{n}" for n in (1, 2, 7, 8, 9, 63, 64, 65, 127, 129, 700)] + ["duplicates", "tight-periodic", "faces",
                                                                                "clustered"]
 
@@ -94,9 +116,25 @@ def test_edge_case(ctx, name, geom):
     assert np.all(r32.outputs[0][~nz] == 0)
     if nz.any():
         assert np.max(np.abs(r32.outputs[0][nz] - ref[nz]) / np.abs(ref[nz])) <= 1e-5
-    if name == "duplicates":  # coincident particles: LJ raises InputError on both paths
-        with pytest.raises(Exception):
-            P.reduce("lj", sp, st, eps=1.0, sigma=0.01)
+    sigma = 0.3 * (1.0 / op.n) ** (1.0 / 3.0)
+    try:
+        lo, lcnt = P.reduce("lj", sp, st, eps=1.0, sigma=sigma)
+    except OracleError as e:  # coincident pair in range (d2 == 0, e.g. across a periodic face)
+        assert "coincident" in str(e)
         for prec in (S.F64, S.MIXED):
             with pytest.raises(S.InputError, match="coincident"):
-                S.reduce(sps, box, store, S.lj_kernel(1.0, 0.01), S.PassConfig(1.0, prec), ctx=ctx)
+                S.reduce(sps, box, store, S.lj_kernel(1.0, sigma), S.PassConfig(1.0, prec), ctx=ctx)
+        lo = None
+    if lo is not None:
+        l64 = S.reduce(sps, box, store, S.lj_kernel(1.0, sigma), S.PassConfig(1.0, S.F64), ctx=ctx)
+        assert np.array_equal(l64.neighbor_count, lcnt)
+        for k in range(4):
+            assert np.array_equal(l64.outputs[k], lo[k]), k
+        l32 = S.reduce(sps, box, store, S.lj_kernel(1.0, sigma), S.PassConfig(1.0, S.MIXED), ctx=ctx)
+        assert np.array_equal(l32.neighbor_count, lcnt)
+        absf, abse = _abs_lj(sp, sigma, mode)
+        err = np.sqrt(sum((l32.outputs[k] - lo[k]) ** 2 for k in range(3)))
+        assert np.max(err / np.maximum(absf, 1e-300)) <= 1e-5
+        assert np.max(np.abs(l32.outputs[3] - lo[3]) / np.maximum(abse, 1e-300)) <= 1e-5
+    if name == "duplicates":  # coincident particles must take the error branch above
+        assert lo is None
