@@ -61,7 +61,6 @@ struct BuildArgs {
     unsigned long long* ctl;  // [0] scratch top, [1] overflow count, [2] scratch overflow flag, [3] max h bits, [4] medium-tier overflow count
     uint64_t scratch_cap;
     uint32_t* overflow_list;
-    uint16_t* btab;  // device-side block-offset index for the pass (first 16 blocks per SC)
     const float4* frame;       // cluster-frame staging copy (frame.cu)
     const unsigned* frame_x;   // its max |offset| per axis (float bits)
     unsigned long long* prof;  // phase clocks (SFCNL_PHASE_PROF builds)
@@ -365,7 +364,6 @@ __device__ bool build_sc(const BuildArgs& A, const Workspace& W, uint64_t sc) {
             // block mask bytes, then zero the nibble bytes of this block
             const unsigned long long bm = (unsigned long long)m0 | ((unsigned long long)m1 << 32);
             if (lane < w / 8) W.ebuf[pos + lane] = uint8_t(bm >> (8 * lane));
-            if (lane == 0 && A.btab && bb / w < 16) A.btab[sc * 16 + bb / w] = uint16_t(pos - mbytes);
             for (uint32_t q = lane; q < (nib + 1) / 2; q += 32) W.ebuf[pos + w / 8 + q] = 0;
             __syncwarp();
             const uint32_t nbase = (pos + w / 8) * 2;  // nibble index of the block's first nibble
@@ -686,15 +684,10 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
     A.prof = c->build_ctl.as<unsigned long long>() + 8;
     A.overflow_list = c->overflow_list.as<uint32_t>();
     A.err = c->derr.as<DevError>();
-    A.btab = nullptr;
     A.leaf_cache = nullptr, A.leaf_count = nullptr, A.leaf_sc0 = sc0;
     if (c->leaf_cache_valid && c->jflags_valid && c->jflags_sc0 == sc0 && c->jflags_sc1 == sc1) {
         // the halo marking of this range already ran the same traversal (build_warp.cuh)
         A.leaf_cache = c->leaf_cache.as<uint32_t>(), A.leaf_count = c->leaf_count.as<uint32_t>();
-    }
-    if (p.compress) {
-        SFCNL_CUDA_TRY(c->btab.reserve(std::max<uint64_t>(num_sc, 1) * 16 * 2));
-        A.btab = c->btab.as<uint16_t>() - sc0 * 16;
     }
 
     unsigned long long ctl[5];
@@ -799,7 +792,6 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
     stage_end(c, kEncode);
     c->blob_bytes = blob_bytes;
     c->has_store = true;
-    c->btab_valid = p.compress != 0;
     return 0;
 }
 

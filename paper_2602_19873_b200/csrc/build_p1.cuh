@@ -243,7 +243,6 @@ __global__ void __launch_bounds__(kBwWarps * 32, 4) k_build_p1(const __grid_cons
                     const uint32_t bsize = w / 8 + (nib + 1) / 2;
                     const unsigned long long bm = (unsigned long long)m0 | ((unsigned long long)m1 << 32);
                     if (lane < w / 8) tenc[pos + lane] = uint8_t(bm >> (8 * lane));
-                    if (lane == 0 && A.btab && bb / w < 16) A.btab[sc * 16 + bb / w] = uint16_t(tmin<uint32_t>(pos - mbytes, 0xffff));
                     for (uint32_t q = lane; q < (nib + 1) / 2 + 4; q += 32) tenc[pos + w / 8 + q] = 0;
                     __syncwarp();
                     const uint32_t nbase = (pos + w / 8) * 2;

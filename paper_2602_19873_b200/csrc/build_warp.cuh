@@ -613,7 +613,6 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
             if (pos + bsize > Sm::kB) return false;
             const unsigned long long bm = (unsigned long long)m0 | ((unsigned long long)m1 << 32);
             if (lane < w / 8) ebuf[pos + lane] = uint8_t(bm >> (8 * lane));
-            if (lane == 0 && A.btab && bb / w < 16) A.btab[sc * 16 + bb / w] = uint16_t(pos - mbytes);
             for (uint32_t q = lane; q < (nib + 1) / 2; q += 32) ebuf[pos + w / 8 + q] = 0;
             __syncwarp();
             const uint32_t nbase = (pos + w / 8) * 2;  // nibble index of the block's first nibble

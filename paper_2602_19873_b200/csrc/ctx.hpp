@@ -116,8 +116,6 @@ struct sfcnl_cu_ctx {
     sfcnl_build_params sp{};
     uint64_t store_n = 0, num_sc = 0, blob_bytes = 0;
     sfcnl_cu::DBuf counts, offsets, blob;
-    sfcnl_cu::DBuf btab;  // device-side codec block offsets per SC (u16 x 16), not part of the store
-    bool btab_valid = false;
     uint64_t sc_base = 0;  // first (global) super-cluster of the current store
     sfcnl_cu::DBuf jflags;  // halo: u8 per global j-cluster, set by run_halo_mark
     bool jflags_valid = false;

@@ -16,17 +16,19 @@
 //   entries in ascending order and its j-cluster in ascending j, evaluating the
 //   reference expressions with round-to-nearest fp64 intrinsics. The per-i
 //   summation order equals the reference's, so gather outputs are bit-equal to
-//   reduce<double>. Symmetric stores use the mirror rule (reduce.hpp:16-21) with
-//   fp64 atomics for the j side (deterministic counts, values within 1e-12).
-// precision 1 (k_pass_fast, ci == 8, cj in {4, 8}, gather): one CTA per SC, one
-//   warp per i-cluster; lane = (i in cluster) x (j quarter). Each decoded block's
-//   j particles are staged once in shared memory as float4 (x,y,z relative to the
-//   SC's first particle, computed in fp64 then rounded; + mass), so the hot loop
-//   is fp32 FMA work on shared memory. The cutoff decision is made in fp32 with a
-//   guard band derived from the rounding-error bound of the relative coordinates;
-//   pairs inside the band are decided by the exact fp64 reference predicate, so
-//   neighbor_count (the pair set) is exact. Contributions accumulate in fp32 per
-//   lane and are combined in fp64.
+//   reduce<double>. Symmetric stores: the three deterministic steps of pass_sym.cuh
+//   (bit-equal to the reference's ordered j-side commit).
+// precision 1 (ci == 8, cj in {4, 8}): warp-per-SC kernels with a dynamic work
+//   counter -- k_pass_item (density, count: one (i-cluster, entry) item per lane,
+//   cluster-frame staging, deterministic per-round reduction), k_pass_warp (LJ,
+//   LJ+Coulomb: lane = (i, j quarter), hi + lo staging, fp64 close pairs),
+//   k_pass_symw (symmetric stores: each stored pair evaluated once, both sides). The
+//   cutoff decision is made in fp32 with a guard band derived from the rounding-error
+//   bound of the staged coordinates; slots inside the band are decided by the exact
+//   fp64 reference predicate, so neighbor_count (the pair set) is exact.
+//   Contributions accumulate in fp32 per lane and are combined in fp64. Other
+//   geometries run precision 0.
+// Also here: the full Verlet list baseline and bench::cluster_overhead (pass_full.cuh).
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -53,7 +55,6 @@ struct PassArgs {
     const uint32_t* counts;
     const uint64_t* offsets;
     const uint8_t* blob;
-    const uint16_t* btab;  // per-SC codec block offsets (device-side index, may be null)
     const double* x;
     const double* y;
     const double* z;
@@ -349,37 +350,11 @@ __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& 
 }
 
 #include "pass_fast.cuh"
-#include "pass_ws.cuh"
 #include "pass_warp.cuh"
 #include "pass_item.cuh"
 #include "pass_full.cuh"
 #include "pass_sym.cuh"
 #include "pass_symf.cuh"
-
-// Device-side block-offset index of an uploaded store: warp per SC walks the codec
-// block headers (first kBtab blocks) and records where each block starts.
-__global__ void k_block_table(const __grid_constant__ PassArgs A, uint16_t* btab) {
-    __shared__ uint32_t scratch[8][64];
-    const uint64_t sc = A.sc_begin + ((blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5);
-    if (sc >= A.num_sc) return;
-    const uint32_t count = A.counts[sc];
-    if (!count) return;
-    const uint64_t begin = A.offsets[sc], end = A.offsets[sc + 1];
-    const uint64_t mb = uint64_t(count) * A.mask_bytes;
-    if (begin + mb > end) return;  // malformed: the pass reports it
-    const uint8_t* idata = A.blob + begin + mb;
-    const uint64_t ilen = end - begin - mb;
-    const uint32_t w = uint32_t(A.w);
-    uint64_t pos = 0, run = 0;
-    for (uint32_t b = 0; b * w < count && b < uint32_t(kBtab); ++b) {
-        if (lane_id() == 0) btab[sc * kBtab + b] = uint16_t(tmin<uint64_t>(pos, 0xffff));
-        uint64_t off;
-        int msg;
-        pos = warp_decode_block(idata, ilen, pos, tmin<uint32_t>(w, count - b * w), int(w), run,
-                                scratch[(threadIdx.x >> 5) & 7], &off, &msg);
-        if (pos == ~0ull) return;
-    }
-}
 
 template <int K, int CJ>
 void launch_pass_warp(sfcnl_cu_ctx* c, const PassArgs& A) {
@@ -604,15 +579,6 @@ int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p) {
     // store arrays are local to the range: shift them so kernels index by global SC
     A.counts = c->counts.as<uint32_t>() - c->sc_base, A.offsets = c->offsets.as<uint64_t>() - c->sc_base;
     A.blob = c->blob.as<uint8_t>();
-    if (fast && A.compress) {
-        if (!c->btab_valid) {
-            SFCNL_CUDA_TRY(c->btab.reserve(c->num_sc * kBtab * 2));
-            launch(c, k_block_table, dim3(unsigned((c->num_sc * 32 + 255) / 256)), dim3(256), 0, A,
-                   c->btab.as<uint16_t>() - c->sc_base * kBtab);
-            c->btab_valid = true;
-        }
-        A.btab = c->btab.as<uint16_t>() - c->sc_base * kBtab;
-    }
     A.x = c->sorted.x.as<double>(), A.y = c->sorted.y.as<double>(), A.z = c->sorted.z.as<double>();
     A.h = c->sorted.h.as<double>();
     A.qs = p.query_scale, A.eps = p.epsilon, A.sigma = p.sigma, A.ck = p.coulomb_k;
