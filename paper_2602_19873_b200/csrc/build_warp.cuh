@@ -291,7 +291,6 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
     double ecoord_cur = 0.0;           // coordinate error bound of the current thresholds
     double pr_me = 0.0, pr2_me = 0.0;  // prefilter radius of i-cluster `lane` (neighbor_build.cpp:136)
     if (lane < nicl) pr_me = dmul(A.scale, A.igeo[icl_base + lane].maxh), pr2_me = dmul(pr_me, pr_me);
-    const uint32_t il = lane >> 2, jq = lane & 3;
     for (uint32_t c0 = 0; c0 < nC; c0 += 32) {
         const uint32_t n = tmin<uint32_t>(32, nC - c0);
         const bool valid = lane < n;

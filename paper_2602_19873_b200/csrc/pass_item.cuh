@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : 5) k_pass_i
     const uint32_t w = uint32_t(A.w);
     const float sig2 = float(A.sigma * A.sigma);
     const float eps24 = float(24.0 * A.eps), eps4 = float(4.0 * A.eps);
-    const float close2 = A.lj_close2 * sig2, tiny2 = kLjTiny2 * sig2;
+    const float close2 = A.lj_close2 * sig2;
     const double sig2d = A.sigma * A.sigma, eps24d = 24.0 * A.eps, eps4d = 4.0 * A.eps;
     // frame staging (density/count): max |offset| per axis of the cluster-frame copy
     float X = 0.f, Xax[3] = {0.f, 0.f, 0.f};

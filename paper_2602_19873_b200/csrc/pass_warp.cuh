@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
     const uint32_t w = uint32_t(A.w);
     const float sig2 = float(A.sigma * A.sigma);
     const float eps24 = float(24.0 * A.eps), eps4 = float(4.0 * A.eps);
-    const float close2 = A.lj_close2 * sig2, tiny2 = kLjTiny2 * sig2;
+    const float close2 = A.lj_close2 * sig2;
     const double sig2d = A.sigma * A.sigma, eps24d = 24.0 * A.eps, eps4d = 4.0 * A.eps;
 
     for (;;) {
