@@ -253,11 +253,25 @@ int sfcnl_cu_node_geometry_range(sfcnl_cu_ctx* ctx, uint64_t p_begin, uint64_t p
  * range computes cluster geometry only for the range and the flagged halo. */
 int sfcnl_cu_halo_mark(sfcnl_cu_ctx* ctx, const sfcnl_build_params* params, uint64_t sc_begin,
                        uint64_t sc_end, uint64_t* num_jclusters);
+/* Symmetric stores over a super-cluster range (the reference's ordered j-side commit,
+ * reduce.hpp:186-218, across ranks). sym_range_entries: the j-side accumulators of the
+ * range's entries (reference order, fp64) -> device arrays "sym.jacc" (entries x outputs x
+ * cj doubles), "sym.jcnt" (entries x cj), "sym.ejcl" (global j-cluster), "sym.esc"
+ * (global super-cluster). sym_range_final: DEVICE arrays of the entries received from
+ * earlier ranks (same layouts, in global entry order) are prepended to the local ones
+ * and every particle of the range folds them around its own i side; outputs / count
+ * as in sfcnl_cu_reduce for the range's particles. Bit-equal to the single-domain
+ * reduce<double> on a symmetric store. */
+int sfcnl_cu_sym_range_entries(sfcnl_cu_ctx* ctx, const sfcnl_pass_params* params, uint64_t* num_entries);
+int sfcnl_cu_sym_range_final(sfcnl_cu_ctx* ctx, const sfcnl_pass_params* params, uint64_t num_remote,
+                             const double* jacc, const uint32_t* jcnt, const uint32_t* ejcl,
+                             const uint32_t* esc, double* const* outs, uint32_t* neighbor_count);
 /* Device pointer + byte length of an internal array for zero-copy collectives:
  * "x","y","z","h", sorted fields by name, "keys","perm","nodes","node_geo",
  * "halo_flags","out0".."out3","count", the input slot "orig.x".."orig.h" and
  * "orig.<field>", the store "store.counts","store.offsets","store.blob", the full
- * list "full.offsets","full.neighbors".
+ * list "full.offsets","full.neighbors", the symmetric range entries "sym.jacc",
+ * "sym.jcnt","sym.ejcl","sym.esc".
  * Valid until the next call that resizes it. */
 int sfcnl_cu_device_array(sfcnl_cu_ctx* ctx, const char* name, void** ptr, uint64_t* bytes);
 

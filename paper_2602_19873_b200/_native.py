@@ -82,7 +82,8 @@ EXPORTS = [
     "sfcnl_cu_read_sorted", "sfcnl_cu_read_order", "sfcnl_cu_set_keys", "sfcnl_cu_apply_order_into",
     "sfcnl_cu_node_geometry_range", "sfcnl_cu_halo_mark", "sfcnl_cu_device_array",
     "sfcnl_cu_set_particle_records", "sfcnl_cu_build_full_list", "sfcnl_cu_get_full_list",
-    "sfcnl_cu_set_full_list", "sfcnl_cu_reduce_full", "sfcnl_cu_cluster_slots",
+    "sfcnl_cu_set_full_list", "sfcnl_cu_reduce_full", "sfcnl_cu_cluster_slots", "sfcnl_cu_sym_range_entries",
+    "sfcnl_cu_sym_range_final",
 ]
 
 _lib = None
@@ -149,6 +150,8 @@ def lib():
         "sfcnl_cu_set_full_list": (C.c_int, [P, u64, C.c_int, C.c_double, P, P, u64]),
         "sfcnl_cu_reduce_full": (C.c_int, [P, C.POINTER(PassParamsC), C.POINTER(P), P]),
         "sfcnl_cu_cluster_slots": (C.c_int, [P, C.POINTER(u64)]),
+        "sfcnl_cu_sym_range_entries": (C.c_int, [P, C.POINTER(PassParamsC), C.POINTER(u64)]),
+        "sfcnl_cu_sym_range_final": (C.c_int, [P, C.POINTER(PassParamsC), u64, P, P, P, P, C.POINTER(P), P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -487,6 +487,32 @@ class Context:
         self.check(self.L.sfcnl_cu_reduce_full(self.h, C.byref(pp), arr, _ptr(cnt)))
         return ReduceResult(list(kernel.names), outs, cnt)
 
+    def sym_range_entries(self, kernel: Kernel, cfg: PassConfig):
+        """Symmetric range store: j-side accumulators of the range's entries (device arrays
+        "sym.jacc", "sym.jcnt", "sym.ejcl", "sym.esc"); returns the entry count."""
+        pp = N.PassParamsC(kernel.kind, int(cfg.precision), float(cfg.query_scale), kernel.epsilon,
+                           kernel.sigma, kernel.coulomb_k)
+        ne = C.c_uint64()
+        self.check(self.L.sfcnl_cu_sym_range_entries(self.h, C.byref(pp), C.byref(ne)))
+        return ne.value
+
+    def sym_range_final(self, kernel: Kernel, cfg: PassConfig, n, remote, download=True):
+        """remote = (jacc, jcnt, ejcl, esc) device tensors of the entries received from
+        earlier ranks (or None); returns the range particles' ReduceResult."""
+        pp = N.PassParamsC(kernel.kind, int(cfg.precision), float(cfg.query_scale), kernel.epsilon,
+                           kernel.sigma, kernel.coulomb_k)
+        nr = 0 if remote is None else int(remote[3].numel())
+        ptrs = [None] * 4 if not nr else [int(t.data_ptr()) for t in remote]
+        nout = len(kernel.names)
+        if not download:
+            self.check(self.L.sfcnl_cu_sym_range_final(self.h, C.byref(pp), nr, *ptrs, None, None))
+            return None
+        outs = [np.empty(n) for _ in range(nout)]
+        cnt = np.empty(n, np.uint32)
+        arr = (C.c_void_p * 4)(*([o.ctypes.data for o in outs] + [None] * (4 - nout)))
+        self.check(self.L.sfcnl_cu_sym_range_final(self.h, C.byref(pp), nr, *ptrs, arr, _ptr(cnt)))
+        return ReduceResult(list(kernel.names), outs, cnt)
+
     def cluster_slots(self):
         """Pair slots of the current gather store (cluster_overhead numerator)."""
         v = C.c_uint64()

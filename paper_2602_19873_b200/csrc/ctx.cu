@@ -513,6 +513,30 @@ int sfcnl_cu_cluster_slots(sfcnl_cu_ctx* c, uint64_t* slots) {
     return finish(c);
 }
 
+int sfcnl_cu_sym_range_entries(sfcnl_cu_ctx* c, const sfcnl_pass_params* p, uint64_t* num_entries) {
+    CallScope scope(c);
+    if (!p) return set_error(c, SFCNL_INPUT_ERROR, "null pass params");
+    uint64_t ne = 0;
+    if (int rc = run_sym_range_entries(c, *p, &ne)) return rc;
+    if (num_entries) *num_entries = ne;
+    return finish(c);
+}
+
+int sfcnl_cu_sym_range_final(sfcnl_cu_ctx* c, const sfcnl_pass_params* p, uint64_t num_remote, const double* jacc,
+                             const uint32_t* jcnt, const uint32_t* ejcl, const uint32_t* esc, double* const* outs,
+                             uint32_t* count) {
+    CallScope scope(c);
+    if (!p) return set_error(c, SFCNL_INPUT_ERROR, "null pass params");
+    if (int rc = run_sym_range_final(c, *p, num_remote, jacc, jcnt, ejcl, esc)) return rc;
+    const int no = p->kernel >= 2 ? 4 : 1;
+    const uint64_t n = pass_out_count(c);
+    if (outs)
+        for (int o = 0; o < no; ++o)
+            if (int rc = download(c, outs[o], c->outs[o].p, n * 8)) return rc;
+    if (int rc = download(c, count, c->ncount.p, n * 4)) return rc;
+    return finish(c);
+}
+
 int sfcnl_cu_build_store_range(sfcnl_cu_ctx* c, const sfcnl_build_params* p, uint64_t sc_begin, uint64_t sc_end,
                                double max_h, uint64_t* num_sc, uint64_t* blob_bytes) {
     CallScope scope(c);
@@ -649,6 +673,10 @@ int sfcnl_cu_device_array(sfcnl_cu_ctx* c, const char* name, void** ptr, uint64_
     else if (nm == "store.offsets" && c->has_store) b = &c->offsets, len = (c->num_sc + 1) * 8;
     else if (nm == "store.blob" && c->has_store) b = &c->blob, len = c->blob_bytes;
     else if (nm == "full.offsets" && c->has_full) b = &c->full_off, len = (c->full_n + 1) * 8;
+    else if (nm == "sym.jacc") b = &c->sym[1], len = c->sym_e_local * (c->sym_e_kernel >= 2 ? 4 : 1) * c->sp.cj * 8;
+    else if (nm == "sym.jcnt") b = &c->sym[2], len = c->sym_e_local * c->sp.cj * 4;
+    else if (nm == "sym.ejcl") b = &c->sym[3], len = c->sym_e_local * 4;
+    else if (nm == "sym.esc") b = &c->sym[4], len = c->sym_e_local * 4;
     else if (nm == "full.neighbors" && c->has_full) b = &c->full_nbr, len = c->full_pairs * 4;
     else if (nm.rfind("orig.", 0) == 0 && c->orig.valid) {
         const std::string f = nm.substr(5);

@@ -138,7 +138,10 @@ struct sfcnl_cu_ctx {
     // symmetric pass (pass_sym.cuh): entry base, j-side accumulators/counts, entry
     // j-cluster/SC, transposed entry lists per j-cluster
     sfcnl_cu::DBuf sym[9];
-    sfcnl_cu::DBuf sym_aux, sym_spec;  // + fp64 j-side sums of the deferred special slots  // symmetric mixed density: per-particle error-bound weights (+ flag counter)
+    sfcnl_cu::DBuf sym_aux, sym_spec;
+    sfcnl_cu::DBuf symc[4];  // domain decomposition: remote + local entry accumulators (sym_range_final)
+    uint64_t sym_e_local = 0;
+    int sym_e_kernel = -1;  // + fp64 j-side sums of the deferred special slots  // symmetric mixed density: per-particle error-bound weights (+ flag counter)
     uint64_t last_redo = 0;  // particles / SCs handed to fp64 by the last mixed pass's error bound  // [8]: deferred special-slot queues of the symmetric fast pass
 
     // errors
@@ -177,6 +180,9 @@ int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p);
 int run_build_full_list(sfcnl_cu_ctx* c, double build_scale);
 int run_reduce_full(sfcnl_cu_ctx* c, const sfcnl_pass_params& p);
 int run_cluster_slots(sfcnl_cu_ctx* c, uint64_t* slots);
+int run_sym_range_entries(sfcnl_cu_ctx* c, const sfcnl_pass_params& p, uint64_t* num_e);
+int run_sym_range_final(sfcnl_cu_ctx* c, const sfcnl_pass_params& p, uint64_t nr, const double* rjacc,
+                        const uint32_t* rjcnt, const uint32_t* rejcl, const uint32_t* resc);
 // cluster-frame staging copy of the sorted positions (frame.cu); m = payload or null
 // clusters overlapping particles [p_lo, p_hi) plus those flagged in jflags (if non-null)
 int run_frame(sfcnl_cu_ctx* c, uint32_t cj, const double* m, uint64_t p_lo = 0, uint64_t p_hi = ~0ull,

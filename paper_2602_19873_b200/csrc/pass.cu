@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "ctx.hpp"
@@ -767,6 +768,146 @@ int run_cluster_slots(sfcnl_cu_ctx* c, uint64_t* slots) {
     SFCNL_CUDA_TRY(cudaMemcpyAsync(slots, c->work_ctr.p, 8, cudaMemcpyDeviceToHost, c->stream));
     SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
     return 0;
+}
+
+// ------------------------------------------------ symmetric stores under domain decomposition
+// The reference order (pass_sym.cuh) folds, per particle, the j-side accumulators of the
+// entries whose j-cluster holds it in GLOBAL entry order around its own i side. With the
+// SCs split over ranks, rank r computes the accumulators of its own entries
+// (sym_range_entries); entries whose j-cluster another rank owns are shipped there
+// (always a later rank: the half-list rule puts j at or after the entry's i-cluster);
+// the owner prepends what it receives (earlier ranks, rank order = global entry order)
+// to its own entries and runs the ordered fold for its particles (sym_range_final).
+namespace {
+int sym_range_args(sfcnl_cu_ctx* c, const sfcnl_pass_params& p, PassArgs& A, const char* who) {
+    if (!c->sorted.valid) return set_error(c, 1, std::string(who) + ": no particles");
+    if (!c->has_store) return set_error(c, 1, std::string(who) + ": no neighbor store");
+    if (c->sp.mode == 0) return set_error(c, 1, std::string(who) + ": the store must be symmetric");
+    const uint64_t n = c->sorted.n;
+    if (c->store_n != n) return set_error(c, 1, "reduce: store/particle-set size mismatch");
+    if (!(p.query_scale >= 0)) return set_error(c, 1, "PassConfig: query_scale must be >= 0");
+    if (p.query_scale > c->sp.build_radius_scale)
+        return set_error(c, 1, "reduce: query_scale exceeds the store's build radius scale");
+    if (p.kernel < 0 || p.kernel > 3) return set_error(c, 1, "reduce: unknown kernel");
+    A = PassArgs{};
+    if (p.kernel == SFCNL_KERNEL_DENSITY) {
+        auto* f = c->sorted.find("m");
+        if (!f) return set_error(c, 1, "ParticleSet: no such field: m");
+        A.m = f->data.as<double>();
+    }
+    if (p.kernel == SFCNL_KERNEL_LJ_COULOMB) {
+        auto* f = c->sorted.find("q");
+        if (!f) return set_error(c, 1, "ParticleSet: no such field: q");
+        A.q = f->data.as<double>();
+    }
+    A.n = n;
+    A.box = c->sorted.box;
+    A.ci = c->sp.ci, A.cj = c->sp.cj, A.icl_per_sc = 64 / c->sp.ci, A.mask_bytes = (A.icl_per_sc + 7) / 8;
+    A.w = c->sp.w, A.compress = c->sp.compress, A.symmetric = 1;
+    A.sc_begin = c->sc_base, A.num_sc = c->sc_base + c->num_sc, A.num_icl = (n + A.ci - 1) / A.ci;
+    A.counts = c->counts.as<uint32_t>() - c->sc_base, A.offsets = c->offsets.as<uint64_t>() - c->sc_base;
+    A.blob = c->blob.as<uint8_t>();
+    A.x = c->sorted.x.as<double>(), A.y = c->sorted.y.as<double>(), A.z = c->sorted.z.as<double>();
+    A.h = c->sorted.h.as<double>();
+    A.qs = p.query_scale, A.eps = p.epsilon, A.sigma = p.sigma, A.ck = p.coulomb_k;
+    A.err = c->derr.as<DevError>();
+    return 0;
+}
+}  // namespace
+
+int run_sym_range_entries(sfcnl_cu_ctx* c, const sfcnl_pass_params& p, uint64_t* num_e) {
+    PassArgs A;
+    if (int rc = sym_range_args(c, p, A, "sym_range_entries")) return rc;
+    const int no = p.kernel >= 2 ? 4 : 1;
+    uint64_t ne = 0;
+    if (c->num_sc) {
+        auto& ebase = c->sym[0];
+        SFCNL_CUDA_TRY(ebase.reserve((c->num_sc + 1) * 8));
+        if (int rc = excl_scan(c, c->counts.as<uint32_t>(), ebase.as<uint64_t>(), c->num_sc)) return rc;
+        uint64_t last = 0;
+        uint32_t lastc = 0;
+        SFCNL_CUDA_TRY(cudaMemcpyAsync(&last, ebase.as<uint64_t>() + c->num_sc - 1, 8, cudaMemcpyDeviceToHost, c->stream));
+        SFCNL_CUDA_TRY(cudaMemcpyAsync(&lastc, c->counts.as<uint32_t>() + c->num_sc - 1, 4, cudaMemcpyDeviceToHost, c->stream));
+        SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        ne = last + lastc;
+    }
+    auto &jacc = c->sym[1], &jcnt = c->sym[2], &ejcl = c->sym[3], &esc = c->sym[4];
+    SFCNL_CUDA_TRY(jacc.reserve(std::max<uint64_t>(ne, 1) * no * A.cj * 8));
+    SFCNL_CUDA_TRY(jcnt.reserve(std::max<uint64_t>(ne, 1) * A.cj * 4));
+    SFCNL_CUDA_TRY(ejcl.reserve(std::max<uint64_t>(ne, 1) * 4));
+    SFCNL_CUDA_TRY(esc.reserve(std::max<uint64_t>(ne, 1) * 4));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(c->derr.p, 0xff, sizeof(DevError), c->stream));
+    if (c->num_sc) {
+        const unsigned grid = unsigned(std::min<uint64_t>(c->num_sc, uint64_t(c->num_sms) * 32));
+        const uint64_t* eb = c->sym[0].as<const uint64_t>() - c->sc_base;  // indexed by global SC
+        switch (p.kernel) {
+            case 0: launch(c, k_sym_jside<0>, dim3(grid), dim3(kExactThreads), 0, A, eb, jacc.as<double>(), jcnt.as<uint32_t>(), ejcl.as<uint32_t>(), esc.as<uint32_t>()); break;
+            case 1: launch(c, k_sym_jside<1>, dim3(grid), dim3(kExactThreads), 0, A, eb, jacc.as<double>(), jcnt.as<uint32_t>(), ejcl.as<uint32_t>(), esc.as<uint32_t>()); break;
+            case 2: launch(c, k_sym_jside<2>, dim3(grid), dim3(kExactThreads), 0, A, eb, jacc.as<double>(), jcnt.as<uint32_t>(), ejcl.as<uint32_t>(), esc.as<uint32_t>()); break;
+            default: launch(c, k_sym_jside<3>, dim3(grid), dim3(kExactThreads), 0, A, eb, jacc.as<double>(), jcnt.as<uint32_t>(), ejcl.as<uint32_t>(), esc.as<uint32_t>()); break;
+        }
+        SFCNL_CUDA_TRY(cudaGetLastError());
+    }
+    c->sym_e_local = ne;
+    c->sym_e_kernel = p.kernel;
+    static const char* const kMsgs[] = {"", "blob slice too short for bitmasks", "truncated bitmask", "truncated nibble stream",
+                                        "trailing bytes in index blob", "raw index blob length mismatch", ""};
+    if (int rc = check_dev_error(c, kMsgs)) return rc;
+    *num_e = ne;
+    return 0;
+}
+
+int run_sym_range_final(sfcnl_cu_ctx* c, const sfcnl_pass_params& p, uint64_t nr, const double* rjacc,
+                        const uint32_t* rjcnt, const uint32_t* rejcl, const uint32_t* resc) {
+    PassArgs A;
+    if (int rc = sym_range_args(c, p, A, "sym_range_final")) return rc;
+    if (c->sym_e_kernel != p.kernel) return set_error(c, 1, "sym_range_final: run sym_range_entries for this kernel first");
+    const int no = p.kernel >= 2 ? 4 : 1;
+    const uint64_t cj = A.cj, nl = c->sym_e_local, nt = nr + nl;
+    auto &cjacc = c->symc[0], &cjcnt = c->symc[1], &cejcl = c->symc[2], &cesc = c->symc[3];
+    SFCNL_CUDA_TRY(cjacc.reserve(std::max<uint64_t>(nt, 1) * no * cj * 8));
+    SFCNL_CUDA_TRY(cjcnt.reserve(std::max<uint64_t>(nt, 1) * cj * 4));
+    SFCNL_CUDA_TRY(cejcl.reserve(std::max<uint64_t>(nt, 1) * 4));
+    SFCNL_CUDA_TRY(cesc.reserve(std::max<uint64_t>(nt, 1) * 4));
+    auto cp = [&](void* dst, const void* src, size_t bytes) -> int {
+        if (bytes) SFCNL_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
+        return 0;
+    };
+    // remote entries first (earlier ranks, in rank order), then the local ones
+    if (int rc = cp(cjacc.p, rjacc, nr * no * cj * 8)) return rc;
+    if (int rc = cp(cjcnt.p, rjcnt, nr * cj * 4)) return rc;
+    if (int rc = cp(cejcl.p, rejcl, nr * 4)) return rc;
+    if (int rc = cp(cesc.p, resc, nr * 4)) return rc;
+    if (int rc = cp(cjacc.as<double>() + nr * no * cj, c->sym[1].p, nl * no * cj * 8)) return rc;
+    if (int rc = cp(cjcnt.as<uint32_t>() + nr * cj, c->sym[2].p, nl * cj * 4)) return rc;
+    if (int rc = cp(cejcl.as<uint32_t>() + nr, c->sym[3].p, nl * 4)) return rc;
+    if (int rc = cp(cesc.as<uint32_t>() + nr, c->sym[4].p, nl * 4)) return rc;
+    const uint64_t ncl = (A.n + cj - 1) / cj;
+    if (int rc = sym_transpose(c, nt, ncl, cejcl.as<const uint32_t>())) return rc;
+    const uint64_t nout = pass_out_count(c), p0 = c->sc_base * 64;
+    for (int o = 0; o < no; ++o) SFCNL_CUDA_TRY(c->outs[o].reserve(std::max<uint64_t>(nout, 1) * 8));
+    SFCNL_CUDA_TRY(c->ncount.reserve(std::max<uint64_t>(nout, 1) * 4));
+    for (int o = 0; o < 4; ++o) A.out[o] = c->outs[o].as<double>() - p0;
+    A.cnt = c->ncount.as<uint32_t>() - p0;
+    SFCNL_CUDA_TRY(cudaMemsetAsync(c->derr.p, 0xff, sizeof(DevError), c->stream));
+    if (c->num_sc) {
+        const unsigned grid = unsigned(std::min<uint64_t>(c->num_sc, uint64_t(c->num_sms) * 32));
+        const double* ja = cjacc.as<const double>();
+        const uint32_t *jc = cjcnt.as<const uint32_t>(), *es = cesc.as<const uint32_t>();
+        const uint64_t* ts = c->sym[6].as<const uint64_t>();
+        const uint32_t* tl = c->sym[7].as<const uint32_t>();
+        switch (p.kernel) {
+            case 0: launch(c, k_sym_final<0>, dim3(grid), dim3(kExactThreads), 0, A, ja, jc, es, ts, tl); break;
+            case 1: launch(c, k_sym_final<1>, dim3(grid), dim3(kExactThreads), 0, A, ja, jc, es, ts, tl); break;
+            case 2: launch(c, k_sym_final<2>, dim3(grid), dim3(kExactThreads), 0, A, ja, jc, es, ts, tl); break;
+            default: launch(c, k_sym_final<3>, dim3(grid), dim3(kExactThreads), 0, A, ja, jc, es, ts, tl); break;
+        }
+        SFCNL_CUDA_TRY(cudaGetLastError());
+    }
+    static const char* const kMsgs[] = {"", "blob slice too short for bitmasks", "truncated bitmask", "truncated nibble stream",
+                                        "trailing bytes in index blob", "raw index blob length mismatch",
+                                        "reduce: coincident particles"};
+    return check_dev_error(c, kMsgs);
 }
 
 }  // namespace sfcnl_cu

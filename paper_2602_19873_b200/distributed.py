@@ -24,7 +24,10 @@ One step (``DomainDecomposition.run``), one process per GPU:
 7. halo: the rank's build traversal marks the candidate j-clusters it will read
    (exactly collect_candidates, neighbor_build.cpp:43-65); the missing ones are
    requested from their owners and their particles exchanged by two all-to-alls;
-8. range build (build_store_range) and range pass (reduce) over owned super-clusters.
+8. range build (build_store_range) and range pass (reduce) over owned super-clusters;
+   symmetric stores additionally ship each entry's j-side accumulators to the owner of
+   its j-cluster, which folds them in global entry order (reverse halo reduction,
+   bit-equal to the single-domain reduce<double>).
 
 Collectives go through ``Comm`` (torch.distributed: NCCL on device tensors; other
 backends, e.g. gloo for CPU tests or several ranks sharing one GPU, are staged through
@@ -134,6 +137,7 @@ class CudaEngine:
     """Per-rank work on one GPU through the C-ABI context (device-resident)."""
 
     def __init__(self, ctx: Context, box: SimulationBox, field_names: Sequence[str], bits=kDefaultSfcBits):
+        self.cj = 8
         self.ctx, self.box, self.fields = ctx, box, list(field_names)
         self.bits = bits
         torch = _torch()
@@ -215,6 +219,24 @@ class CudaEngine:
 
     def reduce(self, kernel: Kernel, cfg: PassConfig, nloc, download):
         return self.ctx.reduce(kernel, cfg, nloc, download=download)
+
+    # symmetric stores: entries -> (ship to owners) -> ordered fold (pass_sym.cuh)
+    def sym_entries(self, kernel: Kernel, cfg: PassConfig):
+        """-> (jacc [E, outputs*cj] f64, jcnt [E, cj] i32, ejcl [E] i32, esc [E] i32) device views."""
+        torch = _torch()
+        ne = self.ctx.sym_range_entries(kernel, cfg)
+        cj, no = self.cj, len(kernel.names)
+        if ne == 0:
+            z = torch.zeros(0, dtype=torch.int32, device=self.device)
+            return torch.zeros((0, no * cj), dtype=torch.float64, device=self.device), z.view(0, 1).expand(0, cj), z, z
+        jacc = self.ctx.device_array("sym.jacc", torch.float64, ne * no * cj).view(ne, no * cj)
+        jcnt = self.ctx.device_array("sym.jcnt", torch.int32, ne * cj).view(ne, cj)
+        ejcl = self.ctx.device_array("sym.ejcl", torch.int32, ne)
+        esc = self.ctx.device_array("sym.esc", torch.int32, ne)
+        return jacc, jcnt, ejcl, esc
+
+    def sym_final(self, kernel: Kernel, cfg: PassConfig, remote, nloc, download):
+        return self.ctx.sym_range_final(kernel, cfg, nloc, remote, download)
 
 
 class DomainDecomposition:
@@ -335,13 +357,49 @@ class DomainDecomposition:
         # (8) range build + pass
         store = E.build_range(self.bp, sc0, sc1, max_h, download)
         mark("build")
-        results = [E.reduce(k, self.cfg, p1 - p0, download) for k in self.kernels]
+        if self.bp.mode != 0:  # symmetric: entries shipped to the owners of their j-clusters
+            results = [self._sym_reduce(k, pb, p1 - p0, download) for k in self.kernels]
+        else:
+            results = [E.reduce(k, self.cfg, p1 - p0, download) for k in self.kernels]
         mark("passes")
         if prof:
             marks[-1][1].synchronize()
             print("dd phases ms:", {b[0]: round(a[1].elapsed_time(b[1]), 2) for a, b in zip(marks, marks[1:])},
                   flush=True)
         return RankResult(r, N, p0, p1, sc0, sc1, nn, halo, store, results)
+
+
+def _sym_reduce_impl(self, kernel, pb, nloc, download):
+    """Symmetric pass over the rank's range (sfcnl_cu_sym_range_*): every entry's j-side
+    accumulators go to the rank owning its j-cluster (a later rank or this one), which
+    folds the received ones (earlier ranks, rank order = global entry order) before its
+    own in the reference order."""
+    torch = _torch()
+    E, comm = self.E, self.comm
+    P, r = comm.world, comm.rank
+    dev = E.device
+    E.cj = self.bp.params.cj
+    jacc, jcnt, ejcl, esc = E.sym_entries(kernel, self.cfg)
+    cj, no = self.bp.params.cj, len(kernel.names)
+    remote = None
+    if P > 1:
+        bounds = torch.tensor(pb[1:], dtype=torch.int64, device=dev)
+        owner = torch.searchsorted(bounds, ejcl.to(torch.int64) * cj, right=True)
+        sel = torch.nonzero(owner != r).view(-1)
+        order = torch.argsort(owner[sel], stable=True)
+        sel = sel[order]
+        rows = torch.cat([jacc[sel], jcnt[sel].to(torch.float64), ejcl[sel].to(torch.float64).unsqueeze(1),
+                          esc[sel].to(torch.float64).unsqueeze(1)], dim=1)
+        send = torch.bincount(owner[sel], minlength=P)
+        mat = comm.all_gather(send).cpu().numpy()  # mat[s, q]: s sends q
+        got = comm.all_to_all_v(rows, mat[r].tolist(), mat[:, r].tolist())
+        if got.shape[0]:
+            remote = (got[:, :no * cj].contiguous(), got[:, no * cj:no * cj + cj].to(torch.int32).contiguous(),
+                      got[:, no * cj + cj].to(torch.int32).contiguous(), got[:, no * cj + cj + 1].to(torch.int32).contiguous())
+    return E.sym_final(kernel, self.cfg, remote, nloc, download)
+
+
+DomainDecomposition._sym_reduce = _sym_reduce_impl
 
 
 def merge_stores(parts: Sequence[NeighborStore]) -> NeighborStore:

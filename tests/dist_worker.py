@@ -45,7 +45,7 @@ def main():
         gp = o.make_evrard(cfg["n"], cfg["target"], False, tuple(cfg["periodic"]), cfg["seed"])
     b = shares(gp.n, world)
     idx = np.arange(b[rank], b[rank + 1])
-    bp = sfcnl.BuildParams(sfcnl.ClusterParams(cfg["ci"], cfg["cj"], cfg["w"]), sfcnl.GATHER,
+    bp = sfcnl.BuildParams(sfcnl.ClusterParams(cfg["ci"], cfg["cj"], cfg["w"]), cfg.get("mode", sfcnl.GATHER),
                            bool(cfg.get("compress", 1)), cfg.get("scale", 1.0))
     kernels = [KERNELS[k]() for k in cfg["kernels"]]
     pcfg = sfcnl.PassConfig(cfg.get("query_scale", 1.0), cfg.get("precision", sfcnl.F64))

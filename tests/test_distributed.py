@@ -59,7 +59,7 @@ def single_domain(cfg):
                             cfg.get("h_jitter", 0.0), cfg["seed"])
     else:
         gp = o.make_evrard(cfg["n"], cfg["target"], False, tuple(cfg["periodic"]), cfg["seed"])
-    keys, perm, sp, tree, store = o.pipeline(gp, ci=cfg["ci"], cj=cfg["cj"], w=cfg["w"],
+    keys, perm, sp, tree, store = o.pipeline(gp, ci=cfg["ci"], cj=cfg["cj"], w=cfg["w"], mode=cfg.get("mode", 0),
                                              scale=cfg.get("scale", 1.0))
     eps_sig = {"lj": (1.0, 0.05, 0.0), "lj_coulomb": (1.0, 0.05, 0.3)}
     outs = []
@@ -121,6 +121,23 @@ GPU_CASES = [
 def test_domain_decomposition_cuda_engine_fp64(tmp_path, case):
     cfg = dict(GPU_CASES[case], engine="cuda", precision=0)
     check(launch(2, cfg, tmp_path), cfg)
+
+
+SYM_CASES = [
+    dict(n=30000, target=50, periodic=[1, 1, 1], seed=7, ci=8, cj=8, w=32, mode=1, h_jitter=0.3,
+         kernels=["density", "lj", "count"]),
+    dict(n=20000, target=40, periodic=[0, 0, 0], seed=3, ci=8, cj=4, w=64, mode=1, dist="evrard", kernels=["density"]),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", range(len(SYM_CASES)))
+def test_domain_decomposition_symmetric_fp64(tmp_path, world, case):
+    """Symmetric stores: the reverse halo reduction keeps the reference's global entry
+    order, so the distributed outputs are bit-equal to the single-domain reduce<double>."""
+    cfg = dict(SYM_CASES[case], engine="cuda", precision=0)
+    check(launch(world, cfg, tmp_path), cfg)
 
 
 @pytest.mark.gpu
