@@ -288,7 +288,7 @@ def run_b200(args, ws, rank, local):
     # streamed: K consecutive steps, each uploading its inputs and downloading its
     # results, with the transfers overlapped with the neighbouring steps' device work
     e2e = float("nan")
-    k_stream = max(8, 4 * args.e2e_steps) if args.e2e_steps > 0 else 0
+    k_stream = max(16, 8 * args.e2e_steps) if args.e2e_steps > 0 else 0
     if k_stream:
         pipe.run_stream(2)  # warm-up: side buffers allocated once
         ctx.synchronize()
