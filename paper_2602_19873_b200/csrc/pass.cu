@@ -353,6 +353,7 @@ __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& 
 #include "pass_fast.cuh"
 #include "pass_warp.cuh"
 #include "pass_item.cuh"
+#include "pass_p1.cuh"
 #include "pass_full.cuh"
 #include "pass_sym.cuh"
 #include "pass_symf.cuh"
@@ -384,7 +385,24 @@ void launch_pass_item(sfcnl_cu_ctx* c, const PassArgs& A) {
 }
 
 template <int K>
+void launch_pass_p1(sfcnl_cu_ctx* c, const PassArgs& A) {
+    const size_t smem = size_t(kPiWarps) * sizeof(P1pSmem);
+    cudaFuncSetAttribute(k_pass_p1<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass_p1<K>, kPiWarps * 32, smem);
+    const uint64_t warps = A.num_sc - A.sc_begin;
+    const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((warps + kPiWarps - 1) / kPiWarps,
+                                                                            uint64_t(c->num_sms) * std::max(per_sm, 1))));
+    cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream);
+    launch(c, k_pass_p1<K>, dim3(grid), dim3(kPiWarps * 32), smem, A, c->work_ctr.as<unsigned long long>());
+}
+
+template <int K>
 void launch_pass(sfcnl_cu_ctx* c, const PassArgs& A, bool fast) {
+    if (fast && A.ci == 1) {  // point clusters (pass_p1.cuh)
+        launch_pass_p1<K>(c, A);
+        return;
+    }
     constexpr bool kLJ = K == SFCNL_KERNEL_LJ || K == SFCNL_KERNEL_LJ_COULOMB;
     if (fast && ((kLJ && !getenv("SFCNL_PASS_ITEM_LJ")) || (!kLJ && getenv("SFCNL_DENSITY_WARP")))) {  // warp-per-SC lane = (i, j-quarter) layout (pass_warp.cuh)
         if (A.cj == 8) launch_pass_warp<K, 8>(c, A);
@@ -554,14 +572,15 @@ int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p) {
     const bool symmetric = c->sp.mode != 0;
     if (symmetric && (c->sc_base != 0 || nout != n))
         return set_error(c, 1, "reduce: symmetric stores cannot be restricted to a super-cluster range");
-    const bool fast = p.precision == 1 && !symmetric && c->sp.ci == 8 && (c->sp.cj == 8 || c->sp.cj == 4);
+    const bool fast = p.precision == 1 && !symmetric &&
+                      ((c->sp.ci == 8 && (c->sp.cj == 8 || c->sp.cj == 4)) || (c->sp.ci == 1 && c->sp.cj == 1));
     if (symmetric || !fast) {
         for (int o = 0; o < no; ++o) SFCNL_CUDA_TRY(cudaMemsetAsync(c->outs[o].p, 0, nout * 8, c->stream));
         SFCNL_CUDA_TRY(cudaMemsetAsync(c->ncount.p, 0, nout * 4, c->stream));
     }
     SFCNL_CUDA_TRY(cudaMemsetAsync(c->derr.p, 0xff, sizeof(DevError), c->stream));
     SFCNL_CUDA_TRY(c->work_ctr.reserve(8));
-    if (fast && (p.kernel == SFCNL_KERNEL_DENSITY || p.kernel == SFCNL_KERNEL_COUNT)) {
+    if (fast && c->sp.ci == 8 && (p.kernel == SFCNL_KERNEL_DENSITY || p.kernel == SFCNL_KERNEL_COUNT)) {
         // staging copy for the item pass: the store's range (+ its halo clusters)
         const uint64_t sc0 = c->sc_base, sc1 = c->sc_base + c->num_sc;
         const bool whole = sc0 == 0 && sc1 == (n + 63) / 64;
