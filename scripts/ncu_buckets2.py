@@ -8,7 +8,7 @@ for line in out.splitlines():
         cur = [line]; sections.append(cur)
     elif cur is not None:
         cur.append(line)
-sec = next(s for s in sections if kern in s[0])
+sec = next(s for s in sections if kern in s[0].replace("(int)", ""))
 rows = list(csv.reader(sec[1:])); h = rows[0]
 IE, SMP = h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)")
 b = collections.defaultdict(lambda: [0, 0, 0])
