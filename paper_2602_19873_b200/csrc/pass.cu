@@ -424,11 +424,11 @@ int sym_transpose(sfcnl_cu_ctx* c, uint64_t num_e, uint64_t ncl, const uint32_t*
     SFCNL_CUDA_TRY(tlist.reserve(std::max<uint64_t>(num_e, 1) * 4));
     const unsigned grid_e = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((num_e + 255) / 256, uint64_t(c->num_sms) * 16)));
     SFCNL_CUDA_TRY(cudaMemsetAsync(tcnt.p, 0, (ncl + 1) * 4, c->stream));
-    if (num_e) launch(c, k_sym_tcount, dim3(grid_e), dim3(256), 0, num_e, ejcl, tcnt.as<uint32_t>());
+    if (num_e) launch(c, k_sym_tcount, dim3(grid_e), dim3(256), 0, num_e, ncl, ejcl, tcnt.as<uint32_t>());
     if (int rc = excl_scan(c, tcnt.as<uint32_t>(), tstart.as<uint64_t>(), ncl + 1)) return rc;
     SFCNL_CUDA_TRY(cudaMemsetAsync(tcnt.p, 0, (ncl + 1) * 4, c->stream));
     if (num_e)
-        launch(c, k_sym_tfill, dim3(grid_e), dim3(256), 0, num_e, ejcl, tstart.as<const uint64_t>(), tcnt.as<uint32_t>(),
+        launch(c, k_sym_tfill, dim3(grid_e), dim3(256), 0, num_e, ncl, ejcl, tstart.as<const uint64_t>(), tcnt.as<uint32_t>(),
                tlist.as<uint32_t>());
     launch(c, k_sym_tsort, dim3(unsigned(std::max<uint64_t>(1, std::min<uint64_t>((ncl + 255) / 256, uint64_t(c->num_sms) * 16)))),
            dim3(256), 0, ncl, tstart.as<const uint64_t>(), tlist.as<uint32_t>());
@@ -464,6 +464,7 @@ int launch_sym(sfcnl_cu_ctx* c, const PassArgs& A) {
     SFCNL_CUDA_TRY(ejcl.reserve(std::max<uint64_t>(num_e, 1) * 4));
     SFCNL_CUDA_TRY(esc.reserve(std::max<uint64_t>(num_e, 1) * 4));
     const unsigned grid_sc = unsigned(std::min<uint64_t>(num_sc, uint64_t(c->num_sms) * 32));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(ejcl.p, 0xff, std::max<uint64_t>(num_e, 1) * 4, c->stream));
     // ebase is indexed by global SC: A.sc_begin == 0 for symmetric stores (whole range)
     launch(c, k_sym_jside<K>, dim3(grid_sc), dim3(kExactThreads), 0, A, ebase.as<const uint64_t>(), jacc.as<double>(),
            jcnt.as<uint32_t>(), ejcl.as<uint32_t>(), esc.as<uint32_t>());
@@ -510,6 +511,7 @@ int launch_sym_fast(sfcnl_cu_ctx* c, PassArgs A) {
     double* jspec = c->sym_spec.as<double>();
     SFCNL_CUDA_TRY(jcnt.reserve(std::max<uint64_t>(num_e, 1) * A.cj * 4));
     SFCNL_CUDA_TRY(ejcl.reserve(std::max<uint64_t>(num_e, 1) * 4));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(ejcl.p, 0xff, std::max<uint64_t>(num_e, 1) * 4, c->stream));
     const size_t smem = ps_smem<K>();
     auto kern = A.cj == 8 ? k_pass_symw<K, 8> : k_pass_symw<K, 4>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -856,6 +858,7 @@ int run_sym_range_entries(sfcnl_cu_ctx* c, const sfcnl_pass_params& p, uint64_t*
     SFCNL_CUDA_TRY(ejcl.reserve(std::max<uint64_t>(ne, 1) * 4));
     SFCNL_CUDA_TRY(esc.reserve(std::max<uint64_t>(ne, 1) * 4));
     SFCNL_CUDA_TRY(cudaMemsetAsync(c->derr.p, 0xff, sizeof(DevError), c->stream));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(ejcl.p, 0xff, std::max<uint64_t>(ne, 1) * 4, c->stream));
     if (c->num_sc) {
         const unsigned grid = unsigned(std::min<uint64_t>(c->num_sc, uint64_t(c->num_sms) * 32));
         const uint64_t* eb = c->sym[0].as<const uint64_t>() - c->sc_base;  // indexed by global SC

@@ -75,16 +75,18 @@ __global__ void __launch_bounds__(kExactThreads) k_sym_jside(const __grid_consta
     }
 }
 
-__global__ void k_sym_tcount(uint64_t num_e, const uint32_t* __restrict__ ejcl, uint32_t* __restrict__ tcnt) {
+// Entries of a super-cluster whose slice failed to decode keep ejcl = ~0 (the error is
+// reported after the pass); they are left out of the lists.
+__global__ void k_sym_tcount(uint64_t num_e, uint64_t ncl, const uint32_t* __restrict__ ejcl, uint32_t* __restrict__ tcnt) {
     for (uint64_t g = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; g < num_e; g += uint64_t(gridDim.x) * blockDim.x)
-        atomicAdd(tcnt + ejcl[g], 1u);
+        if (ejcl[g] < ncl) atomicAdd(tcnt + ejcl[g], 1u);
 }
 
-__global__ void k_sym_tfill(uint64_t num_e, const uint32_t* __restrict__ ejcl, const uint64_t* __restrict__ tstart,
+__global__ void k_sym_tfill(uint64_t num_e, uint64_t ncl, const uint32_t* __restrict__ ejcl, const uint64_t* __restrict__ tstart,
                             uint32_t* __restrict__ tfill, uint32_t* __restrict__ tlist) {
     for (uint64_t g = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; g < num_e; g += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t c = ejcl[g];
-        tlist[tstart[c] + atomicAdd(tfill + c, 1u)] = uint32_t(g);
+        if (c < ncl) tlist[tstart[c] + atomicAdd(tfill + c, 1u)] = uint32_t(g);
     }
 }
 
