@@ -138,3 +138,32 @@ def test_edge_case(ctx, name, geom):
         assert np.max(np.abs(l32.outputs[3] - lo[3]) / np.maximum(abse, 1e-300)) <= 1e-5
     if name == "duplicates":  # coincident particles must take the error branch above
         assert lo is None
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_empty_particle_set(ctx, mode):
+    """n = 0 through every stage (the reference returns a one-node octree, an empty
+    store with offsets [0], empty outputs; the full list has offsets [0])."""
+    import paper_2602_19873_b200 as S
+    e = np.zeros(0)
+    ps = S.ParticleSet(e, e, e, e, {"m": e, "q": e})
+    box = S.SimulationBox((0, 0, 0), (1, 1, 1), (True, True, True))
+    order = S.sort_by_sfc(ps, box, ctx=ctx)
+    assert len(order.keys) == 0 and len(order.perm) == 0
+    tree = S.build_octree(order, ctx=ctx)
+    op = _particles(e, e, e, e, [0, 0, 0, 1, 1, 1], (1, 1, 1))
+    keys, perm, sp, otree, st = P.pipeline(op, mode=mode)
+    assert np.array_equal(tree.nodes["particle_end"], otree.pend)
+    assert np.array_equal(tree.nodes["first_child"], otree.first_child)
+    sps = S.apply_sfc_order(ps, order, ctx=ctx)
+    store = S.build_neighbor_store(sps, box, tree, S.BuildParams(S.ClusterParams(8, 8, 32), mode, True, 1.0), ctx=ctx)
+    assert len(store.counts) == 0 and np.array_equal(store.offsets, st.offsets) and len(store.blob) == 0
+    for prec in (S.F64, S.MIXED):
+        for k in (S.count_kernel(), S.sph_density_kernel(), S.lj_kernel(1.0, 0.1)):
+            res = S.reduce(sps, box, store, k, S.PassConfig(1.0, prec), ctx=ctx)
+            assert len(res.neighbor_count) == 0 and all(len(o) == 0 for o in res.outputs)
+    if mode == 0:
+        fl = S.build_full_list(ps, box, 1.0, ctx=ctx)
+        assert np.array_equal(fl.offsets, np.zeros(1, np.uint64)) and len(fl.neighbors) == 0
+        res = S.reduce_full(ps, box, fl, S.sph_density_kernel(), ctx=ctx)
+        assert len(res.outputs[0]) == 0
