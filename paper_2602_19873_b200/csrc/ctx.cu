@@ -108,6 +108,9 @@ int set_slot(sfcnl_cu_ctx* c, Slot& s, uint64_t n, const double* x, const double
              const double* h, const sfcnl_box* box) {
     if (int rc = check_box(c, box)) return rc;
     if (n && (!x || !y || !z || !h)) return set_error(c, SFCNL_INPUT_ERROR, "null particle array");
+    // particle indices are 32-bit throughout the reference (SfcOrder::perm, OctreeNode
+    // particle ranges, j-cluster indices): 2^32 - 1 particles at most
+    if (n > 0xffffffffull) return set_error(c, SFCNL_INPUT_ERROR, "ParticleSet: more than 2^32 - 1 particles");
     s.valid = false;
     s.n = n;
     s.box = make_box(box);
@@ -551,6 +554,7 @@ int sfcnl_cu_alloc_sorted(sfcnl_cu_ctx* c, uint64_t n, const sfcnl_box* box, con
                           int nfields) {
     CallScope scope(c);
     if (int rc = check_box(c, box)) return rc;
+    if (n > 0xffffffffull) return set_error(c, SFCNL_INPUT_ERROR, "ParticleSet: more than 2^32 - 1 particles");
     Slot& s = c->sorted;
     s.valid = false;
     s.n = n;
