@@ -112,6 +112,7 @@ def test_domain_decomposition_oracle_engine(tmp_path, world, case):
 
 GPU_CASES = [
     dict(n=40000, target=60, periodic=[1, 1, 1], seed=11, ci=8, cj=8, w=32, kernels=["density", "lj"]),
+    dict(n=12000, target=40, periodic=[1, 1, 0], seed=8, ci=1, cj=1, w=32, h_jitter=0.2, kernels=["density", "lj_coulomb"]),
     dict(n=30000, target=50, periodic=[0, 0, 0], seed=4, ci=8, cj=4, w=64, dist="evrard", kernels=["density"]),
 ]
 
@@ -125,7 +126,7 @@ def test_domain_decomposition_cuda_engine_fp64(tmp_path, case):
 
 SYM_CASES = [
     dict(n=30000, target=50, periodic=[1, 1, 1], seed=7, ci=8, cj=8, w=32, mode=1, h_jitter=0.3,
-         kernels=["density", "lj", "count"]),
+         kernels=["density", "lj", "count", "lj_coulomb"]),
     dict(n=20000, target=40, periodic=[0, 0, 0], seed=3, ci=8, cj=4, w=64, mode=1, dist="evrard", kernels=["density"]),
 ]
 
