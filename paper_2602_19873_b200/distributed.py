@@ -14,8 +14,9 @@ One step (``DomainDecomposition.run``), one process per GPU:
    a 64-round binary search on the key value (one all-reduce of P-1 counts per round,
    no host sync), then ties split in rank order (= global id order);
 3. all-to-all of the particle payload (x, y, z, h, fields) to the owners;
-4. owner: local SFC sort of what it received (stable => (key, global id) order) and
-   a gather straight into its slice of global-index arrays (apply_order_into);
+4. owner: the P received runs (each in (key, global id) order) are merged by binary
+   searches ((key, source rank) order = the global stable order, no re-sort) and
+   written straight into its slice of global-index arrays;
 5. all-gather of the owned keys -> every rank builds the identical global octree
    (reference numbering);
 6. node geometry from owned particles only, combined exactly by one MIN all-reduce
@@ -167,19 +168,53 @@ class CudaEngine:
         return self.ctx.device_array("keys", torch.int64, self.n_local)
 
     def payload(self):
+        """Columns in local key order: x, y, z, h, fields, and the key's bits as a float64
+        (one all-to-all per contiguous column: no row packing)."""
         torch = _torch()
-        return torch.stack(self._cols(self.n_local), dim=1)
+        keys = self.ctx.device_array("keys", torch.int64, self.n_local)
+        return self._cols(self.n_local) + [keys.view(torch.float64)]
 
     # -- (4) owner placement; returns the owned sorted keys
-    def own(self, recv, n_total, p0):
+    def own(self, recv, n_total, p0, runs=None):
+        """The received rows are P runs (one per source rank, source order), each sorted
+        by (key, global id); their merge in (key, source rank) order is the global
+        (key, global id) order. Position of a row of run s = its index in s + the
+        number of rows of runs q < s with key <= its key + of runs q > s with key < its
+        key (binary searches, no re-sort). The rows are written straight into the
+        global-index arrays at [p0, p0 + n)."""
         torch = _torch()
-        n = recv.shape[0]
-        self.ctx.set_particle_records(n, recv.contiguous(), self.fields, self.box)
-        self.ctx.sort(self.bits)
+        nf = 4 + len(self.fields)
+        cols_in = list(recv) if isinstance(recv, (list, tuple)) else [recv[:, f] for f in range(nf + 1)]
+        n = cols_in[0].shape[0]
+        keys = cols_in[nf].contiguous().view(torch.int64)
+        runs = [n] if runs is None else [int(v) for v in runs]
+        bnd = np.concatenate([[0], np.cumsum(runs)]).astype(np.int64)
+        nonempty = [q for q in range(len(runs)) if runs[q]]
+        if len(nonempty) <= 1:
+            dest = None
+        else:
+            dest = torch.empty(n, dtype=torch.int64, device=keys.device)
+            for s_ in nonempty:
+                seg = keys[bnd[s_]:bnd[s_ + 1]]
+                acc = torch.arange(seg.numel(), dtype=torch.int64, device=keys.device)
+                for q in nonempty:
+                    if q != s_:
+                        acc += torch.searchsorted(keys[bnd[q]:bnd[q + 1]], seg, right=q < s_)
+                dest[bnd[s_]:bnd[s_ + 1]] = acc
         self.ctx.alloc_sorted(n_total, self.box, self.fields)
-        self.ctx.apply_order_into(p0)
+        cols = self._cols(n_total)
+        for f in range(nf):
+            dst = cols[f].narrow(0, p0, n)
+            if dest is None:
+                dst.copy_(cols_in[f])
+            else:
+                dst.index_copy_(0, dest, cols_in[f].contiguous())
         self.n_total = n_total
-        return self.ctx.device_array("keys", torch.int64, n).clone()
+        if dest is None:
+            return keys.clone()
+        out = torch.empty_like(keys)
+        out.index_copy_(0, dest, keys)
+        return out
 
     # -- (5) global octree
     def octree(self, gkeys, bucket):
@@ -309,12 +344,18 @@ class DomainDecomposition:
         send = np.diff(cut_h[r]).tolist()
         recv = [int(cut_h[s, r + 1] - cut_h[s, r]) for s in range(P)]
         # (3) payload to owners
-        moved = comm.all_to_all_v(E.payload(), send, recv)
+        pay = E.payload()
+        if isinstance(pay, (list, tuple)):
+            moved = [comm.all_to_all_v(col, send, recv) for col in pay]
+            n_moved = int(moved[0].shape[0])
+        else:
+            moved = comm.all_to_all_v(pay, send, recv)
+            n_moved = int(moved.shape[0])
         mark("payload_a2a")
         # (4) owners place their particles at global positions [p0, p1)
         p0, p1 = pb[r], pb[r + 1]
-        assert moved.shape[0] == p1 - p0, "distributed split lost particles"
-        own_keys = E.own(moved, N, p0)
+        assert n_moved == p1 - p0, "distributed split lost particles"
+        own_keys = E.own(moved, N, p0, recv)
         mark("own_sort_place")
         # (5) global keys -> global octree
         gkeys = comm.all_gather_v(own_keys, [pb[q + 1] - pb[q] for q in range(P)])

@@ -39,7 +39,7 @@ class OracleEngine:
     def payload(self):
         return torch.from_numpy(np.stack([getattr(self.sl, c) for c in COLS], 1))
 
-    def own(self, recv, n_total, p0):
+    def own(self, recv, n_total, p0, runs=None):
         a = recv.numpy()
         ps = Particles(*[np.ascontiguousarray(a[:, k]) for k in range(6)], self.box6.copy(), self.periodic)
         keys, perm = self.o.sort_by_sfc(ps, self.bits)
