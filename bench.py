@@ -183,7 +183,13 @@ def cpu_reference(n, target, steps=1):
         stages = {k: t[i] for i, k in enumerate(["sort_by_sfc", "apply_sfc_order", "build_octree",
                                                  "build_neighbor_store", "reduce_density", "reduce_lj", "total"])}
     ms = float(np.median(times))
-    return {"value": ms * 1e6 / n, "unit": UNIT, "cores": threads, "kind": "reference",
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), model)
+    except OSError:
+        pass
+    return {"value": ms * 1e6 / n, "unit": UNIT, "cores": threads, "kind": "reference", "cpu_model": model,
             "sample": f"uniform {n} particles (same density/h for {target:.0f} nbrs), full build + density + LJ, "
                       f"median of {steps}", "stages_ms": stages, "bytes_per_particle": st[0]}
 
@@ -202,7 +208,7 @@ def run_reference(args, ws, rank):
            "data": "synthetic (reference make_uniform, seed 42)",
            "config": {"workload": "C2 uniform periodic, 200 nbrs, 8x8 gather compressed, build+density+LJ",
                       "n_per_gpu": args.n, "sample_n": n},
-           "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+           "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")},
            "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "stages_ms": res["stages_ms"], "wall_s": round(time.time() - t0, 1)}
     print(json.dumps(out), flush=True)
@@ -346,7 +352,7 @@ def run_b200(args, ws, rank, local):
     if rank == 0 and not args.no_cpu_baseline:
         try:
             cb = cpu_reference(args.cpu_sample, args.target, 1)
-            out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
             out["cpu_baseline"]["stages_ms"] = cb["stages_ms"]
         except Exception as e:  # the checker library is absent
             out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
