@@ -330,9 +330,11 @@ def run_b200(args, ws, rank, local):
         "warmup": args.warmup, "ms_per_step": round(ms_max, 3), "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "mixed f32/f64 (exact f64 cutoff decisions)",
         "data": "synthetic (make_uniform, seed 42+rank)",
-        "config": {"workload": "C2: 2^26 uniform periodic unit cube per GPU, 200 nbrs, ClusterParams(8,8,32) "
+        "config": {"workload": ("C2: 2^26" if n == 1 << 26 else f"C2-shaped: {n}") +
+                               " uniform periodic unit cube per GPU, 200 nbrs, ClusterParams(8,8,32) "
                                "gather compressed, build + SPH density + LJ (mixed)",
-                   "n_per_gpu": n, "global_particles": n * ws, "l2": "inputs 2.7 GB > L2, no flush",
+                   "n_per_gpu": n, "global_particles": n * ws,
+                   "l2": f"inputs {n * 40 / 1e9:.2f} GB " + ("> L2, no flush" if n * 40 > 126e6 else "(fits L2)"),
                    "bytes_per_particle": round(bpp, 4), "parallelism": f"domain-replica x{ws}"},
         "e2e": {"value": round(e2e * 1e6 / n, 4), "unit": UNIT, "ms_per_step": round(e2e, 2),
                 "h2d_bytes_per_step": pipe.h2d_bytes(), "d2h_bytes_per_step": pipe.d2h_bytes(),
@@ -431,7 +433,7 @@ def run_b200_distributed(args, ws, rank, local):
         "warmup": args.warmup, "ms_per_step": round(ms_max, 3), "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "mixed f32/f64 (exact f64 cutoff decisions)",
         "data": "synthetic (make_uniform per rank, seed 42+rank, global density)",
-        "config": {"workload": f"C2 weak-scaled: {ws} x 2^26 uniform periodic unit cube, 200 nbrs, "
+        "config": {"workload": f"C2 weak-scaled: {ws} x " + ("2^26" if n == 1 << 26 else str(n)) + " uniform periodic unit cube, 200 nbrs, "
                                "ClusterParams(8,8,32) gather compressed, build + SPH density + LJ (mixed)",
                    "n_per_gpu": n, "global_particles": n * ws, "l2": "inputs 2.7 GB/GPU > L2, no flush",
                    "parallelism": f"sfc-domain x{ws} (NCCL all-to-all + halo)",
