@@ -563,7 +563,7 @@ int launch_build_warp(sfcnl_cu_ctx* c, const BuildArgs& A, uint64_t sc0, uint64_
     launch(c, k_build_warp<Sm, kMinMain>, dim3(grid), dim3(kBwWarps * 32), smem, A, sc0, sc1,
            c->work_ctr.as<unsigned long long>(), (const uint32_t*)nullptr, A.overflow_list, 1);
     SFCNL_CUDA_TRY(cudaGetLastError());
-    SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (int rc_rb = readback(c, ctl, c->build_ctl.p, 5 * 8)) return rc_rb;
     SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
     *ovf_list = A.overflow_list;
     *ovf_count = 0;
@@ -576,7 +576,7 @@ int launch_build_warp(sfcnl_cu_ctx* c, const BuildArgs& A, uint64_t sc0, uint64_
         launch(c, k_build_warp<SmM, 3>, dim3(grid_m), dim3(kBwWarps * 32), smem_m, A, uint64_t(0), uint64_t(ctl[1]),
                c->work_ctr.as<unsigned long long>(), (const uint32_t*)A.overflow_list, A.overflow_list + num_sc, 4);
         SFCNL_CUDA_TRY(cudaGetLastError());
-        SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
+        if (int rc_rb = readback(c, ctl, c->build_ctl.p, 5 * 8)) return rc_rb;
         SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
         *ovf_list = A.overflow_list + num_sc;
         *ovf_count = ctl[4];
@@ -625,7 +625,7 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
     if (!c->has_tree || c->tree_n != n)
         return set_error(c, 2, "build_neighbor_store: octree/particle-set mismatch");
     unsigned long long maxh_bits = 0;
-    SFCNL_CUDA_TRY(cudaMemcpyAsync(&maxh_bits, c->build_ctl.as<unsigned long long>() + 3, 8, cudaMemcpyDeviceToHost, c->stream));
+    if (int rc_rb = readback(c, &maxh_bits, c->build_ctl.as<unsigned long long>() + 3, 8)) return rc_rb;
     SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
     double max_h;
     memcpy(&max_h, &maxh_bits, 8);
@@ -729,14 +729,14 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
             launch(c, k_build_p1, dim3(grid), dim3(kBwWarps * 32), smem, A, sc0, sc1, c->work_ctr.as<unsigned long long>(),
                    c->fallback_ws.as<uint8_t>(), wstride, kCap);
             SFCNL_CUDA_TRY(cudaGetLastError());
-            SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
+            if (int rc_rb = readback(c, ctl, c->build_ctl.p, 5 * 8)) return rc_rb;
             SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
             ovf_count = ctl[1];
         } else {
             const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(num_sc, uint64_t(c->num_sms) * 64)));
             launch(c, k_build_smem, dim3(grid), dim3(kBuildThreads), 0, A, sc0, sc1);
             SFCNL_CUDA_TRY(cudaGetLastError());
-            SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
+            if (int rc_rb = readback(c, ctl, c->build_ctl.p, 5 * 8)) return rc_rb;
             SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
             ovf_count = ctl[1];
         }
@@ -753,7 +753,7 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
             launch(c, k_build_global, dim3(unsigned(nblk)), dim3(kBuildThreads), 0, A, (const uint32_t*)ovf_list,
                    uint64_t(ovf_count), c->fallback_ws.as<uint8_t>(), stride, fcap, ccap, ecap);
             SFCNL_CUDA_TRY(cudaGetLastError());
-            SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
+            if (int rc_rb = readback(c, ctl, c->build_ctl.p, 5 * 8)) return rc_rb;
             SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
             static const char* const kMsgs[] = {"", "", "", "build_neighbor_store: workspace capacity exceeded"};
             const int rc = check_dev_error(c, kMsgs);
@@ -781,7 +781,7 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
         if (rc) return rc;
     }
     uint64_t blob_bytes = 0;
-    SFCNL_CUDA_TRY(cudaMemcpyAsync(&blob_bytes, c->offsets.as<uint64_t>() + num_sc, 8, cudaMemcpyDeviceToHost, c->stream));
+    if (int rc_rb = readback(c, &blob_bytes, c->offsets.as<uint64_t>() + num_sc, 8)) return rc_rb;
     SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
     SFCNL_CUDA_TRY(c->blob.reserve(std::max<uint64_t>(blob_bytes, 16)));
     launch(c, k_compact, dim3(unsigned((num_sc * 32 + 255) / 256)), dim3(256), 0, num_sc,
@@ -842,7 +842,7 @@ int run_halo_mark(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, ui
                c->work_ctr.as<unsigned long long>());
         SFCNL_CUDA_TRY(cudaGetLastError());
         unsigned long long ctl[2];
-        SFCNL_CUDA_TRY(cudaMemcpyAsync(ctl, c->build_ctl.p, 2 * 8, cudaMemcpyDeviceToHost, c->stream));
+        if (int rc_rb = readback(c, ctl, c->build_ctl.p, 2 * 8)) return rc_rb;
         SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
         if (ctl[1]) {
             const uint32_t fcap = uint32_t(std::min<uint64_t>(c->num_nodes + 8, 0x7fffffffull));

@@ -36,10 +36,31 @@ int set_error(sfcnl_cu_ctx* c, int code, const std::string& msg, uint64_t off) {
     return code;
 }
 
+constexpr size_t kMapBytes = 64 * 1024;
+
+__global__ void k_readback(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst, size_t bytes) {
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < bytes; k += size_t(gridDim.x) * blockDim.x)
+        dst[k] = src[k];
+}
+
+int readback(sfcnl_cu_ctx* c, void* dst, const void* src, size_t bytes) {
+    if (!bytes) return 0;
+    if (!c->hmap || bytes > kMapBytes) {  // fallback: the copy engine
+        SFCNL_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+        SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        return 0;
+    }
+    k_readback<<<unsigned(std::min<size_t>((bytes + 255) / 256, 64)), 256, 0, c->stream>>>(
+        static_cast<const unsigned char*>(src), static_cast<unsigned char*>(c->dmap), bytes);
+    SFCNL_CUDA_TRY(cudaGetLastError());
+    SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    std::memcpy(dst, c->hmap, bytes);
+    return 0;
+}
+
 int check_dev_error(sfcnl_cu_ctx* c, const char* const* messages) {
     DevError e;
-    SFCNL_CUDA_TRY(cudaMemcpyAsync(&e, c->derr.p, sizeof e, cudaMemcpyDeviceToHost, c->stream));
-    SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (int rc = readback(c, &e, c->derr.p, sizeof e)) return rc;
     if (e.key == ~0ull) return 0;
     const int code = int(e.key & 0xff);
     const int status = code >> 4, msg = code & 15;
@@ -183,6 +204,15 @@ int sfcnl_cu_ctx_create(int device, sfcnl_cu_ctx** out) {
     c->num_sms = prop.multiProcessorCount;
     SFCNL_CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     for (auto& e : c->ev) SFCNL_CUDA_TRY(cudaEventCreate(&e));
+    if (cudaHostAlloc(&c->hmap, kMapBytes, cudaHostAllocMapped) == cudaSuccess) {
+        if (cudaHostGetDevicePointer(&c->dmap, c->hmap, 0) != cudaSuccess) {
+            cudaFreeHost(c->hmap);
+            c->hmap = c->dmap = nullptr;
+        }
+    } else {
+        cudaGetLastError();
+        c->hmap = nullptr;
+    }
     SFCNL_CUDA_TRY(c->derr.reserve(sizeof(DevError)));
     SFCNL_CUDA_TRY(cudaMemsetAsync(c->derr.p, 0xff, sizeof(DevError), c->stream));
     uint16_t table[48 * 8];
@@ -201,6 +231,7 @@ void sfcnl_cu_ctx_destroy(sfcnl_cu_ctx* c) {
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->hmap) cudaFreeHost(c->hmap);
     delete c;
 }
 

@@ -149,6 +149,8 @@ struct sfcnl_cu_ctx {
     sfcnl_cu::DBuf ptrs;  // small pointer tables
     sfcnl_cu::DBuf scan_tmp;
     sfcnl_cu::DBuf small_host_dev;  // tiny device scratch for readbacks
+    void* hmap = nullptr;            // mapped pinned host page for small readbacks (no copy engine)
+    void* dmap = nullptr;            // its device alias
 
     // timing
     bool timing = false;
@@ -162,6 +164,10 @@ namespace sfcnl_cu {
 int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
 int set_error(sfcnl_cu_ctx* c, int code, const std::string& msg, uint64_t off = 0);
 int check_dev_error(sfcnl_cu_ctx* c, const char* const* messages);
+// Small device -> host readback (<= 64 KB) written by a kernel into a mapped pinned page:
+// it does not queue behind bulk transfers on the copy engines (StreamedPipeline). Syncs
+// the context's stream.
+int readback(sfcnl_cu_ctx* c, void* dst, const void* src, size_t bytes);
 
 void stage_begin(sfcnl_cu_ctx* c, Stage s);
 void stage_end(sfcnl_cu_ctx* c, Stage s);

@@ -202,7 +202,7 @@ int run_build_octree(sfcnl_cu_ctx* c, uint32_t bucket) {
             if (rc) return rc;
         }
         uint32_t I = 0;
-        SFCNL_CUDA_TRY(cudaMemcpyAsync(&I, lv.ipos.as<uint32_t>() + m, 4, cudaMemcpyDeviceToHost, c->stream));
+        if (int rc_rb = readback(c, &I, lv.ipos.as<uint32_t>() + m, 4)) return rc_rb;
         SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
         lv.internal = I;
         nlev = d + 1;

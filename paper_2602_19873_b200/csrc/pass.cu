@@ -442,8 +442,8 @@ int sym_entry_base(sfcnl_cu_ctx* c, const PassArgs& A, uint64_t num_sc, uint64_t
     if (int rc = excl_scan(c, A.counts + A.sc_begin, ebase.as<uint64_t>(), num_sc)) return rc;
     uint64_t last = 0;
     uint32_t lastc = 0;
-    SFCNL_CUDA_TRY(cudaMemcpyAsync(&last, ebase.as<uint64_t>() + num_sc - 1, 8, cudaMemcpyDeviceToHost, c->stream));
-    SFCNL_CUDA_TRY(cudaMemcpyAsync(&lastc, A.counts + A.num_sc - 1, 4, cudaMemcpyDeviceToHost, c->stream));
+    if (int rc_rb = readback(c, &last, ebase.as<uint64_t>() + num_sc - 1, 8)) return rc_rb;
+    if (int rc_rb = readback(c, &lastc, A.counts + A.num_sc - 1, 4)) return rc_rb;
     SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
     *num_e = last + lastc;
     return 0;
@@ -497,7 +497,7 @@ int launch_sym_fast(sfcnl_cu_ctx* c, PassArgs A) {
         launch(c, k_max_h, dim3(unsigned(std::min<uint64_t>((A.n + 255) / 256, uint64_t(c->num_sms) * 8))), dim3(256), 0, A.n,
                A.h, c->small_host_dev.as<unsigned long long>());
         unsigned long long bits = 0;
-        SFCNL_CUDA_TRY(cudaMemcpyAsync(&bits, c->small_host_dev.p, 8, cudaMemcpyDeviceToHost, c->stream));
+        if (int rc_rb = readback(c, &bits, c->small_host_dev.p, 8)) return rc_rb;
         SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
         A.maxh = __longlong_as_double_host(bits);
     }
@@ -533,7 +533,7 @@ int launch_sym_fast(sfcnl_cu_ctx* c, PassArgs A) {
         launch(c, k_sym_check, dim3(unsigned(std::min<uint64_t>((A.n + 255) / 256, uint64_t(c->num_sms) * 16))), dim3(256), 0,
                A.n, A.qs, (const double*)A.out[0], (const double*)aux, flagged);
         unsigned long long nf = 0;
-        SFCNL_CUDA_TRY(cudaMemcpyAsync(&nf, flagged, 8, cudaMemcpyDeviceToHost, c->stream));
+        if (int rc_rb = readback(c, &nf, flagged, 8)) return rc_rb;
         SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
         c->last_redo = nf;
         if (nf) return launch_sym<K>(c, A);
@@ -678,7 +678,7 @@ int run_build_full_list(sfcnl_cu_ctx* c, double build_scale) {
                (const uint64_t*)nullptr, (uint32_t*)nullptr);
     if (int rc = excl_scan(c, c->full_cnt.as<uint32_t>(), c->full_off.as<uint64_t>(), n + 1)) return rc;
     uint64_t pairs = 0;
-    SFCNL_CUDA_TRY(cudaMemcpyAsync(&pairs, c->full_off.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, c->stream));
+    if (int rc_rb = readback(c, &pairs, c->full_off.as<uint64_t>() + n, 8)) return rc_rb;
     SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
     SFCNL_CUDA_TRY(c->full_nbr.reserve(std::max<uint64_t>(pairs, 1) * 4));
     if (A.num_sc)
@@ -786,7 +786,7 @@ int run_cluster_slots(sfcnl_cu_ctx* c, uint64_t* slots) {
                                         "raw index blob length mismatch",
                                         ""};
     if (int rc = check_dev_error(c, kMsgs)) return rc;
-    SFCNL_CUDA_TRY(cudaMemcpyAsync(slots, c->work_ctr.p, 8, cudaMemcpyDeviceToHost, c->stream));
+    if (int rc_rb = readback(c, slots, c->work_ctr.p, 8)) return rc_rb;
     SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
     return 0;
 }
@@ -847,8 +847,8 @@ int run_sym_range_entries(sfcnl_cu_ctx* c, const sfcnl_pass_params& p, uint64_t*
         if (int rc = excl_scan(c, c->counts.as<uint32_t>(), ebase.as<uint64_t>(), c->num_sc)) return rc;
         uint64_t last = 0;
         uint32_t lastc = 0;
-        SFCNL_CUDA_TRY(cudaMemcpyAsync(&last, ebase.as<uint64_t>() + c->num_sc - 1, 8, cudaMemcpyDeviceToHost, c->stream));
-        SFCNL_CUDA_TRY(cudaMemcpyAsync(&lastc, c->counts.as<uint32_t>() + c->num_sc - 1, 4, cudaMemcpyDeviceToHost, c->stream));
+        if (int rc_rb = readback(c, &last, ebase.as<uint64_t>() + c->num_sc - 1, 8)) return rc_rb;
+        if (int rc_rb = readback(c, &lastc, c->counts.as<uint32_t>() + c->num_sc - 1, 4)) return rc_rb;
         SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
         ne = last + lastc;
     }

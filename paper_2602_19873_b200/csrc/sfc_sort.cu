@@ -327,7 +327,7 @@ int run_sort_by_sfc(sfcnl_cu_ctx* c, int bits) {
     launch(c, k_digit_base, dim3(npass), dim3(256), 0, (const uint32_t*)c->hist.as<uint32_t>(),
            c->digit_base.as<uint32_t>(), npass);
     std::vector<uint32_t> hist(npass * 256);
-    SFCNL_CUDA_TRY(cudaMemcpyAsync(hist.data(), c->hist.p, npass * 256 * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (int rc_rb = readback(c, hist.data(), c->hist.p, npass * 256 * 4)) return rc_rb;
     SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
     const size_t smem = size_t(kTile) * 12;
     SFCNL_CUDA_TRY(cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
