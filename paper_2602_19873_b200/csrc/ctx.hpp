@@ -127,7 +127,7 @@ struct sfcnl_cu_ctx {
     // (5) pass
     sfcnl_cu::DBuf outs[4], ncount, jstage;
     sfcnl_cu::DBuf work_ctr;  // dynamic work counter of the warp-per-SC kernels
-    sfcnl_cu::DBuf frame, frame_x;  // cluster-frame fp32 positions (+ payload), max |offset| per axis (frame.cu)
+    sfcnl_cu::DBuf frame, frame_x, frame_xcl;  // cluster-frame fp32 positions (+ payload), max |offset| per axis (frame.cu)
 
     // full Verlet list baseline (pass_full.cuh): CSR offsets u64[n+1], neighbors u32
     bool has_full = false;

@@ -11,7 +11,8 @@
 // 2^-24 (|shift| + |off_p| + |s_p|) <= 2^-23 (|s_p| + |off_p|) (+ fp64 rounding far
 // below the guard margins), which the callers' guard bands account for. The global
 // maximum |off| per axis (X) bounds the image ambiguity of the per-cluster shift:
-// callers treat a super-cluster as unsafe when max|rel_i| + r_max + X >= 0.49 L.
+// callers treat a super-cluster as unsafe when max|rel_i| + r_max + X >= 0.49 L. The
+// per-cluster maximum |off| (xcl) bounds the staging error of a given cluster.
 #include "ctx.hpp"
 
 namespace sfcnl_cu {
@@ -22,7 +23,7 @@ namespace {
 __global__ void k_frame(uint64_t n, uint32_t cj, const double* __restrict__ x, const double* __restrict__ y,
                         const double* __restrict__ z, const double* __restrict__ m, Box box, uint64_t c_lo,
                         uint64_t c_hi, const uint8_t* __restrict__ jflags, float4* __restrict__ frame,
-                        unsigned* __restrict__ xmax) {
+                        unsigned* __restrict__ xmax, unsigned* __restrict__ xcl) {
     float ax = 0.f, ay = 0.f, az = 0.f;
     for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n; p += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t cl = p / cj;
@@ -42,6 +43,8 @@ __global__ void k_frame(uint64_t n, uint32_t cj, const double* __restrict__ x, c
         }
         ax = fmaxf(ax, fabsf(f[0])), ay = fmaxf(ay, fabsf(f[1])), az = fmaxf(az, fabsf(f[2]));
         frame[p] = make_float4(f[0], f[1], f[2], m ? float(m[p]) : 0.f);
+        // per-cluster max |offset| (non-negative floats order like their bits)
+        atomicMax(xcl + cl, __float_as_uint(fmaxf(fabsf(f[0]), fmaxf(fabsf(f[1]), fabsf(f[2])))));
     }
     ax = warp_fmax(ax), ay = warp_fmax(ay), az = warp_fmax(az);
     if (lane_id() == 0) {  // non-negative floats order like their bit patterns
@@ -60,11 +63,14 @@ int run_frame(sfcnl_cu_ctx* c, uint32_t cj, const double* m, uint64_t p_lo, uint
     SFCNL_CUDA_TRY(c->frame.reserve(std::max<uint64_t>(n, 1) * sizeof(float4)));
     SFCNL_CUDA_TRY(c->frame_x.reserve(4 * sizeof(unsigned)));
     SFCNL_CUDA_TRY(cudaMemsetAsync(c->frame_x.p, 0, 4 * sizeof(unsigned), c->stream));
+    const uint64_t ncl = (n + cj - 1) / cj;
+    SFCNL_CUDA_TRY(c->frame_xcl.reserve(std::max<uint64_t>(ncl, 1) * sizeof(unsigned)));
+    SFCNL_CUDA_TRY(cudaMemsetAsync(c->frame_xcl.p, 0, std::max<uint64_t>(ncl, 1) * sizeof(unsigned), c->stream));
     if (n) {
         const int grid = int(std::min<uint64_t>((n + 255) / 256, uint64_t(c->num_sms) * 16));
         launch(c, k_frame, dim3(grid), dim3(256), 0, n, cj, c->sorted.x.as<const double>(), c->sorted.y.as<const double>(),
                c->sorted.z.as<const double>(), m, c->sorted.box, c_lo, c_hi, jflags, c->frame.as<float4>(),
-               c->frame_x.as<unsigned>());
+               c->frame_x.as<unsigned>(), c->frame_xcl.as<unsigned>());
     }
     return 0;
 }

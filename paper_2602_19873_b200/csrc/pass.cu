@@ -68,6 +68,7 @@ struct PassArgs {
     float sig2f;      // float(sigma^2)
     const float4* frame;     // cluster-frame staging copy (frame.cu), density/count
     const unsigned* frame_x; // its max |offset| per axis (float bits)
+    const unsigned* frame_xcl;  // per j-cluster max |offset| (float bits)
     double* out[4];
     uint32_t* cnt;
     DevError* err;
@@ -592,6 +593,7 @@ int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p) {
         if (rc) return rc;
         A.frame = c->frame.as<const float4>();
         A.frame_x = c->frame_x.as<const unsigned>();
+        A.frame_xcl = c->frame_xcl.as<const unsigned>();
     }
     A.n = n;
     A.box = c->sorted.box;

@@ -152,19 +152,20 @@ __global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : 5) k_pass_i
         eax = warp_fmax(eax), eay = warp_fmax(eay), eaz = warp_fmax(eaz), er = warp_fmax(er);
         // per-particle / per-cluster images against the SC origin are exact for every
         // in-range pair when max|rel_i| + max r (+ X for the cluster frame) < 0.49 L
-        bool unsafe = (A.box.per[0] && double(eax) + double(er) + double(Xax[0]) >= 0.49 * A.box.len[0]) ||
-                      (A.box.per[1] && double(eay) + double(er) + double(Xax[1]) >= 0.49 * A.box.len[1]) ||
-                      (A.box.per[2] && double(eaz) + double(er) + double(Xax[2]) >= 0.49 * A.box.len[2]);
+        const bool unsafe = (A.box.per[0] && double(eax) + double(er) + double(Xax[0]) >= 0.49 * A.box.len[0]) ||
+                            (A.box.per[1] && double(eay) + double(er) + double(Xax[1]) >= 0.49 * A.box.len[1]) ||
+                            (A.box.per[2] && double(eaz) + double(er) + double(Xax[2]) >= 0.49 * A.box.len[2]);
         const float Ei = fmaxf(eax, fmaxf(eay, eaz));
-        if (K == SFCNL_KERNEL_DENSITY) {
-            // W(q) near the support edge amplifies the distance error (|dW/dq| / W ~ 3 / (1 - q)):
-            // SCs whose staged coordinates are coarse relative to their smallest h (far
-            // candidates of a tiny-h cluster; error of an in-range pair <= 2^-24 E_i +
-            // 2^-23 (E_i + r + X), frame.cu) take the fp64 path for every slot
-            hmin = warp_fmin(hmin);
-            const double ec = 5.9604644775390625e-08 * double(Ei) + 1.1920928955078125e-07 * (double(Ei) + double(er) + double(X));
-            unsafe |= 1.7320508075688772 * ec > kPiDensityDq * double(hmin);
-        }
+        // W(q) near the support edge amplifies the distance error (|dW/dq| / W ~ 3 / (1 - q)):
+        // chunks whose staged coordinates are coarse relative to the SC's smallest h (far
+        // candidates of a tiny-h cluster; error of an in-range pair <= 2^-24 E_i +
+        // 2^-23 (E_i + r + X_J), X_J = the staged clusters' max offset, frame.cu) take the
+        // fp64 path for every slot
+        hmin = warp_fmin(hmin);
+        const double ec_i = 5.9604644775390625e-08 * double(Ei) + 1.1920928955078125e-07 * (double(Ei) + double(er));
+        // with the global max offset X the whole SC is fine: no per-chunk check
+        const bool check_chunks =
+            K == SFCNL_KERNEL_DENSITY && 1.7320508075688772 * (ec_i + 1.1920928955078125e-07 * double(X)) > kPiDensityDq * double(hmin);
         __syncwarp();
 
         bool coincident = false;
@@ -203,8 +204,13 @@ __global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : 5) k_pass_i
                 const uint32_t my_msk = have ? uint32_t(rec[bb + h0 + lane]) : 0u;
                 const int jl0_me = int(my_idx) * CJ - int(p0);
                 const bool self_me = have && jl0_me > -CJ && jl0_me < kSC;
+                bool coarse = false;
+                if (K == SFCNL_KERNEL_DENSITY && check_chunks && !unsafe) {
+                    const float xc = warp_fmax(have ? __uint_as_float(A.frame_xcl[my_idx]) : 0.f);
+                    coarse = 1.7320508075688772 * (ec_i + 1.1920928955078125e-07 * double(xc)) > kPiDensityDq * double(hmin);
+                }
 
-                if (unsafe) {
+                if (unsafe || coarse) {
                     // every slot through the reference predicate + fp64 kernel
                     for (uint32_t b = 0; b < nicl; ++b) {
                         unsigned mine = __ballot_sync(0xffffffffu, (my_msk >> b) & 1u);
