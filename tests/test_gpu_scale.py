@@ -92,11 +92,17 @@ def _range_store(run, sc0, sc1):
 
 
 def test_density_mixed_on_sampled_ranges(run):
+    same = total = 0
     for sc0, sc1 in run["ranges"]:
         outs, cnt = P.reduce_range("density", run["sp"], _range_store(run, sc0, sc1), sc0)
         p0, p1 = 64 * sc0, 64 * sc0 + len(cnt)
         assert np.array_equal(run["rho"].neighbor_count[p0:p1], cnt)
         assert np.max(np.abs(run["rho"].outputs[0][p0:p1] - outs[0]) / np.abs(outs[0])) <= 1e-5
+        same += int(np.sum(run["rho"].outputs[0][p0:p1] == outs[0]))
+        total += len(cnt)
+    # the mixed pass must actually run its fp32 path (its results are not bit-equal to fp64);
+    # guards against precision checks that silently route the configuration to fp64
+    assert same < 0.5 * total, (same, total)
 
 
 def test_lj_mixed_on_sampled_ranges(run):
