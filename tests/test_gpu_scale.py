@@ -140,6 +140,7 @@ def test_lj_mixed_on_sampled_ranges(run):
                     absf[ii - p0] += np.sum(np.abs(24.0 * inv2 * (2 * s6 * s6 - s6)) * np.sqrt(d2) * ok, 1)
                     abse[ii - p0] += np.sum(np.abs(4.0 * (s6 * s6 - s6)) * ok, 1)
         f = run["lj"].outputs
+        assert np.sum(f[3][p0:p1] == outs[3]) < 0.5 * (p1 - p0)  # the fp32 path ran
         err = np.sqrt(sum((f[k][p0:p1] - outs[k]) ** 2 for k in range(3)))
         assert np.max(err / np.maximum(absf, 1e-300)) <= 1e-5
         assert np.max(np.abs(f[3][p0:p1] - outs[3]) / np.maximum(abse, 1e-300)) <= 1e-5
