@@ -307,6 +307,32 @@ class Oracle:
             _p(store.offsets, U64), _p(blob, U8), D(query_scale), D(eps), D(sigma), D(ck), optr, _p(cnt, U32)))
         return [o[:nloc] for o in outs], cnt[:nloc]
 
+    # ---- reference-only checkers for the full-size parity tests
+    def cluster_geometry(self, ps: Particles, width):
+        """compute_cluster_geometry (neighbor_build.cpp:19-38) via cluster_aabb /
+        cluster_max_radius (cluster.hpp:77-90): (lo (ncl,3), hi (ncl,3), maxh (ncl,))."""
+        assert self.kind == "reference"
+        ncl = (ps.n + width - 1) // width
+        lo, hi, mh = np.empty((max(ncl, 1), 3)), np.empty((max(ncl, 1), 3)), np.empty(max(ncl, 1))
+        self._check(self._f("cluster_geometry")(U64(ps.n), _p(ps.x, D), _p(ps.y, D), _p(ps.z, D), _p(ps.h, D),
+                                                U32(width), _p(lo, D), _p(hi, D), _p(mh, D)))
+        return lo[:ncl], hi[:ncl], mh[:ncl]
+
+    def lj_abs_sums(self, ps: Particles, store: Store, query_scale=1.0, eps=1.0, sigma=1.0, threads=1):
+        """sum_j |F_ij| and sum_j |E_ij| per particle through the reference's reduce<double>
+        with a make_pair_kernel user kernel (the LJ normwise tolerance denominators)."""
+        assert self.kind == "reference"
+        n = ps.n
+        absf, abse = np.zeros(n), np.zeros(n)
+        per = (C.c_int * 3)(*ps.periodic)
+        blob = store.blob if len(store.blob) else np.zeros(1, np.uint8)
+        self._check(self._f("lj_abs_sums")(
+            U64(n), _p(ps.x, D), _p(ps.y, D), _p(ps.z, D), _p(ps.h, D), _p(ps.box6, D), per, U32(store.ci),
+            U32(store.cj), C.c_int(store.w), C.c_int(store.mode), C.c_int(store.compress), D(store.scale),
+            U64(len(store.counts)), _p(store.counts, U32), _p(store.offsets, U64), _p(blob, U8),
+            U64(len(store.blob)), D(query_scale), C.c_int(threads), D(eps), D(sigma), _p(absf, D), _p(abse, D)))
+        return absf, abse
+
     # ---- full Verlet list baseline (reference only: baselines.hpp:39-131)
     def full_list(self, ps: Particles, build_scale=1.0, kernels=(), query_scale=1.0, eps=1.0, sigma=1.0, mode=0):
         """build_full_list (cell grid, baselines.cpp:39-131) -> (offsets u64[n+1],

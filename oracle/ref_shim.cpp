@@ -15,7 +15,9 @@
 //   ref_reduce                           reduce.hpp:38-231 (+ simd_avx2.cpp when isa=avx2)
 //   ref_codec_*                          nibble_codec.hpp:20-63
 //   ref_pipeline                         the run_bench sequence (bench.cpp:147-186), all stages timed
+#include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -486,5 +488,60 @@ REF_API int ref_pipeline(uint64_t n, const double* x, const double* y, const dou
         out_stats[2] = double(entries);
         out_stats[3] = double(store.blob.size());
         if (rho_out) std::memcpy(rho_out, dens.output("rho").data(), n * 8);
+    });
+}
+
+// ---- per-cluster geometry (compute_cluster_geometry, neighbor_build.cpp:19-38) ---------
+// Clusters [k*width, min((k+1)*width, n)) through the reference's own cluster_aabb /
+// cluster_max_radius (cluster.hpp:77-90). lo/hi: [ncl*3], maxh: [ncl].
+REF_API int ref_cluster_geometry(uint64_t n, const double* x, const double* y, const double* z,
+                                 const double* h, uint32_t width, double* lo, double* hi,
+                                 double* maxh) {
+    return guarded([&] {
+        const auto ps = make_ps(n, x, y, z, h, nullptr, nullptr);
+        const uint64_t ncl = (n + width - 1) / width;
+        for (uint64_t k = 0; k < ncl; ++k) {
+            const uint64_t b = k * width, e = std::min<uint64_t>(b + width, n);
+            const auto a = sfcnl_ref::cluster_aabb(ps, b, e);
+            for (int d = 0; d < 3; ++d) lo[3 * k + d] = a.lo[d], hi[3 * k + d] = a.hi[d];
+            maxh[k] = sfcnl_ref::cluster_max_radius(ps, b, e);
+        }
+    });
+}
+
+// ---- LJ normwise tolerance denominators ------------------------------------------
+// sum_j |F_ij| and sum_j |E_ij| over each particle's in-range neighbourhood, computed by
+// the reference's own reduce<double> (reduce.hpp:38-231) with a user pair kernel built by
+// make_pair_kernel (pair_kernel.hpp:81-91): the same pair set and term formulas as
+// LjKernel (builtin_kernels.hpp:54-66), absolute values summed.
+REF_API int ref_lj_abs_sums(uint64_t n, const double* x, const double* y, const double* z,
+                            const double* h, const double* box6, const int* per, uint32_t ci,
+                            uint32_t cj, int w, int mode, int compress, double scale,
+                            uint64_t num_sc, const uint32_t* counts, const uint64_t* offsets,
+                            const uint8_t* blob, uint64_t blob_size, double query_scale,
+                            int threads, double eps, double sigma, double* absf, double* abse) {
+    return guarded([&] {
+        const auto ps = make_ps(n, x, y, z, h, nullptr, nullptr);
+        const auto box = make_box(box6, per);
+        const auto store = make_store(n, ci, cj, w, mode, compress, scale, num_sc, counts,
+                                      offsets, blob, blob_size);
+        using sfcnl_ref::OutputSpec;
+        auto k = sfcnl_ref::make_pair_kernel<double, 0, 2>(
+            std::array<const char*, 0>{},
+            std::array<OutputSpec, 2>{{{"absf", sfcnl_ref::Symmetry::even, sfcnl_ref::Reduction::sum},
+                                       {"abse", sfcnl_ref::Symmetry::even, sfcnl_ref::Reduction::sum}}},
+            [eps, sigma](const sfcnl_ref::PairArgs<double>& a, const std::array<double, 0>&,
+                         const std::array<double, 0>&) -> std::array<double, 2> {
+                const double inv2 = 1.0 / a.d2;
+                const double s2 = sigma * sigma * inv2;
+                const double s6 = s2 * s2 * s2;
+                const double coef = 24.0 * eps * inv2 * (2.0 * s6 * s6 - s6);
+                const double e = 4.0 * eps * (s6 * s6 - s6);
+                return {std::fabs(coef) * std::sqrt(a.d2), std::fabs(e)};
+            });
+        const sfcnl_ref::PassConfig cfg(query_scale, sfcnl_ref::Isa::automatic, threads);
+        const auto r = sfcnl_ref::reduce<double>(ps, box, store, k, cfg);
+        std::memcpy(absf, r.outputs[0].data(), n * 8);
+        std::memcpy(abse, r.outputs[1].data(), n * 8);
     });
 }

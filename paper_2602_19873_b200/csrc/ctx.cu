@@ -471,6 +471,7 @@ int sfcnl_cu_set_store(sfcnl_cu_ctx* c, const sfcnl_build_params* p, uint64_t n,
     if (int rc = upload(c, c->offsets, offsets, (num_sc + 1) * 8)) return rc;
     if (int rc = upload(c, c->blob, blob, blob_bytes)) return rc;
     c->sp = *p;
+    c->clgeo_whole = false;
     c->store_n = n;
     c->num_sc = num_sc;
     c->blob_bytes = blob_bytes;
@@ -701,6 +702,12 @@ int sfcnl_cu_device_array(sfcnl_cu_ctx* c, const char* name, void** ptr, uint64_
     else if (nm == "node_geo" && c->has_tree) b = &c->node_geo, len = c->num_nodes * sizeof(Geo);
     else if (nm == "nodes" && c->has_tree) b = &c->nodes, len = c->num_nodes * sizeof(Node);
     else if (nm == "halo_flags" && c->jflags_valid) b = &c->jflags, len = c->jflags_len;
+    // per-cluster geometry of the last build (compute_cluster_geometry, neighbor_build.cpp:19-38):
+    // Geo {lo[3], hi[3], maxh, pad} per cluster; j-clusters alias i-clusters when ci == cj
+    else if (nm == "cluster_geo.i" && c->has_store && c->clgeo_whole && c->sorted.valid)
+        b = &c->igeo, len = (c->sorted.n + c->sp.ci - 1) / c->sp.ci * sizeof(Geo);
+    else if (nm == "cluster_geo.j" && c->has_store && c->clgeo_whole && c->sorted.valid)
+        b = c->sp.cj == c->sp.ci ? &c->igeo : &c->jgeo, len = (c->sorted.n + c->sp.cj - 1) / c->sp.cj * sizeof(Geo);
     else if (nm.rfind("out", 0) == 0 && nm.size() == 4 && nm[3] >= '0' && nm[3] <= '3')
         b = &c->outs[nm[3] - '0'], len = pass_out_count(c) * 8;
     else if (nm == "count") b = &c->ncount, len = pass_out_count(c) * 4;

@@ -114,6 +114,7 @@ struct sfcnl_cu_ctx {
     // (4) store
     bool has_store = false;
     sfcnl_build_params sp{};
+    bool clgeo_whole = false;  // igeo/jgeo hold every cluster of the current sorted set (device_array)
     uint64_t store_n = 0, num_sc = 0, blob_bytes = 0;
     sfcnl_cu::DBuf counts, offsets, blob;
     uint64_t sc_base = 0;  // first (global) super-cluster of the current store

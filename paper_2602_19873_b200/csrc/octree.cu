@@ -303,6 +303,7 @@ int run_cluster_geometry(sfcnl_cu_ctx* c, uint32_t ci, uint32_t cj, uint64_t p0,
     SFCNL_CUDA_TRY(c->jgeo.reserve(std::max<uint64_t>(nj, 1) * sizeof(Geo)));
     if (!n) return 0;
     if (p1 > n) p1 = n;
+    c->clgeo_whole = p0 == 0 && p1 == n && !jflags;
     stage_begin(c, kClusterGeo);
     // i-clusters: the range (plus the flagged halo when the array doubles as jgeo)
     launch(c, k_cluster_geo, dim3(blocks_for(ni)), dim3(256), 0, n, ci, ni, c->sorted.x.as<const double>(),

@@ -1,0 +1,157 @@
+"""Full-size parity against the UNMODIFIED reference (oracle/_ref, compiled from
+/root/reference/proj/src), at the BASELINE.json sizes, with no sampling and no
+GPU-produced intermediates on the reference side:
+
+* C2: 2^26 uniform particles, periodic unit cube, 200 neighbours, 8x8 gather compressed;
+* C3: Evrard sphere, 2^24 particles, per-particle h, open box.
+
+The inputs come from the reference's own generator (generators.cpp:21-82) and the same
+host bytes go to both sides. The reference runs its whole pipeline on the host
+(sort_by_sfc -> apply_sfc_order -> build_octree -> compute_node_aabbs/max_radius ->
+build_neighbor_store -> reduce<double>) with every host thread; the GPU runs its own
+through the C-ABI. Compared in full:
+
+* SfcOrder keys and perm (hilbert.cpp:8-26)                       bit-exact
+* every octree node (octree.cpp:43-59)                             bit-exact
+* node AABBs and max radii (octree.cpp:68-96)                      bit-exact
+* cluster AABBs and max h (neighbor_build.cpp:19-38)              bit-exact
+* NeighborStore counts / offsets / every blob byte                 bit-exact
+* fp64 density and LJ (reduce<double>, reduce.hpp:38-231)          bit-exact, counts exact
+* mixed density: counts exact, relative error <= 1e-5 for every particle
+* mixed LJ: counts exact, |F - F_ref| <= 1e-5 * sum_j |F_ij| and |E - E_ref| <= 1e-5 *
+  sum_j |E_ij| for every particle (denominators from the reference's reduce<double>
+  with a make_pair_kernel user kernel, oracle/ref_shim.cpp ref_lj_abs_sums).
+
+The reference side takes a few minutes at C2 on the GPU box's host cores.
+SFCNL_FULLSIZE=0 skips these tests."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2602_19873_b200 as S
+from oracle.oracle import Oracle, available
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not available("reference"), reason="oracle/_ref not built"),
+              pytest.mark.skipif(os.environ.get("SFCNL_FULLSIZE", "1") == "0", reason="SFCNL_FULLSIZE=0")]
+THREADS = os.cpu_count() or 1
+
+CONFIGS = {
+    "C2": ("uniform", int(os.environ.get("SFCNL_FULLSIZE_C2_N", str(1 << 26)))),
+    "C3": ("evrard", int(os.environ.get("SFCNL_FULLSIZE_C3_N", str(1 << 24)))),
+}
+
+
+@pytest.fixture(scope="module", params=sorted(CONFIGS))
+def run(request):
+    import torch
+    gen, n = CONFIGS[request.param]
+    R = Oracle("reference")
+    op = (R.make_uniform(n, float(n), 200.0, (1, 1, 1), 0.0, 42) if gen == "uniform"
+          else R.make_evrard(n, 200.0, False, (0, 0, 0), 42))
+    sigma = 0.5 * (1.0 / n) ** (1.0 / 3.0)
+    bp = S.BuildParams(S.ClusterParams(8, 8, 32), S.GATHER, True, 1.0)
+
+    # ---- GPU, through the C-ABI
+    ctx = S.Context(0)
+    box = S.SimulationBox(tuple(op.box6[:3]), tuple(op.box6[3:]), tuple(bool(v) for v in op.periodic))
+    ctx.set_particles(S.ParticleSet(op.x, op.y, op.z, op.h, {"m": op.m}), box)
+    ctx.sort()
+    g = {}
+    g["keys"], g["perm"] = ctx.get_order(n)
+    ctx.apply_order()
+    nn = ctx.octree(64)
+    g["nodes"] = ctx.get_octree(nn)
+    g["node_geo"] = ctx.node_geometry(nn)
+    nsc, nb = ctx.build_store(bp)
+    g["store"] = ctx.get_store(bp, n, nsc, nb)
+    cg = ctx.device_array("cluster_geo.i", torch.float64).view(-1, 8).cpu().numpy()
+    g["cluster_geo"] = (cg[:, 0:3], cg[:, 3:6], cg[:, 6])
+    g["rho64"] = ctx.reduce(S.sph_density_kernel(), S.PassConfig(1.0, S.F64), n)
+    g["rho32"] = ctx.reduce(S.sph_density_kernel(), S.PassConfig(1.0, S.MIXED), n)
+    g["lj64"] = ctx.reduce(S.lj_kernel(1.0, sigma), S.PassConfig(1.0, S.F64), n)
+    g["lj32"] = ctx.reduce(S.lj_kernel(1.0, sigma), S.PassConfig(1.0, S.MIXED), n)
+    ctx.close()
+
+    # ---- reference, on the host, from the same input bytes
+    r = {}
+    r["keys"], r["perm"] = R.sort_by_sfc(op)
+    sp = op.permuted(r["perm"])  # apply_sfc_order (hilbert.cpp:28-44) is a gather by perm
+    del op
+    tree, lo, hi, rad = R.node_geometry(r["keys"], sp)
+    r["tree"], r["node_geo"] = tree, (lo, hi, rad)
+    r["cluster_geo"] = R.cluster_geometry(sp, 8)
+    r["store"] = R.build_store(sp, tree, 8, 8, 32, 0, 1, 1.0, threads=THREADS)
+    r["rho"] = R.reduce("density", sp, r["store"], threads=THREADS)
+    r["lj"] = R.reduce("lj", sp, r["store"], eps=1.0, sigma=sigma, threads=THREADS)
+    r["lj_abs"] = R.lj_abs_sums(sp, r["store"], eps=1.0, sigma=sigma, threads=THREADS)
+    return g, r
+
+
+def test_sfc_order(run):
+    g, r = run
+    assert np.array_equal(g["keys"], r["keys"])
+    assert np.array_equal(g["perm"], r["perm"])
+
+
+def test_octree_nodes(run):
+    g, r = run
+    nodes, t = g["nodes"], r["tree"]
+    assert len(nodes) == len(t.pend)
+    for gf, rf in (("key_first", "key_first"), ("key_last", "key_last"), ("particle_begin", "pbegin"),
+                   ("particle_end", "pend"), ("first_child", "first_child"), ("depth", "depth")):
+        assert np.array_equal(np.asarray(nodes[gf]).astype(np.int64), getattr(t, rf).astype(np.int64)), gf
+
+
+def test_node_geometry(run):
+    g, r = run
+    for a, b in zip(g["node_geo"], r["node_geo"]):
+        assert np.array_equal(a, b)
+
+
+def test_cluster_geometry(run):
+    g, r = run
+    for a, b in zip(g["cluster_geo"], r["cluster_geo"]):
+        assert np.array_equal(a, b)
+
+
+def test_store_every_byte(run):
+    g, r = run
+    assert np.array_equal(g["store"].counts, r["store"].counts)
+    assert np.array_equal(g["store"].offsets, r["store"].offsets)
+    assert np.array_equal(g["store"].blob, r["store"].blob)
+    assert S.memory_footprint(g["store"]).bytes_per_particle <= 4.0
+
+
+def test_fp64_density_and_lj_bit_exact(run):
+    g, r = run
+    outs, cnt = r["rho"]
+    assert np.array_equal(g["rho64"].neighbor_count, cnt)
+    assert np.array_equal(g["rho64"].outputs[0], outs[0])
+    outs, cnt = r["lj"]
+    assert np.array_equal(g["lj64"].neighbor_count, cnt)
+    for k in range(4):
+        assert np.array_equal(g["lj64"].outputs[k], outs[k]), k
+
+
+def test_mixed_density_all_particles(run):
+    g, r = run
+    outs, cnt = r["rho"]
+    assert np.array_equal(g["rho32"].neighbor_count, cnt)
+    nz = outs[0] != 0
+    assert np.all(g["rho32"].outputs[0][~nz] == 0)
+    assert np.max(np.abs(g["rho32"].outputs[0][nz] - outs[0][nz]) / np.abs(outs[0][nz])) <= 1e-5
+    assert np.sum(g["rho32"].outputs[0] == outs[0]) < 0.5 * len(cnt)  # the fp32 path ran
+
+
+def test_mixed_lj_all_particles(run):
+    g, r = run
+    outs, cnt = r["lj"]
+    absf, abse = r["lj_abs"]
+    f = g["lj32"].outputs
+    assert np.array_equal(g["lj32"].neighbor_count, cnt)
+    err = np.sqrt(sum((f[k] - outs[k]) ** 2 for k in range(3)))
+    assert np.max(err / np.maximum(absf, 1e-300)) <= 1e-5
+    assert np.max(np.abs(f[3] - outs[3]) / np.maximum(abse, 1e-300)) <= 1e-5
+    assert np.sum(f[3] == outs[3]) < 0.5 * len(cnt)

@@ -56,6 +56,29 @@ def test_sort_octree_store_match_reference(golden, ctx):
     assert np.array_equal(store.blob, g["blob"])
 
 
+@pytest.mark.skipif(not __import__("oracle.oracle", fromlist=["available"]).available("reference"),
+                    reason="oracle/_ref not built")
+def test_cluster_geometry_matches_reference(golden, ctx):
+    """A6 directly: the per-cluster AABB and max h the build reads (k_cluster_geo,
+    octree.cu) against compute_cluster_geometry (neighbor_build.cpp:19-38) through the
+    reference's own cluster_aabb / cluster_max_radius (cluster.hpp:77-90), i-clusters
+    (width ci) and j-clusters (width cj), bit for bit."""
+    import torch
+    g = golden
+    R = Oracle("reference")
+    sp, box = golden_particles(g, sorted_=True)
+    bp = _bp(g)
+    tree = S.build_octree(S.SfcOrder(g["keys"], g["perm"], 21), 64, ctx=ctx)
+    S.build_neighbor_store(sp, box, tree, bp, ctx=ctx)
+    osp = oracle_particles(g, sorted_=True)
+    for name, width in (("cluster_geo.i", bp.params.ci), ("cluster_geo.j", bp.params.cj)):
+        cg = ctx.device_array(name, torch.float64).view(-1, 8).cpu().numpy()
+        lo, hi, mh = R.cluster_geometry(osp, width)
+        assert np.array_equal(cg[:, 0:3], lo), name
+        assert np.array_equal(cg[:, 3:6], hi), name
+        assert np.array_equal(cg[:, 6], mh), name
+
+
 def test_pass_fp64_matches_reference(golden, ctx):
     g = golden
     sp, box = golden_particles(g, sorted_=True)
