@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsfcnl_b200.so")
+# SFCNL_LIB: an alternative build of the same library (A/B runs of compile-time variants)
+LIB_PATH = os.environ.get("SFCNL_LIB") or os.path.join(HERE, "libsfcnl_b200.so")
 
 # status codes (sfcnl_cu.h)
 OK, INPUT_ERROR, BUILD_ERROR, DECODE_ERROR, CUDA_ERROR = 0, 1, 2, 3, 4

@@ -46,7 +46,12 @@ struct PiSmem {
     double iscale[K == SFCNL_KERNEL_DENSITY ? 64 : 1];  // [i] density: 2 * 8 / (pi h^3)
     double acc[64][NO];
     uint32_t cnt[64];
-    float part[8][NO + 1][32];  // per round: [row ii][output | count][lane]
+#ifndef SFCNL_PI_PAD
+#define SFCNL_PI_PAD 1
+#endif
+    // per round: [row ii][output | count][lane]; rows padded so the per-i reduction (lanes
+    // of one i-cluster read the same item column of 8 different rows) is conflict-free
+    float part[8][NO + 1][32 + SFCNL_PI_PAD];
     uint32_t idx[64];
     uint8_t items[256];
 };
@@ -444,14 +449,14 @@ __global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : 5) k_pass_i
                             if (ncnt != nh0 + nh1) band_rows |= 1u << ii;  // a slot with d2 in [lo, hi]
                             if (LJ) close_bits |= (unsigned long long)crow << (8 * ii);
                             float* pp = &S.part[ii][0][lane];
-                            pp[NO * 32] = ncnt;
+                            pp[NO * (32 + SFCNL_PI_PAD)] = ncnt;
                             if (K != SFCNL_KERNEL_COUNT) {
                                 const f2 accs[4] = {acc0, acc1, acc2, acc3};
 #pragma unroll
                                 for (int o = 0; o < NO; ++o) {
                                     float a0, a1;
                                     f2u(accs[o], a0, a1);
-                                    pp[o * 32] = K == SFCNL_KERNEL_LJ ? (a0 + a1) * (o < 3 ? eps24 : eps4) : a0 + a1;
+                                    pp[o * (32 + SFCNL_PI_PAD)] = K == SFCNL_KERNEL_LJ ? (a0 + a1) * (o < 3 ? eps24 : eps4) : a0 + a1;
                                 }
                             }
                         }
@@ -480,7 +485,7 @@ __global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : 5) k_pass_i
                             float* pp = &S.part[ii][0][lane];
                             if (!(dd2 >= double(kLjTiny2) * sig2d)) {
                                 // coincidence range: the reference predicate + fp64 kernel
-                                pp[NO * 32] -= 1.f;
+                                pp[NO * (32 + SFCNL_PI_PAD)] -= 1.f;
                                 const int rc = rare_slot<K>(A, p0 + li, jb0 + jj, dmul(S.ir[li], S.ir[li]), &S.acc[li][0]);
                                 if (rc > 0) atomicAdd(&S.cnt[li], 1u);
                                 coincident |= rc < 0;
@@ -495,8 +500,9 @@ __global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : 5) k_pass_i
                                 en += qq * irr;
                                 coef += qq * irr * in2;
                             }
-                            pp[0] += float(coef * ddx), pp[32] += float(coef * ddy);
-                            pp[64] += float(coef * ddz), pp[96] += float(en);
+                            constexpr int R = 32 + SFCNL_PI_PAD;
+                            pp[0] += float(coef * ddx), pp[R] += float(coef * ddy);
+                            pp[2 * R] += float(coef * ddz), pp[3 * R] += float(en);
                         }
                     }
                     // band rows: the reference's predicate decides the slots in [lo, hi]

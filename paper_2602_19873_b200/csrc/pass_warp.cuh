@@ -37,7 +37,11 @@ constexpr int kPwChunk = 32;   // entries staged at a time
 // (coincidence range) take the reference's fp64 path (rare_slot).
 constexpr float kLjClose2 = 1.5f;
 constexpr float kLjTiny2 = 1e-6f;
+#ifdef SFCNL_PW_TWO
+constexpr bool kTwo = true;
+#else
 constexpr bool kTwo = false;
+#endif
 constexpr bool kTwoDensityOff = true;
 
 template <int K>
