@@ -46,7 +46,9 @@ def parse():
     p.add_argument("--particles", "--n", dest="n", type=int, default=1 << 26)  # per GPU
     p.add_argument("--target", type=float, default=200.0)
     p.add_argument("--e2e-steps", type=int, default=2)
-    p.add_argument("--cpu-sample", type=int, default=1 << 20)
+    p.add_argument("--cpu-sample", type=int, default=1 << 20)  # cpu_baseline leg of the b200 arm
+    p.add_argument("--ref-n", type=int, default=0)  # --impl reference: particles (0 = the full workload)
+    p.add_argument("--no-f64", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
@@ -159,6 +161,25 @@ def composite_roofline(stage, n, pk, ms):
             "model": "HBM bytes for streaming stages, FP32 lane-ops for build/passes (bench.py composite_roofline)"}
 
 
+# FP32 lane-ops per unit of work (SURVEY §8(d) cost model): per pair slot the
+# d2 (and for LJ the hi+lo correction) + masks, per in-range pair the kernel value
+LANE_OP_MODEL = {
+    "pass_fx": "12 per pair slot (hi+lo d2: 9, mask 3) + 16 per in-range pair (rcp, s6, coef, energy, 4 sums)",
+    "pass_rho": "18 per pair slot (d2 6, sqrt, spline 10, mask) + 12 per in-range pair",
+    "build": "9 per exact pair test (464 per particle, neighbor_build.cpp:128-161)",
+}
+
+
+def lane_ops(kernel, slots, hits, n):
+    if kernel == "pass_fx":
+        return 12 * slots + 16 * hits
+    if kernel == "pass_rho":
+        return 18 * slots + 12 * hits
+    if kernel == "build":
+        return 9 * 464 * n
+    return None
+
+
 # ---------------------------------------------------------------- CPU reference
 def cpu_reference(n, target, steps=1):
     """The unmodified reference (oracle/_ref) on all host threads; every stage timed."""
@@ -195,19 +216,23 @@ def cpu_reference(n, target, steps=1):
 
 
 def run_reference(args, ws, rank):
+    """The unmodified reference on the host cores, on the SAME workload as the b200 arm
+    (C2: 2^26 particles per GPU, build + density + LJ). One full-size step takes about two
+    minutes on 16 threads, so the arm times ONE step after a small warm-up sample (page-in
+    of the library and the thread pool); --ref-n overrides the size."""
     if rank != 0:
         return
-    n = args.cpu_sample
+    n = args.ref_n or args.n
     t0 = time.time()
-    for _ in range(args.warmup if args.warmup < 2 else 1):
-        cpu_reference(n, args.target, 1)
-    res = cpu_reference(n, args.target, max(1, min(args.steps, 3)))
+    if args.warmup:
+        cpu_reference(min(n, 1 << 18), args.target, 1)
+    res = cpu_reference(n, args.target, 1)
     out = {"metric": METRIC, "value": res["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-           "steps": max(1, min(args.steps, 3)), "warmup": args.warmup, "ms_per_step": res["value"] * n / 1e6,
+           "steps": 1, "warmup": args.warmup, "ms_per_step": res["value"] * n / 1e6,
            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (reference make_uniform, seed 42)",
            "config": {"workload": "C2 uniform periodic, 200 nbrs, 8x8 gather compressed, build+density+LJ",
-                      "n_per_gpu": args.n, "sample_n": n},
+                      "n_per_gpu": args.n, "sample_n": n, "same_config": n == args.n},
            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")},
            "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "stages_ms": res["stages_ms"], "wall_s": round(time.time() - t0, 1)}
@@ -263,7 +288,17 @@ def run_b200(args, ws, rank, local):
     for k in kernels:
         ctx.reduce(k, pipe.cfg, n, download=False)
         stage["pass_" + k.names[0]] = ctx.stage_times()["pass"]
+    # fp64 (bit-exact, = reduce<double>) passes over the same store, for the secondary line
+    if not args.no_f64:
+        for k in kernels:
+            ctx.reduce(k, S.PassConfig(1.0, S.F64), n, download=False)
+            stage["f64_" + k.names[0]] = ctx.stage_times()["pass"]
     ctx.set_timing(False)
+    # work counters of this store for the FP32 lane-op roofline: pair slots (cluster_overhead
+    # numerator, bench.cpp:93-122) and in-range pairs (sum of LJ neighbour counts)
+    slots = ctx.cluster_slots()
+    ctx.reduce(kernels[1], pipe.cfg, n, download=False)
+    hits = int(ctx.device_array("count", torch.int32, n).to(torch.int64).sum().item())
 
     barrier(ws)
     ctx.synchronize()
@@ -305,6 +340,7 @@ def run_b200(args, ws, rank, local):
 
     bpp = (pipe.blob_bytes + 4 * pipe.num_sc + 8 * (pipe.num_sc + 1)) / n
     pk, pk_kind = peaks()
+    stage_mixed = {k: v for k, v in stage.items() if not k.startswith("f64_")}
     # dominant kernel + its algorithmic bytes
     algo_bytes = {
         "build": 32 + 8 + 3.77,            # sorted x,y,z,h read + node/cluster geo (amortised) + store write
@@ -312,17 +348,25 @@ def run_b200(args, ws, rank, local):
         "pass_fx": 32 + 3.77 + 36,         # i x,y,z,h + list + 4 outputs + count written
         "sort": 24 * ((3 * 21 + 7) // 8),
     }
-    dom = max(stage, key=lambda k: stage[k])
-    dom_ms = stage[dom]
+    dom = max(stage_mixed, key=lambda k: stage_mixed[k])
+    dom_ms = stage_mixed[dom]
     ab = algo_bytes.get(dom, 48.0) * n
     achieved = ab / (dom_ms * 1e-3) / 1e9
-    traffic, pipe_util = None, None
-    try:  # DRAM bytes of the same kernel from the committed ncu capture of this workload
-        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
+    # FP32 lane-op roofline of the dominant kernel: algorithmic lane-ops per
+    # launch from this store's own work counters, over the measured launch time; peak = every
+    # FP32 lane of the part busy every cycle (148 SMs x 128 lanes x max SM clock)
+    ops = lane_ops(dom, slots, hits, n)
+    sm_mhz = pk.get("sm_max_mhz", 1965.0)
+    peak_t = 148 * 128 * sm_mhz * 1e6 / 1e12
+    achieved_t = ops / (dom_ms * 1e-3) / 1e12 if ops else None
+    traffic, pipe_util, cap = None, None, None
+    try:  # DRAM bytes and pipe utilisation of the same kernel from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "r02", "traffic.json")) as f:
             tj = json.load(f)
         if int(tj["n"]) == n:
             traffic = tj["dram_bytes_per_launch"].get(dom)
-            pipe_util = tj["pipe_util_pct_8m"].get(dom)
+            pipe_util = tj["pipe_util_pct"].get(dom)
+            cap = tj.get("capture")
     except (OSError, KeyError, ValueError):
         pass
     out = {
@@ -342,13 +386,23 @@ def run_b200(args, ws, rank, local):
                         "store + pass outputs, overlapped with the neighbouring steps' device work",
                 "serialised_ms_per_step": round(e2e_sync, 2)},
         "gpu_launches": int(launches),
-        "stages_ms": {k: round(v, 3) for k, v in stage.items()},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
-                     "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
-                     "peak_kind": pk_kind, "pipe_util_pct": pipe_util,
-                     "note": "pass/build are FP32-pipe/latency bound (SURVEY §8(d)): the HBM fraction is per the "
-                             "schema; pipe_util_pct = ncu FMA/ALU pipe and issue utilisation of this kernel"},
-        "roofline_composite": composite_roofline(stage, n, pk, ms_max),
+        "stages_ms": {k: round(v, 3) for k, v in stage_mixed.items()},
+        "f64": ({"ms_per_step": round(ms_max - stage["pass_rho"] - stage["pass_fx"] + stage["f64_rho"] + stage["f64_fx"], 3),
+                 "pass_rho_ms": round(stage["f64_rho"], 3), "pass_fx_ms": round(stage["f64_fx"], 3),
+                 "note": "same step with the bit-exact fp64 passes (= reduce<double>) instead of the mixed ones"}
+                if "f64_rho" in stage else None),
+        "roofline": {"bound": "fp32", "kernel": dom,
+                     "achieved": round(achieved_t, 3) if achieved_t else None, "peak": round(peak_t, 2),
+                     "unit": "TFLOP/s", "frac": round(achieved_t / peak_t, 4) if achieved_t else None,
+                     "traffic": traffic, "traffic_capture": cap, "pipe_util_pct": pipe_util,
+                     "work": {"pair_slots": int(slots), "in_range_pairs": hits, "lane_ops": ops,
+                              "model": LANE_OP_MODEL.get(dom)},
+                     "note": "FP32 lane-ops (one per FADD/FMUL/FFMA lane), peak = 148 SMs x 128 FP32 lanes x max SM "
+                             "clock; the build and passes are FP32-issue bound (SURVEY §8(d))",
+                     "hbm": {"achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                             "frac": round(achieved / pk["hbm_gbs"], 4), "peak_kind": pk_kind,
+                             "algorithmic_bytes_per_particle": algo_bytes.get(dom)}},
+        "roofline_composite": composite_roofline(stage_mixed, n, pk, ms_max),
         "clocks": clk.summary(),
     }
     if rank == 0 and not args.no_cpu_baseline:

@@ -287,8 +287,9 @@ __global__ void __launch_bounds__(kExactThreads) k_pass_exact(const __grid_const
     }
 }
 
-// One SC of the fp64 reference-order pass; threads >= 64 only take part in the
-// block barriers (the fast kernel uses this for SCs it cannot handle safely).
+// One SC of the fp64 reference-order pass for gather stores of any cluster shape
+// (symmetric stores take pass_sym.cuh);
+// threads >= 64 only take part in the block barriers.
 template <int K>
 __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& st, uint32_t* s_idx,
                          unsigned long long* s_msk, int* s_len) {
@@ -314,12 +315,9 @@ __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& 
                 const uint64_t jb = uint64_t(s_idx[e]) * A.cj, je = tmin<uint64_t>(jb + A.cj, A.n);
                 for (uint64_t j = jb; j < je; ++j) {
                     if (i == j) continue;
-                    if (A.symmetric && i > j && uint64_t(A.ci) * (j / A.ci) <= uint64_t(A.cj) * (i / A.cj)) continue;
                     double dx, dy, dz;
                     const double d2 = pair_d2_exact(xi, yi, zi, A.x[j], A.y[j], A.z[j], A.box, &dx, &dy, &dz);
-                    double rr = r;
-                    if (A.symmetric) rr = dmul(A.qs, smax(hi, A.h[j]));
-                    if (d2 > dmul(rr, rr)) continue;
+                    if (d2 > dmul(r, r)) continue;
                     double v[4];
                     if (eval_exact<K>(A, i, j, d2, dx, dy, dz, hi, v)) {
                         coincident = true;
@@ -328,25 +326,14 @@ __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& 
 #pragma unroll
                     for (int o = 0; o < NO; ++o) acc[o] = dadd(acc[o], v[o]);
                     ++cnt;
-                    if (A.symmetric) {
-#pragma unroll
-                        for (int o = 0; o < NO; ++o) atomicAdd(A.out[o] + j, (NO == 4 && o < 3) ? -v[o] : v[o]);
-                        atomicAdd(A.cnt + j, 1u);
-                    }
                 }
             }
         }
         if (coincident) raise_error(A.err, sc, SFCNL_INPUT_ERROR, kMsgCoincident, 0);
         if (active) {
-            if (A.symmetric) {
 #pragma unroll
-                for (int o = 0; o < NO; ++o) atomicAdd(A.out[o] + i, acc[o]);
-                atomicAdd(A.cnt + i, cnt);
-            } else {
-#pragma unroll
-                for (int o = 0; o < NO; ++o) A.out[o][i] = acc[o];
-                A.cnt[i] = cnt;
-            }
+            for (int o = 0; o < NO; ++o) A.out[o][i] = acc[o];
+            A.cnt[i] = cnt;
         }
     }
 }
