@@ -266,6 +266,71 @@ int sfcnl_cu_sym_range_entries(sfcnl_cu_ctx* ctx, const sfcnl_pass_params* param
 int sfcnl_cu_sym_range_final(sfcnl_cu_ctx* ctx, const sfcnl_pass_params* params, uint64_t num_remote,
                              const double* jacc, const uint32_t* jcnt, const uint32_t* ejcl,
                              const uint32_t* esc, double* const* outs, uint32_t* neighbor_count);
+/* ---- (6b) O(N/P) decomposition: local index space, distributed octree ---------
+ * Per rank memory proportional to its own particles plus its halo:
+ *   key_hist          radix-select splitter: for each of nq boundaries, the number of
+ *                     LOCAL sorted keys (the current SfcOrder) in each of the 65536
+ *                     buckets [prefix[q] + b << shift, prefix[q] + (b + 1) << shift);
+ *                     hist is a DEVICE int64 array of nq x 65536 (sum it over ranks).
+ *   merge_runs        owner placement: the n received rows are nruns runs (host
+ *                     run_bounds[nruns + 1]), each sorted by (key, global id); rows are
+ *                     written to out in (key, run) order = the global stable order.
+ *                     cols / out: HOST arrays of ncols DEVICE column pointers.
+ *   build_octree_dist build_octree (octree.cpp:9-59) of the GLOBAL key multiset whose
+ *                     local part is the current SfcOrder: per level the child bounds
+ *                     (local lower bounds) are summed over ranks by fn (in-place SUM of
+ *                     count u32 on the device, on the context's stream). Identical node
+ *                     arrays on every rank (reference numbering), global particle ranges.
+ *   leaf_boxes        per node (6 doubles lo[3], hi[3], DEVICE num_nodes x 6): the box of
+ *                     the rank's particles of every LEAF overlapping [p_begin, p_end)
+ *                     (x/y/z: DEVICE owned columns, element g - p_begin); other nodes empty.
+ *   domain_boxes      the boxes of nbox equal chunks of the owned particles (nbox x 6).
+ *   halo_select       owner side of the halo: flags[q * n_owned_clusters + k] = 1 when
+ *                     owned cluster k (cj particles from p_begin) overlaps a leaf whose
+ *                     box is within `reach` (periodic aabb_dist_sq) of one of rank q's
+ *                     nbox domain boxes (DEVICE nranks x nbox x 6); the rank's own row is
+ *                     left zero. Conservative: every leaf any super-cluster of rank q can
+ *                     accept (collect_candidates, neighbor_build.cpp:43-65) is selected.
+ *   pack_clusters     rows (DEVICE, nclusters*cj x ncols, row-major) of the listed owned
+ *                     clusters (global ids) from the owned columns; tail slots past p_end
+ *                     are NaN.
+ *   dd_place          local index space: the sorted slot (alloc_sorted(n_local)) receives
+ *                     the owned columns and the halo rows at local cluster lpos[c] (DEVICE
+ *                     u32 per global cluster); padding clusters (lc2g == ~0) are NaN.
+ *                     Also writes lc2g (local cluster -> global cluster).
+ *   dd_localize       the global octree's particle ranges mapped to the local index space
+ *                     (g -> lpos[g / cj] * cj + (present ? g % cj : 0)), and the maps that
+ *                     the range build (local clusters -> global ids in the encoded list)
+ *                     and the passes (decoded global ids -> local clusters) use.
+ *   dd_lc2g           lc2g[lpos[c]] = c for every present global cluster c, ~0 elsewhere.
+ *   dd_clear          back to the single-domain index space. */
+typedef int (*sfcnl_allreduce_u32)(void* user, uint32_t* device_data, uint64_t count);
+int sfcnl_cu_key_hist(sfcnl_cu_ctx* ctx, uint32_t nq, const uint64_t* prefix, int shift, int64_t* hist);
+int sfcnl_cu_merge_runs(sfcnl_cu_ctx* ctx, uint64_t n, uint32_t ncols, const double* const* cols,
+                        const uint64_t* keys, uint32_t nruns, const uint64_t* run_bounds, double* const* out);
+int sfcnl_cu_build_octree_dist(sfcnl_cu_ctx* ctx, uint32_t bucket, uint64_t n_global, sfcnl_allreduce_u32 fn,
+                               void* user, uint64_t* num_nodes);
+int sfcnl_cu_leaf_boxes(sfcnl_cu_ctx* ctx, uint64_t p_begin, uint64_t p_end, const double* x, const double* y,
+                        const double* z, double* boxes);
+int sfcnl_cu_domain_boxes(sfcnl_cu_ctx* ctx, uint64_t n_owned, const double* x, const double* y, const double* z,
+                          uint32_t nbox, double* boxes);
+int sfcnl_cu_halo_select(sfcnl_cu_ctx* ctx, uint64_t p_begin, uint64_t p_end, uint32_t cj,
+                         const double* leaf_boxes, uint32_t nranks, uint32_t self_rank, uint32_t nbox,
+                         const double* domain_boxes, double reach, uint8_t* flags);
+int sfcnl_cu_pack_clusters(sfcnl_cu_ctx* ctx, uint64_t p_begin, uint64_t p_end, uint32_t cj,
+                           const uint32_t* clusters, uint64_t nclusters, uint32_t ncols,
+                           const double* const* cols, double* rows);
+int sfcnl_cu_dd_place(sfcnl_cu_ctx* ctx, uint64_t n_global, uint64_t p_begin, uint64_t p_end, uint32_t cj,
+                      const uint32_t* lpos, uint64_t n_local, uint32_t ncols, const double* const* owned_cols,
+                      const uint32_t* halo_clusters, uint64_t nhalo, const double* halo_rows, uint32_t* lc2g);
+int sfcnl_cu_dd_localize(sfcnl_cu_ctx* ctx, uint32_t cj, const uint32_t* lpos, const uint8_t* present,
+                         uint64_t n_global_clusters, const uint32_t* lc2g);
+int sfcnl_cu_dd_lc2g(sfcnl_cu_ctx* ctx, uint64_t n_global_clusters, const uint32_t* lpos, const uint8_t* present,
+                     uint32_t* lc2g, uint64_t n_local_clusters);
+int sfcnl_cu_dd_clear(sfcnl_cu_ctx* ctx);
+/* Device bytes currently allocated by the context (every internal buffer). */
+int sfcnl_cu_memory_bytes(sfcnl_cu_ctx* ctx, uint64_t* bytes);
+
 /* Device pointer + byte length of an internal array for zero-copy collectives:
  * "x","y","z","h", sorted fields by name, "keys","perm","nodes","node_geo",
  * "halo_flags","out0".."out3","count", the input slot "orig.x".."orig.h" and

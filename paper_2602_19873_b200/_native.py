@@ -84,8 +84,13 @@ EXPORTS = [
     "sfcnl_cu_node_geometry_range", "sfcnl_cu_halo_mark", "sfcnl_cu_device_array",
     "sfcnl_cu_set_particle_records", "sfcnl_cu_build_full_list", "sfcnl_cu_get_full_list",
     "sfcnl_cu_set_full_list", "sfcnl_cu_reduce_full", "sfcnl_cu_cluster_slots", "sfcnl_cu_sym_range_entries",
-    "sfcnl_cu_sym_range_final",
+    "sfcnl_cu_sym_range_final", "sfcnl_cu_key_hist", "sfcnl_cu_merge_runs", "sfcnl_cu_build_octree_dist",
+    "sfcnl_cu_leaf_boxes", "sfcnl_cu_domain_boxes", "sfcnl_cu_halo_select", "sfcnl_cu_pack_clusters",
+    "sfcnl_cu_dd_place", "sfcnl_cu_dd_localize", "sfcnl_cu_dd_lc2g", "sfcnl_cu_dd_clear", "sfcnl_cu_memory_bytes",
 ]
+
+# int (*)(void* user, uint32_t* device_data, uint64_t count): in-place SUM over ranks
+ALLREDUCE_U32 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64)
 
 _lib = None
 
@@ -153,6 +158,18 @@ def lib():
         "sfcnl_cu_cluster_slots": (C.c_int, [P, C.POINTER(u64)]),
         "sfcnl_cu_sym_range_entries": (C.c_int, [P, C.POINTER(PassParamsC), C.POINTER(u64)]),
         "sfcnl_cu_sym_range_final": (C.c_int, [P, C.POINTER(PassParamsC), u64, P, P, P, P, C.POINTER(P), P]),
+        "sfcnl_cu_key_hist": (C.c_int, [P, u32, P, C.c_int, P]),
+        "sfcnl_cu_merge_runs": (C.c_int, [P, u64, u32, C.POINTER(P), P, u32, C.POINTER(u64), C.POINTER(P)]),
+        "sfcnl_cu_build_octree_dist": (C.c_int, [P, u32, u64, ALLREDUCE_U32, P, C.POINTER(u64)]),
+        "sfcnl_cu_leaf_boxes": (C.c_int, [P, u64, u64, P, P, P, P]),
+        "sfcnl_cu_domain_boxes": (C.c_int, [P, u64, P, P, P, u32, P]),
+        "sfcnl_cu_halo_select": (C.c_int, [P, u64, u64, u32, P, u32, u32, u32, P, C.c_double, P]),
+        "sfcnl_cu_pack_clusters": (C.c_int, [P, u64, u64, u32, P, u64, u32, C.POINTER(P), P]),
+        "sfcnl_cu_dd_place": (C.c_int, [P, u64, u64, u64, u32, P, u64, u32, C.POINTER(P), P, u64, P, P]),
+        "sfcnl_cu_dd_localize": (C.c_int, [P, u32, P, P, u64, P]),
+        "sfcnl_cu_dd_lc2g": (C.c_int, [P, u64, P, P, P, u64]),
+        "sfcnl_cu_dd_clear": (C.c_int, [P]),
+        "sfcnl_cu_memory_bytes": (C.c_int, [P, C.POINTER(u64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -67,6 +67,7 @@ struct BuildArgs {
     uint32_t* leaf_cache;      // accepted leaves per SC of [sc_lo, ...) (halo_mark -> range build), or null
     uint32_t* leaf_count;      // their number per SC (~0u: not cached)
     uint64_t leaf_sc0;         // first SC of the cache
+    const uint32_t* lc2g;      // domain decomposition (dd.cu): local cluster -> global id of the encoded list, or null
     DevError* err;
 };
 
@@ -304,7 +305,7 @@ __device__ bool build_sc(const BuildArgs& A, const Workspace& W, uint64_t sc) {
         const unsigned long long mk = keep ? W.cmask[k] : 0;
         uint32_t tot;
         const uint32_t ex = block_excl_scan(keep ? 1u : 0u, scratch, &tot);
-        if (keep) W.cand[nE + ex] = jc, W.cmask[nE + ex] = mk;
+        if (keep) W.cand[nE + ex] = A.lc2g ? A.lc2g[jc] : jc, W.cmask[nE + ex] = mk;
         nE += tot;
         __syncthreads();
     }
@@ -663,7 +664,8 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
     SFCNL_CUDA_TRY(c->overflow_list.reserve(num_sc * 8));  // main-tier list, then medium-tier list
     uint64_t scratch_cap = std::max<uint64_t>(c->scratch.bytes, (p_hi - p_lo) * 16 + (1 << 20));
 
-    BuildArgs A;
+    BuildArgs A{};
+    A.lc2g = c->dd_lc2g;
     A.n = n;
     A.box = box;
     A.scale = p.build_radius_scale;

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kBwWarps * 32, 4) k_build_p1(const __grid_cons
             const unsigned kb = __ballot_sync(0xffffffffu, keep);
             if (keep) {
                 const uint32_t at = nE + __popc(kb & lanemask_lt());
-                tidx[at] = cand, tmsk[at] = mask;
+                tidx[at] = A.lc2g ? A.lc2g[cand] : cand, tmsk[at] = mask;
             }
             nE += __popc(kb);
         }

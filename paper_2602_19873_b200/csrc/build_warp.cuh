@@ -561,7 +561,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
         if (nE + __popc(kb) > Sm::kE) return false;
         if (keep) {
             const uint32_t at = nE + __popc(kb & lanemask_lt());
-            S.eidx[at] = cand, S.emsk[at] = uint8_t(mask);
+            S.eidx[at] = A.lc2g ? A.lc2g[cand] : cand, S.emsk[at] = uint8_t(mask);
         }
         nE += __popc(kb);
         __syncwarp();  // staging consumed

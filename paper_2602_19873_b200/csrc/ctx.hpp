@@ -12,6 +12,9 @@
 
 namespace sfcnl_cu {
 
+// Device bytes held by every DBuf of the process (sfcnl_cu_memory_bytes).
+uint64_t& dbuf_total_bytes();
+
 // Grow-only device allocation: the hot path reuses buffers across steps.
 struct DBuf {
     void* p = nullptr;
@@ -30,7 +33,7 @@ struct DBuf {
     }
     ~DBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFree(p), dbuf_total_bytes() -= bytes;
         p = nullptr;
         bytes = 0;
     }
@@ -39,7 +42,7 @@ struct DBuf {
         release();
         const size_t want = b ? b : 16;
         cudaError_t e = cudaMalloc(&p, want);
-        if (e == cudaSuccess) bytes = want;
+        if (e == cudaSuccess) bytes = want, dbuf_total_bytes() += want;
         else p = nullptr;
         return e;
     }
@@ -103,6 +106,7 @@ struct sfcnl_cu_ctx {
     // level-synchronous construction scratch, one entry per depth
     struct Level {
         sfcnl_cu::DBuf kf, pb, pe, flag, ipos, ikeys, irank;
+        sfcnl_cu::DBuf g;  // distributed build: global particle ranges [pb | pe] (all-reduced local bounds)
         uint64_t count = 0, internal = 0;
     };
     std::vector<Level> levels;
@@ -145,6 +149,12 @@ struct sfcnl_cu_ctx {
     int sym_e_kernel = -1;  // + fp64 j-side sums of the deferred special slots  // symmetric mixed density: per-particle error-bound weights (+ flag counter)
     uint64_t last_redo = 0;  // particles / SCs handed to fp64 by the last mixed pass's error bound  // [8]: deferred special-slot queues of the symmetric fast pass
 
+    // O(N/P) domain decomposition (dd.cu): local cluster -> global id (encoder) and
+    // global -> local cluster (pass decoders), caller-owned device arrays; null = off
+    const uint32_t* dd_lc2g = nullptr;
+    const uint32_t* dd_g2l = nullptr;
+    sfcnl_cu::DBuf dd_tab;  // device pointer tables / small scratch of the dd kernels
+
     // errors
     sfcnl_cu::DBuf derr;  // DevError
     sfcnl_cu::DBuf ptrs;  // small pointer tables
@@ -176,7 +186,16 @@ void stage_end(sfcnl_cu_ctx* c, Stage s);
 // Kernel drivers (each in its own .cu).
 int run_sort_by_sfc(sfcnl_cu_ctx* c, int bits);
 int run_apply_order(sfcnl_cu_ctx* c, int64_t into = -1);  // into >= 0: gather into sorted[into..]
-int run_build_octree(sfcnl_cu_ctx* c, uint32_t bucket);
+// Distributed octree (domain decomposition): every rank holds a disjoint part of the
+// global key multiset in c->keys (sorted); a node's global particle bound is the sum over
+// ranks of the local lower bounds, so each level's child bounds are all-reduced (SUM) by
+// the caller's collective and the result is the single-domain tree on every rank.
+struct DistTree {
+    uint64_t n_global;
+    sfcnl_allreduce_u32 fn;  // in-place SUM over ranks of `count` u32 on the device
+    void* user;
+};
+int run_build_octree(sfcnl_cu_ctx* c, uint32_t bucket, const DistTree* dt = nullptr);
 int run_tree_levels_from_nodes(sfcnl_cu_ctx* c, const std::vector<uint8_t>& depth);
 int run_node_geometry(sfcnl_cu_ctx* c, uint64_t p0 = 0, uint64_t p1 = ~0ull);  // leaves clip to [p0, p1)
 // clusters overlapping particles [p0, p1), plus j-clusters flagged in jflags (if non-null)

@@ -173,10 +173,12 @@ inline unsigned blocks_for(uint64_t m, int t = 256) { return unsigned((m + t - 1
 
 }  // namespace
 
-int run_build_octree(sfcnl_cu_ctx* c, uint32_t bucket) {
+int run_build_octree(sfcnl_cu_ctx* c, uint32_t bucket, const DistTree* dt) {
     if (bucket < 1) return set_error(c, 1, "build_octree: bucket_size must be >= 1");
     if (!c->has_order) return set_error(c, 1, "build_octree: no SFC order");
     const uint64_t n = c->order_n;
+    const uint64_t n_tree = dt ? dt->n_global : n;
+    if (n_tree > 0xffffffffull) return set_error(c, 1, "build_octree: more than 2^32 - 1 particles");
     const int bits = c->bits;
     stage_begin(c, kOctree);
     auto& L = c->levels;
@@ -187,6 +189,15 @@ int run_build_octree(sfcnl_cu_ctx* c, uint32_t bucket) {
     launch(c, k_root, dim3(1), dim3(1), 0, L[0].kf.as<uint64_t>(), L[0].pb.as<uint32_t>(),
            L[0].pe.as<uint32_t>(), uint32_t(n));
     L[0].count = 1;
+    // global ranges of a level: the local ones (distributed: [pb | pe] all-reduced)
+    auto gpb = [&](int d) { return dt ? L[d].g.as<uint32_t>() : L[d].pb.as<uint32_t>(); };
+    auto gpe = [&](int d) { return dt ? L[d].g.as<uint32_t>() + L[d].count : L[d].pe.as<uint32_t>(); };
+    if (dt) {
+        const uint32_t root[2] = {0u, uint32_t(n_tree)};
+        SFCNL_CUDA_TRY(L[0].g.reserve(8));
+        SFCNL_CUDA_TRY(cudaMemcpyAsync(L[0].g.p, root, 8, cudaMemcpyHostToDevice, c->stream));
+        SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    }
     int nlev = 0;
     uint64_t internal_total = 0;
     SFCNL_CUDA_TRY(c->small_host_dev.reserve(64));
@@ -195,8 +206,8 @@ int run_build_octree(sfcnl_cu_ctx* c, uint32_t bucket) {
         const uint64_t m = lv.count;
         SFCNL_CUDA_TRY(lv.flag.reserve(m * 4));
         SFCNL_CUDA_TRY(lv.ipos.reserve((m + 1) * 4));
-        launch(c, k_flags, dim3(blocks_for(m)), dim3(256), 0, (const uint32_t*)lv.pb.as<uint32_t>(),
-               (const uint32_t*)lv.pe.as<uint32_t>(), m, bucket, int(d < bits), lv.flag.as<uint32_t>());
+        launch(c, k_flags, dim3(blocks_for(m)), dim3(256), 0, (const uint32_t*)gpb(d),
+               (const uint32_t*)gpe(d), m, bucket, int(d < bits), lv.flag.as<uint32_t>());
         {
             const int rc = excl_scan(c, lv.flag.as<uint32_t>(), lv.ipos.as<uint32_t>(), m);
             if (rc) return rc;
@@ -222,6 +233,16 @@ int run_build_octree(sfcnl_cu_ctx* c, uint32_t bucket) {
                (const uint32_t*)cur.ipos.as<uint32_t>(), (const uint64_t*)c->keys.as<uint64_t>(),
                cur.ikeys.as<uint64_t>(), nx.kf.as<uint64_t>(), nx.pb.as<uint32_t>(), nx.pe.as<uint32_t>());
         SFCNL_CUDA_TRY(cudaGetLastError());
+        if (dt) {  // global child bounds = SUM over ranks of the local lower bounds
+            const uint64_t cnt = nx.count;
+            SFCNL_CUDA_TRY(nx.g.reserve(cnt * 8));
+            SFCNL_CUDA_TRY(cudaMemcpyAsync(nx.g.p, nx.pb.p, cnt * 4, cudaMemcpyDeviceToDevice, c->stream));
+            SFCNL_CUDA_TRY(cudaMemcpyAsync(nx.g.as<uint32_t>() + cnt, nx.pe.p, cnt * 4, cudaMemcpyDeviceToDevice,
+                                           c->stream));
+            SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+            if (dt->fn(dt->user, nx.g.as<uint32_t>(), cnt * 2))
+                return set_error(c, SFCNL_CUDA_ERROR, "build_octree: all-reduce callback failed");
+        }
     }
     // DFS-preorder ranks of internal nodes.
     std::vector<LevelRef> refs(nlev);
@@ -242,8 +263,8 @@ int run_build_octree(sfcnl_cu_ctx* c, uint32_t bucket) {
     for (int d = 0; d < nlev; ++d) c->level_off[d + 1] = c->level_off[d] + L[d].count;
     for (int d = 0; d < nlev; ++d) {
         launch(c, k_write_nodes, dim3(blocks_for(L[d].count)), dim3(256), 0, d, bits, L[d].count,
-               (const uint64_t*)L[d].kf.as<uint64_t>(), (const uint32_t*)L[d].pb.as<uint32_t>(),
-               (const uint32_t*)L[d].pe.as<uint32_t>(), (const uint32_t*)L[d].flag.as<uint32_t>(),
+               (const uint64_t*)L[d].kf.as<uint64_t>(), (const uint32_t*)gpb(d),
+               (const uint32_t*)gpe(d), (const uint32_t*)L[d].flag.as<uint32_t>(),
                (const uint32_t*)L[d].ipos.as<uint32_t>(), (const uint32_t*)L[d].irank.as<uint32_t>(),
                (const uint32_t*)(d ? L[d - 1].irank.as<uint32_t>() : nullptr), c->nodes.as<Node>(),
                c->level_nodes.as<uint32_t>() + c->level_off[d]);
@@ -252,7 +273,7 @@ int run_build_octree(sfcnl_cu_ctx* c, uint32_t bucket) {
     stage_end(c, kOctree);
     c->num_nodes = total;
     c->tree_bits = bits;
-    c->tree_n = n;
+    c->tree_n = n_tree;
     c->has_tree = true;
     drop_external(c);
     return 0;

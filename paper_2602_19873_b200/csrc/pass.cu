@@ -71,6 +71,7 @@ struct PassArgs {
     const unsigned* frame_xcl;  // per j-cluster max |offset| (float bits)
     double* out[4];
     uint32_t* cnt;
+    const uint32_t* g2l;  // domain decomposition (dd.cu): decoded global cluster id -> local, or null
     DevError* err;
 };
 
@@ -213,6 +214,8 @@ __device__ int next_block(const PassArgs& A, uint64_t sc, ScStream& s, uint32_t 
                 idx[k] = uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16) | (uint32_t(p[3]) << 24);
             }
         }
+        if (A.g2l && result > 0)  // same lane -> element mapping as the decode: no barrier
+            for (uint32_t k = threadIdx.x; k < len; k += 32) idx[k] = A.g2l[idx[k]];
         for (uint32_t k = threadIdx.x; k < len; k += 32) {
             unsigned long long mv = 0;
             const uint8_t* r = s.rec + uint64_t(first + k) * A.mask_bytes;
@@ -599,6 +602,7 @@ int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p) {
     for (int o = 0; o < 4; ++o) A.out[o] = c->outs[o].as<double>() - p0;
     A.cnt = c->ncount.as<uint32_t>() - p0;
     A.err = c->derr.as<DevError>();
+    A.g2l = c->dd_g2l;
     stage_begin(c, kPass);
     if (symmetric) {
         const bool sym_fast = p.precision == 1 && c->sp.ci == 8 && (c->sp.cj == 8 || c->sp.cj == 4) &&
@@ -826,7 +830,7 @@ int sym_range_args(sfcnl_cu_ctx* c, const sfcnl_pass_params& p, PassArgs& A, con
 }  // namespace
 
 int run_sym_range_entries(sfcnl_cu_ctx* c, const sfcnl_pass_params& p, uint64_t* num_e) {
-    PassArgs A;
+    PassArgs A{};
     if (int rc = sym_range_args(c, p, A, "sym_range_entries")) return rc;
     const int no = p.kernel >= 2 ? 4 : 1;
     uint64_t ne = 0;
@@ -870,7 +874,7 @@ int run_sym_range_entries(sfcnl_cu_ctx* c, const sfcnl_pass_params& p, uint64_t*
 
 int run_sym_range_final(sfcnl_cu_ctx* c, const sfcnl_pass_params& p, uint64_t nr, const double* rjacc,
                         const uint32_t* rjcnt, const uint32_t* rejcl, const uint32_t* resc) {
-    PassArgs A;
+    PassArgs A{};
     if (int rc = sym_range_args(c, p, A, "sym_range_final")) return rc;
     if (c->sym_e_kernel != p.kernel) return set_error(c, 1, "sym_range_final: run sym_range_entries for this kernel first");
     const int no = p.kernel >= 2 ? 4 : 1;

@@ -201,6 +201,8 @@ __global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : 5) k_pass_i
                     S.idx[k] = uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16) | (uint32_t(p[3]) << 24);
                 }
             }
+            if (A.g2l)  // domain decomposition: stored global ids -> local clusters (same lanes as the decode)
+                for (uint32_t k = lane; k < len; k += 32) S.idx[k] = A.g2l[S.idx[k]];
             __syncwarp();
             for (uint32_t h0 = 0; h0 < len; h0 += 32) {
                 const uint32_t n = tmin<uint32_t>(32, len - h0);

@@ -183,6 +183,8 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                     S.idx[k] = uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16) | (uint32_t(p[3]) << 24);
                 }
             }
+            if (A.g2l)  // domain decomposition: stored global ids -> local clusters (same lanes as the decode)
+                for (uint32_t k = lane; k < len; k += 32) S.idx[k] = A.g2l[S.idx[k]];
             __syncwarp();
             for (uint32_t h0 = 0; h0 < len; h0 += kPwChunk) {
                 const uint32_t n = tmin<uint32_t>(kPwChunk, len - h0);

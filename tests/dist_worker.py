@@ -63,6 +63,9 @@ def main():
     rec = dict(p0=res.p_begin, p1=res.p_end, sc0=res.sc_begin, sc1=res.sc_end, n=res.n_total,
                num_nodes=res.num_nodes, halo=res.halo_particles, counts=res.store.counts,
                offsets=res.store.offsets, blob=res.store.blob)
+    t = getattr(E, "tree", None)
+    if t is not None:  # the rank's copy of the (distributed) global octree
+        rec.update(t_kf=t.key_first, t_kl=t.key_last, t_pb=t.pbegin, t_pe=t.pend, t_fc=t.first_child, t_d=t.depth)
     for k, rr in enumerate(res.results):
         for j, v in enumerate(rr.outputs):
             rec[f"k{k}_o{j}"] = v

@@ -61,6 +61,7 @@ def single_domain(cfg):
         gp = o.make_evrard(cfg["n"], cfg["target"], False, tuple(cfg["periodic"]), cfg["seed"])
     keys, perm, sp, tree, store = o.pipeline(gp, ci=cfg["ci"], cj=cfg["cj"], w=cfg["w"], mode=cfg.get("mode", 0),
                                              scale=cfg.get("scale", 1.0))
+    single_domain.tree = tree
     eps_sig = {"lj": (1.0, 0.05, 0.0), "lj_coulomb": (1.0, 0.05, 0.3)}
     outs = []
     for k in cfg["kernels"]:
@@ -94,6 +95,12 @@ def check(parts, cfg, exact=True):
             else:
                 assert np.allclose(got, ref, rtol=1e-5, atol=1e-5 * np.abs(ref).max()), (k, j)
     assert all(int(p["halo"]) > 0 for p in parts)
+    t = single_domain.tree
+    for p in parts:  # every rank holds the single-domain octree (distributed build)
+        if "t_kf" in p:
+            for a, b in (("t_kf", t.key_first), ("t_kl", t.key_last), ("t_pb", t.pbegin), ("t_pe", t.pend),
+                         ("t_fc", t.first_child), ("t_d", t.depth)):
+                assert np.array_equal(p[a], b), a
 
 
 CPU_CASES = [
@@ -108,6 +115,13 @@ CPU_CASES = [
 def test_domain_decomposition_oracle_engine(tmp_path, world, case):
     cfg = dict(CPU_CASES[case], engine="oracle")
     check(launch(world, cfg, tmp_path), cfg)
+
+
+def test_domain_decomposition_legacy_orchestration(tmp_path, monkeypatch):
+    """The global-index orchestration (symmetric stores use it) on the oracle engine."""
+    monkeypatch.setenv("SFCNL_DD_LEGACY", "1")
+    cfg = dict(CPU_CASES[0], engine="oracle")
+    check(launch(2, cfg, tmp_path), cfg)
 
 
 GPU_CASES = [
