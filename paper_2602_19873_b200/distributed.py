@@ -298,6 +298,7 @@ class _CudaEngineLocal:
                                            int(hid.numel()), _ptr(rows), _ptr(lc2g)))
         self.ctx.check(L.sfcnl_cu_dd_localize(h, int(cj), _ptr(lpos), _ptr(present), ngc, _ptr(lc2g)))
         self._maps = (lpos, present, lc2g)  # the context keeps raw pointers to lpos / lc2g
+        self.owned = None  # placed: the staging columns are released
         self.n_local = n_local
         self.n_total = n_global
         return o_own
@@ -323,11 +324,15 @@ class CudaEngine(_CudaEngineLocal):
 
     # -- inputs: the rank's particles stay resident (device copies) across steps
     def upload(self, ps: ParticleSet):
+        """The rank's input particles into the context's input slot (device copies that stay
+        resident across steps; the staging tensors are released)."""
         torch = _torch()
         cols = [ps.x, ps.y, ps.z, ps.h] + [ps.field(k) for k in self.fields]
         with torch.cuda.stream(self.stream):
-            self.inp = [torch.from_numpy(np.ascontiguousarray(c)).to(self.device, non_blocking=True) for c in cols]
-        self.n_local = ps.size()
+            inp = [torch.from_numpy(np.ascontiguousarray(c)).to(self.device, non_blocking=True) for c in cols]
+            self.ctx.set_particles_device(ps.size(), inp, self.fields, self.box)
+            self.ctx.synchronize()
+        self.n_in = ps.size()
 
     def _cols(self, n):
         torch = _torch()
@@ -336,17 +341,16 @@ class CudaEngine(_CudaEngineLocal):
     # -- (1) local sort; returns sorted keys (int64)
     def local_sort(self):
         torch = _torch()
-        self.ctx.set_particles_device(self.n_local, self.inp, self.fields, self.box)
         self.ctx.sort(self.bits)
         self.ctx.apply_order()
-        return self.ctx.device_array("keys", torch.int64, self.n_local)
+        return self.ctx.device_array("keys", torch.int64, self.n_in)
 
     def payload(self):
         """Columns in local key order: x, y, z, h, fields, and the key's bits as a float64
         (one all-to-all per contiguous column: no row packing)."""
         torch = _torch()
-        keys = self.ctx.device_array("keys", torch.int64, self.n_local)
-        return self._cols(self.n_local) + [keys.view(torch.float64)]
+        keys = self.ctx.device_array("keys", torch.int64, self.n_in)
+        return self._cols(self.n_in) + [keys.view(torch.float64)]
 
     # -- (4) owner placement; returns the owned sorted keys
     def own(self, recv, n_total, p0, runs=None):

@@ -43,7 +43,7 @@ def main():
                             cfg.get("h_jitter", 0.0), cfg["seed"])
     else:
         gp = o.make_evrard(cfg["n"], cfg["target"], False, tuple(cfg["periodic"]), cfg["seed"])
-    b = shares(gp.n, world)
+    b = [gp.n * q // world for q in range(world + 1)] if cfg.get("even_shares") else shares(gp.n, world)
     idx = np.arange(b[rank], b[rank + 1])
     bp = sfcnl.BuildParams(sfcnl.ClusterParams(cfg["ci"], cfg["cj"], cfg["w"]), cfg.get("mode", sfcnl.GATHER),
                            bool(cfg.get("compress", 1)), cfg.get("scale", 1.0))
@@ -58,8 +58,35 @@ def main():
         ctx = sfcnl.Context(int(os.environ.get("LOCAL_RANK", "0")))
         E = CudaEngine(ctx, box, ["m", "q"])
         E.upload(sfcnl.ParticleSet(gp.x[idx], gp.y[idx], gp.z[idx], gp.h[idx], {"m": gp.m[idx], "q": gp.q[idx]}))
+    mem = {}
+    if cfg.get("measure_memory"):
+        # single-GPU footprint of the same step on the rank's own particles (own context)
+        c1 = sfcnl.Context(int(os.environ.get("LOCAL_RANK", "0")))
+        ps1 = sfcnl.ParticleSet(gp.x[idx], gp.y[idx], gp.z[idx], gp.h[idx], {"m": gp.m[idx], "q": gp.q[idx]})
+        pipe = sfcnl.Pipeline(c1, ps1, box, bp, kernels, pcfg)
+        pipe.upload()
+        pipe.run()
+        c1.synchronize()
+        mem["single"] = E.memory_bytes()  # every DBuf of the process: c1 (E's context is still empty)
+        c1.close()
+        del pipe, c1
+        mem["base"] = E.memory_bytes()
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats()
     dd = DomainDecomposition(E, Comm(), bp, kernels, pcfg)
-    res = dd.run(download=True)
+    res = dd.run(download=not cfg.get("measure_memory"))
+    if cfg.get("measure_memory"):
+        torch.cuda.synchronize()
+        mem["dd_ctx"] = E.memory_bytes() - mem["base"]
+        mem["dd_torch"] = torch.cuda.memory_allocated()
+        mem["dd_torch_peak"] = torch.cuda.max_memory_allocated()
+        mem["n_in"] = len(idx)
+        mem["n_local"] = E.n_local
+        mem["halo"] = res.halo_particles
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), **{k: np.array(v) for k, v in mem.items()})
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     rec = dict(p0=res.p_begin, p1=res.p_end, sc0=res.sc_begin, sc1=res.sc_end, n=res.n_total,
                num_nodes=res.num_nodes, halo=res.halo_particles, counts=res.store.counts,
                offsets=res.store.offsets, blob=res.store.blob)

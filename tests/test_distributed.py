@@ -190,3 +190,25 @@ def test_range_build_and_pass_slices_single_gpu():
             got = ctx.reduce(sfcnl.sph_density_kernel(), c, p1 - p0)
             assert np.array_equal(got.neighbor_count, r.neighbor_count[p0:p1])
             assert np.array_equal(got.outputs[0], r.outputs[0][p0:p1])
+
+
+@pytest.mark.gpu
+def test_domain_decomposition_memory_per_rank(tmp_path):
+    """O(N/P): at a simulated world of 8 (eight ranks sharing cuda:0), every rank's device
+    allocation for the build + density + LJ step -- its context's buffers plus the torch
+    tensors of the orchestration (owned columns, halo rows, index maps), steady state after
+    the step -- stays within 1.3x the single-GPU footprint of the same step on the rank's
+    own particles. The legacy orchestration allocated every global-index
+    array (48 B x N_total per rank) and the whole node geometry."""
+    cfg = dict(n=32 << 20, target=200, periodic=[1, 1, 1], seed=21, ci=8, cj=8, w=32, kernels=["density", "lj"],
+               engine="cuda", precision=1, measure_memory=True, even_shares=True)
+    parts = launch(8, cfg, tmp_path, timeout=1200)
+    ratios = []
+    for p in parts:
+        dd = int(p["dd_ctx"]) + int(p["dd_torch"])
+        ratios.append(dd / int(p["single"]))
+        print(f"rank single {int(p['single']) / 2**20:.0f} MiB dd {dd / 2**20:.0f} MiB "
+              f"(ctx {int(p['dd_ctx']) / 2**20:.0f} + torch {int(p['dd_torch']) / 2**20:.0f}, peak torch "
+              f"{int(p['dd_torch_peak']) / 2**20:.0f}) n_in {int(p['n_in'])} n_local {int(p['n_local'])} "
+              f"halo {int(p['halo'])}")
+    assert max(ratios) <= 1.3, ratios
