@@ -270,11 +270,6 @@ int run_build_octree(sfcnl_cu_ctx* c, uint32_t bucket, const DistTree* dt) {
                c->level_nodes.as<uint32_t>() + c->level_off[d]);
     }
     SFCNL_CUDA_TRY(cudaGetLastError());
-    if (dt) {  // a rank holds the global tree: drop the construction scratch (O(N_global / bucket))
-        SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
-        for (auto& lv : L)
-            for (DBuf* b : {&lv.kf, &lv.pb, &lv.pe, &lv.flag, &lv.ipos, &lv.ikeys, &lv.irank, &lv.g}) b->release();
-    }
     stage_end(c, kOctree);
     c->num_nodes = total;
     c->tree_bits = bits;

@@ -297,6 +297,8 @@ class _CudaEngineLocal:
                                            4 + len(self.fields), _ptr_array(self.owned), _ptr(hid32),
                                            int(hid.numel()), _ptr(rows), _ptr(lc2g)))
         self.ctx.check(L.sfcnl_cu_dd_localize(h, int(cj), _ptr(lpos), _ptr(present), ngc, _ptr(lc2g)))
+        if o_own == 0 and n_local == n_global:  # one rank: the local space is the global one
+            self.ctx.check(L.sfcnl_cu_dd_clear(h))
         self._maps = (lpos, present, lc2g)  # the context keeps raw pointers to lpos / lc2g
         self.owned = None  # placed: the staging columns are released
         self.n_local = n_local
