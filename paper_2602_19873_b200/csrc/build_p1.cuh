@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(kBwWarps * 32, 4) k_build_p1(const __grid_cons
                 if (valid) sx = float(rel(A.x[j], ox, 0)), sy = float(rel(A.y[j], oy, 1)), sz = float(rel(A.z[j], oz, 2));
                 const float Ej = warp_fmax(valid ? fmaxf(fabsf(sx), fmaxf(fabsf(sy), fabsf(sz))) : 0.f);
                 if (Ej > Ej_run) {  // thresholds for a running bound of the staged |coordinates|
+                    __syncwarp();      // every lane is done with the previous chunk's thresholds
                     Ej_run = fmaxf(Ej, Ej_run * 1.0625f);
                     const double ecoord = 5.9604644775390625e-08 * (double(Ei) + double(Ej_run));
 #pragma unroll

@@ -582,6 +582,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
 #pragma unroll
             for (int b = 0; b < 4; ++b) ebuf[mbytes + 4 * k + b] = uint8_t(v >> (8 * b));
         }
+        __syncwarp();  // the byte stores are read back as words by the copy-out below
         pos = mbytes + 4 * nE;
     } else {
         // nibble codec (nibble_codec.cpp:56-134): blocks of w differences

@@ -411,7 +411,7 @@ void launch_pass(sfcnl_cu_ctx* c, const PassArgs& A, bool fast) {
 int sym_transpose(sfcnl_cu_ctx* c, uint64_t num_e, uint64_t ncl, const uint32_t* ejcl) {
     auto &tcnt = c->sym[5], &tstart = c->sym[6], &tlist = c->sym[7];
     SFCNL_CUDA_TRY(tcnt.reserve((ncl + 1) * 4));
-    SFCNL_CUDA_TRY(tstart.reserve((ncl + 1) * 8));
+    SFCNL_CUDA_TRY(tstart.reserve((ncl + 2) * 8));  // scan of ncl + 1 counts: ncl + 2 entries
     SFCNL_CUDA_TRY(tlist.reserve(std::max<uint64_t>(num_e, 1) * 4));
     const unsigned grid_e = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((num_e + 255) / 256, uint64_t(c->num_sms) * 16)));
     SFCNL_CUDA_TRY(cudaMemsetAsync(tcnt.p, 0, (ncl + 1) * 4, c->stream));
@@ -660,7 +660,7 @@ int run_build_full_list(sfcnl_cu_ctx* c, double build_scale) {
     A.qs = build_scale;
     A.err = c->derr.as<DevError>();
     SFCNL_CUDA_TRY(c->full_cnt.reserve((n + 1) * 4));
-    SFCNL_CUDA_TRY(c->full_off.reserve((n + 1) * 8));
+    SFCNL_CUDA_TRY(c->full_off.reserve((n + 2) * 8));  // scan of n + 1 counts: n + 2 entries
     SFCNL_CUDA_TRY(cudaMemsetAsync(c->full_cnt.p, 0, (n + 1) * 4, c->stream));
     SFCNL_CUDA_TRY(cudaMemsetAsync(c->derr.p, 0xff, sizeof(DevError), c->stream));
     c->has_full = false;
