@@ -348,6 +348,7 @@ __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& 
 #include "pass_full.cuh"
 #include "pass_sym.cuh"
 #include "pass_symf.cuh"
+#include "pass_x64.cuh"
 
 template <int K, int CJ>
 void launch_pass_warp(sfcnl_cu_ctx* c, const PassArgs& A) {
@@ -388,6 +389,19 @@ void launch_pass_p1(sfcnl_cu_ctx* c, const PassArgs& A) {
     launch(c, k_pass_p1<K>, dim3(grid), dim3(kPiWarps * 32), smem, A, c->work_ctr.as<unsigned long long>());
 }
 
+template <int K, int CJ>
+void launch_pass_x64(sfcnl_cu_ctx* c, const PassArgs& A) {
+    const size_t smem = px_smem<K>();
+    cudaFuncSetAttribute(k_pass_x64<K, CJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass_x64<K, CJ>, kPxWarps * 32, smem);
+    const uint64_t warps = A.num_sc - A.sc_begin;
+    const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((warps + kPxWarps - 1) / kPxWarps,
+                                                                            uint64_t(c->num_sms) * std::max(per_sm, 1))));
+    cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream);
+    launch(c, k_pass_x64<K, CJ>, dim3(grid), dim3(kPxWarps * 32), smem, A, c->work_ctr.as<unsigned long long>());
+}
+
 template <int K>
 void launch_pass(sfcnl_cu_ctx* c, const PassArgs& A, bool fast) {
     if (fast && A.ci == 1) {  // point clusters (pass_p1.cuh)
@@ -401,6 +415,9 @@ void launch_pass(sfcnl_cu_ctx* c, const PassArgs& A, bool fast) {
     } else if (fast) {  // item-parallel layout (pass_item.cuh)
         if (A.cj == 8) launch_pass_item<K, 8>(c, A);
         else launch_pass_item<K, 4>(c, A);
+    } else if (A.ci == 8 && (A.cj == 8 || A.cj == 4) && !getenv("SFCNL_PASS_EXACT_V1")) {  // fp64, pass_x64.cuh
+        if (A.cj == 8) launch_pass_x64<K, 8>(c, A);
+        else launch_pass_x64<K, 4>(c, A);
     } else {
         const unsigned grid = unsigned(std::min<uint64_t>(A.num_sc - A.sc_begin, uint64_t(c->num_sms) * 32));
         launch(c, k_pass_exact<K>, dim3(grid), dim3(kExactThreads), 0, A);
