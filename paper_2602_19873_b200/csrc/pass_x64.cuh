@@ -355,25 +355,42 @@ __global__ void __launch_bounds__(kPxWarps * 32, 3) k_pass_x64(const __grid_cons
                     next += __popc(nb);
                     if (!__any_sync(0xffffffffu, job >= 0)) break;
                     if (job < 0) continue;
-                    if (jm == 0) {
-                        je = __ffs(jnz) - 1;
-                        jnz &= jnz - 1;
-                        jm = S.hm[job][je];
+                    // two marked slots per step (independent fp64 chains), added in order
+                    uint32_t sl[2];
+                    bool two = false;
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        if (t == 1) {
+                            two = jm != 0 || jnz != 0;
+                            if (!two) break;
+                        }
+                        if (jm == 0) {
+                            je = __ffs(jnz) - 1;
+                            jnz &= jnz - 1;
+                            jm = S.hm[job][je];
+                        }
+                        sl[t] = je * 8 + (__ffs(jm) - 1);
+                        jm &= jm - 1;
                     }
-                    const uint32_t jj = __ffs(jm) - 1;
-                    jm &= jm - 1;
-                    const uint32_t sl = je * 8 + jj;
-                    double dx, dy, dz;
-                    const double d2 = pair_d2_exact(xi, yi, zi, S.jx[sl], S.jy[sl], S.jz[sl], A.box, &dx, &dy, &dz);
-                    if (d2 > r2) continue;
-                    double v[4];
-                    if (eval_x64<K>(A, d2, dx, dy, dz, hh, sg, kPay ? S.jp[sl] : 0.0, qci, v)) {
-                        coincident = true;
-                        continue;
+                    if (!two) sl[1] = sl[0];
+                    double d2[2], dx[2], dy[2], dz[2], v[2][4];
+                    int bad2[2];
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        d2[t] = pair_d2_exact(xi, yi, zi, S.jx[sl[t]], S.jy[sl[t]], S.jz[sl[t]], A.box, &dx[t], &dy[t], &dz[t]);
+                        bad2[t] = eval_x64<K>(A, d2[t], dx[t], dy[t], dz[t], hh, sg, kPay ? S.jp[sl[t]] : 0.0, qci, v[t]);
                     }
 #pragma unroll
-                    for (int o = 0; o < NO; ++o) acc[o] = dadd(acc[o], v[o]);
-                    ++jc;
+                    for (int t = 0; t < 2; ++t) {
+                        if ((t == 1 && !two) || d2[t] > r2) continue;
+                        if (bad2[t]) {
+                            coincident = true;
+                            continue;
+                        }
+#pragma unroll
+                        for (int o = 0; o < NO; ++o) acc[o] = dadd(acc[o], v[t][o]);
+                        ++jc;
+                    }
                 }
                 __syncwarp();  // the chunk's staging and hit masks are consumed
             }
