@@ -26,6 +26,7 @@
 // SCs whose frontier/candidates/bytes exceed the shared-memory capacities are
 // re-run by the same code with global-memory workspaces (fallback launch).
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <vector>
 
@@ -52,6 +53,8 @@ struct BuildArgs {
     const double* h;
     const Node* nodes;
     const Geo* ngeo;
+    const float4* ngeo32;      // node boxes rounded to fp32 {lo, -}, {hi, -} (gather traversal pre-test), or null
+    float trav_m;              // max |coordinate| of a (shifted) box bound, for the pre-test's error bound
     const Geo* igeo;
     const Geo* jgeo;
     uint32_t* counts;
@@ -550,6 +553,31 @@ __global__ void k_validate(uint64_t n, const double* __restrict__ x, const doubl
     if (lane_id() == 0 && local) atomicMax(maxh_bits, local);
 }
 
+// Node boxes rounded to nearest fp32 for the traversal's pre-test (build_warp.cuh).
+__global__ void k_node_box32(uint64_t m, const Geo* __restrict__ g, float4* __restrict__ out) {
+    for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < m; k += uint64_t(gridDim.x) * blockDim.x) {
+        const Geo v = g[k];
+        out[2 * k] = make_float4(float(v.lo[0]), float(v.lo[1]), float(v.lo[2]), 0.f);
+        out[2 * k + 1] = make_float4(float(v.hi[0]), float(v.hi[1]), float(v.hi[2]), 0.f);
+    }
+}
+
+// fp32 node boxes for the gather traversal (null for symmetric stores or when disabled)
+int node_boxes32(sfcnl_cu_ctx* c, BuildArgs& A, bool gather) {
+    A.ngeo32 = nullptr;
+    A.trav_m = 0.f;
+    if (!gather || getenv("SFCNL_TRAV_FP64") || c->num_nodes == 0) return 0;
+    SFCNL_CUDA_TRY(c->node_geo32.reserve(c->num_nodes * 2 * sizeof(float4)));
+    launch(c, k_node_box32, dim3(unsigned(std::min<uint64_t>((c->num_nodes + 255) / 256, uint64_t(c->num_sms) * 8))),
+           dim3(256), 0, uint64_t(c->num_nodes), (const Geo*)A.ngeo, c->node_geo32.as<float4>());
+    A.ngeo32 = c->node_geo32.as<const float4>();
+    double m = 0.0;
+    for (int d = 0; d < 3; ++d)
+        m = std::max(m, std::max(std::fabs(A.box.lo[d]), std::fabs(A.box.hi[d])) + (A.box.per[d] ? A.box.len[d] : 0.0));
+    A.trav_m = float(m * 1.0001);
+    return 0;
+}
+
 // Main warp-build tier over [sc0, sc1), then the medium tier over its overflow list;
 // SCs beyond both are returned in (*ovf_list, *ovf_count) for k_build_global.
 template <class Sm, class SmM>
@@ -568,6 +596,7 @@ int launch_build_warp(sfcnl_cu_ctx* c, const BuildArgs& A, uint64_t sc0, uint64_
     SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
     *ovf_list = A.overflow_list;
     *ovf_count = 0;
+    if (getenv("SFCNL_BUILD_STATS")) fprintf(stderr, "[sfcnl] warp build: %llu of %llu SCs to the medium tier\n", ctl[1], (unsigned long long)(sc1 - sc0));
     if (ctl[1]) {  // medium tier over the overflow list; what still overflows -> ctl[4]
         const size_t smem_m = size_t(kBwWarps) * sizeof(SmM);
         cudaFuncSetAttribute(k_build_warp<SmM, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_m));
@@ -678,6 +707,7 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
     A.ngeo = c->node_geo.as<Geo>();
     A.igeo = c->igeo.as<Geo>();
     A.jgeo = p.cj == p.ci ? c->igeo.as<Geo>() : c->jgeo.as<Geo>();
+    if (int rc = node_boxes32(c, A, p.mode == 0)) return rc;
     // per-SC outputs are indexed by the global SC index: offset the bases by sc0
     A.counts = c->counts.as<uint32_t>() - sc0;
     A.sizes = c->sc_size.as<uint32_t>() - sc0;
@@ -830,6 +860,7 @@ int run_halo_mark(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, ui
         A.nodes = c->nodes.as<Node>();
         A.ngeo = c->node_geo.as<Geo>();
         A.igeo = c->igeo.as<Geo>();
+        if (int rc = node_boxes32(c, A, p.mode == 0)) return rc;
         A.ctl = c->build_ctl.as<unsigned long long>();
         A.overflow_list = c->overflow_list.as<uint32_t>();
         A.err = c->derr.as<DevError>();

@@ -31,9 +31,10 @@
 // An SC that exceeds a capacity (frontier, entries, bytes) is listed for the
 // global-memory fallback kernel (k_build_global), which runs the generic build_sc.
 constexpr int kBwWarps = 4;
-constexpr uint32_t kBwF = 512;   // frontier entries per buffer
+// main tier: no SC of the C2 / C3 workloads exceeds these (the medium tier takes the rest)
+constexpr uint32_t kBwF = 320;   // frontier entries per buffer
 constexpr uint32_t kBwE = 384;   // entries per SC (~170 at 200 neighbours)
-constexpr uint32_t kBwBytes = 4096;  // encoded bytes (aliases the frontier)
+constexpr uint32_t kBwBytes = 2560;  // encoded bytes (aliases the frontier)
 constexpr uint32_t kLeafCacheCap = 256;  // accepted leaves kept per SC by halo marking
 
 // Per-warp shared-memory slice. Two capacity tiers: the main kernel runs every SC with
@@ -59,7 +60,7 @@ struct BwSmemT {
         uint8_t ebuf[B];  // encoder output (after the masks: the frontier is dead)
     } u;
     float4 sa[4][32];  // staged j pairs [p][candidate]: {x_2p, x_2p+1, y_2p, y_2p+1}
-    float2 sz[4][32];  //                                 {z_2p, z_2p+1}
+    float4 sz[4][32];  //                                 {z_2p, z_2p+1, -, -}
     float4 ia[64];     // [ii*8 + b] {x, y, z, lo} SC frame + cutoff threshold (guard band below)
     float ihi[64];     // [ii*8 + b] hi threshold (guard band above)
     float iab[8][6];
@@ -93,9 +94,30 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // warp scans place children and tagged accepted leaves, so the accepted leaves end
 // up in key order in *out (one of the two buffers). Returns their number, or ~0u
 // when the frontier exceeds kBwF.
+//
+// Gather traversal pre-test (A.ngeo32): the box gap in fp32 from boxes rounded to
+// nearest. Every input carries an error <= u M (u = 2^-24, M >= any |bound| incl. the
+// periodic shifts), the shift and the difference one rounding each, so a gap is off by
+// at most d = u (5 M + r) near the cutoff, and the squared distance by
+// B = 2 sqrt(3) r d + 3 d^2 + 3 u r^2; d2_f32 > r^2 + 2B rejects, d2_f32 < r^2 - 2B
+// accepts (d2 - err(d2) grows with d2), anything between runs the exact fp64 test.
+__device__ __forceinline__ float gap32(float alo, float ahi, float blo, float bhi) {
+    return fmaxf(fmaxf(alo, blo) - fminf(ahi, bhi), 0.f);
+}
+
 __device__ __forceinline__ uint32_t warp_bfs(const BuildArgs& A, const Geo& scg, double r2, uint32_t* fa,
                                              uint32_t* fb, uint32_t** out, uint32_t cap = kBwF) {
     const unsigned lane = lane_id();
+    const bool pre = A.ngeo32 != nullptr;
+    float slo[3], shi[3], L32[3], r2lo = 0.f, r2hi = 0.f;
+    if (pre) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) slo[d] = float(scg.lo[d]), shi[d] = float(scg.hi[d]), L32[d] = float(A.box.len[d]);
+        const double u = 5.9604644775390625e-08, r = sqrt(r2);
+        const double dl = u * (5.0 * double(A.trav_m) + r);
+        const double B = 2.0 * (3.4641016151377544 * r * dl + 3.0 * dl * dl + 3.0 * u * r2) + 1e-12 * r2 + 1e-300;
+        r2lo = __double2float_rd(r2 - B), r2hi = __double2float_ru(r2 + B);
+    }
     if (lane == 0) fa[0] = 0;
     uint32_t nA = 1;
     __syncwarp();
@@ -113,13 +135,32 @@ __device__ __forceinline__ uint32_t warp_bfs(const BuildArgs& A, const Geo& scg,
                 } else {
                     const Node nd = A.nodes[e];
                     if (nd.pend > nd.pbegin) {
-                        const Geo ng = A.ngeo[e];
-                        double rr2 = r2;
-                        if (A.symmetric) {  // scale * max(sc_maxh, node_maxh) (neighbor_build.cpp:122-125)
-                            const double rr = dmul(A.scale, smax(scg.maxh, ng.maxh));
-                            rr2 = dmul(rr, rr);
+                        int acc = -1;  // pre-test: 1 accept, 0 reject, -1 undecided
+                        if (pre) {
+                            const float4 lo = A.ngeo32[2 * e], hi = A.ngeo32[2 * e + 1];
+                            const float bl[3] = {lo.x, lo.y, lo.z}, bh[3] = {hi.x, hi.y, hi.z};
+                            float d2f = 0.f;
+#pragma unroll
+                            for (int d = 0; d < 3; ++d) {
+                                float g = gap32(slo[d], shi[d], bl[d], bh[d]);
+                                if (A.box.per[d]) {
+                                    g = fminf(g, gap32(slo[d], shi[d], bl[d] - L32[d], bh[d] - L32[d]));
+                                    g = fminf(g, gap32(slo[d], shi[d], bl[d] + L32[d], bh[d] + L32[d]));
+                                }
+                                d2f = fmaf(g, g, d2f);
+                            }
+                            acc = d2f > r2hi ? 0 : (d2f < r2lo ? 1 : -1);
                         }
-                        if (!(aabb_dist_sq(scg, ng, A.box) > rr2)) {
+                        if (acc < 0) {
+                            const Geo ng = A.ngeo[e];
+                            double rr2 = r2;
+                            if (A.symmetric) {  // scale * max(sc_maxh, node_maxh) (neighbor_build.cpp:122-125)
+                                const double rr = dmul(A.scale, smax(scg.maxh, ng.maxh));
+                                rr2 = dmul(rr, rr);
+                            }
+                            acc = !(aabb_dist_sq(scg, ng, A.box) > rr2);
+                        }
+                        if (acc) {
                             fc = nd.first_child;
                             emit = fc < 0 ? 1 : 8;
                         }
@@ -159,6 +200,65 @@ __device__ __forceinline__ void sc_box(const BuildArgs& A, uint64_t icl_base, ui
     }
     const double r = dmul(A.scale, scg.maxh);
     r2 = dmul(r, r);
+}
+
+// unsafe SCs: the reference's mask loop in fp64 for one candidate (lane = candidate,
+// neighbor_build.cpp:128-161)
+template <bool SYM>
+__device__ __forceinline__ uint32_t unsafe_mask(const BuildArgs& A, uint32_t cand, uint64_t icl_base, uint32_t nicl) {
+    const uint32_t cj = A.cj;
+    uint32_t mask = 0;
+    const Geo jg = A.jgeo[cand];
+    const uint64_t jb = uint64_t(cand) * cj, je = tmin<uint64_t>(jb + cj, A.n);
+    for (uint32_t b = 0; b < nicl; ++b) {
+        if (SYM && (icl_base + b) * 8 > jb) continue;  // half-list rule (neighbor_build.cpp:133)
+        const Geo ig = A.igeo[icl_base + b];
+        const double pre_r = dmul(A.scale, SYM ? smax(ig.maxh, jg.maxh) : ig.maxh);
+        if (aabb_dist_sq(ig, jg, A.box) > dmul(pre_r, pre_r)) continue;
+        const uint64_t ib = (icl_base + b) * 8, ie = tmin<uint64_t>(ib + 8, A.n);
+        bool hit = false;
+        for (uint64_t i = ib; i < ie && !hit; ++i) {
+            const double xi = A.x[i], yi = A.y[i], zi = A.z[i];
+            const double rr = dmul(A.scale, A.h[i]);
+            for (uint64_t j = jb; j < je; ++j) {
+                if (i == j) continue;
+                const double d2 = pair_d2_exact(xi, yi, zi, A.x[j], A.y[j], A.z[j], A.box, nullptr, nullptr, nullptr);
+                const double rs = SYM ? dmul(A.scale, smax(A.h[i], A.h[j])) : rr;
+                if (d2 <= dmul(rs, rs)) {
+                    hit = true;
+                    break;
+                }
+            }
+        }
+        if (hit) mask |= 1u << b;
+    }
+    return mask;
+}
+
+// an item whose fp32 row minima fell inside the guard band: the reference's exact pair
+// predicate on those rows, then its prefilter (neighbor_build.cpp:136-155) -- any
+// exact hit suffices
+template <bool SYM>
+__device__ __forceinline__ bool band_item(const BuildArgs& A, uint64_t p0, uint64_t icl_base, uint32_t b, uint32_t cc,
+                                       uint32_t band_rows) {
+#ifdef SFCNL_PHASE_PROF
+    atomicAdd(A.prof + 10, 1ull);
+#endif
+    const uint32_t cj = A.cj;
+    const uint64_t jb = uint64_t(cc) * cj;
+    bool ex = false;
+    for (int ii = 0; ii < 8 && !ex; ++ii) {
+        if (!((band_rows >> ii) & 1u)) continue;
+        const uint64_t gi = p0 + b * 8 + ii;
+        for (uint32_t jj = 0; jj < cj && !ex; ++jj) {
+            if (jb + jj >= A.n || jb + jj == gi) continue;
+            ex = exact_hit(A, A.x[gi], A.y[gi], A.z[gi], A.h[gi], jb + jj);
+        }
+    }
+    if (!ex) return false;
+    const Geo ig = A.igeo[icl_base + b];
+    const double pr = dmul(A.scale, SYM ? smax(ig.maxh, A.jgeo[cc].maxh) : ig.maxh);
+    return !(aabb_dist_sq(ig, A.jgeo[cc], A.box) > dmul(pr, pr));
 }
 
 // Returns false when a capacity is exceeded (nothing published).
@@ -310,32 +410,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
         uint32_t mask = 0;
         if (unsafe) {
             // reference loop in fp64, lane = candidate (neighbor_build.cpp:128-161)
-            if (valid) {
-                const Geo jg = A.jgeo[cand];
-                const uint64_t jb = uint64_t(cand) * cj, je = tmin<uint64_t>(jb + cj, A.n);
-                for (uint32_t b = 0; b < nicl; ++b) {
-                    if (SYM && (icl_base + b) * 8 > jb) continue;  // half-list rule (neighbor_build.cpp:133)
-                    const Geo ig = A.igeo[icl_base + b];
-                    const double pre_r = dmul(A.scale, SYM ? smax(ig.maxh, jg.maxh) : ig.maxh);
-                    if (aabb_dist_sq(ig, jg, A.box) > dmul(pre_r, pre_r)) continue;
-                    const uint64_t ib = (icl_base + b) * 8, ie = tmin<uint64_t>(ib + 8, A.n);
-                    bool hit = false;
-                    for (uint64_t i = ib; i < ie && !hit; ++i) {
-                        const double xi = A.x[i], yi = A.y[i], zi = A.z[i];
-                        const double rr = dmul(A.scale, A.h[i]);
-                        for (uint64_t j = jb; j < je; ++j) {
-                            if (i == j) continue;
-                            const double d2 = pair_d2_exact(xi, yi, zi, A.x[j], A.y[j], A.z[j], A.box, nullptr, nullptr, nullptr);
-                            const double rs = SYM ? dmul(A.scale, smax(A.h[i], A.h[j])) : rr;
-                            if (d2 <= dmul(rs, rs)) {
-                                hit = true;
-                                break;
-                            }
-                        }
-                    }
-                    if (hit) mask |= 1u << b;
-                }
-            }
+            if (valid) mask = unsafe_mask<SYM>(A, cand, icl_base, nicl);
         } else {
             // stage (cluster frame, frame.cu): shift = fl32(minimage(c_J - o)) per candidate,
             // s = shift + off per particle; [p][candidate] pair-packed. Every load of the
@@ -431,7 +506,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
                     const float4 a = S.sa[p][lane];
-                    const float2 z = S.sz[p][lane];
+                    const float4 z = S.sz[p][lane];
                     if (a.x != 1e30f) {
                         jlo[0] = fminf(jlo[0], a.x), jhi[0] = fmaxf(jhi[0], a.x);
                         jlo[1] = fminf(jlo[1], a.z), jhi[1] = fmaxf(jhi[1], a.z);
@@ -481,12 +556,12 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
                 const uint32_t cc = __shfl_sync(0xffffffffu, cand, c);
                 const bool self = iv && j0 >= -7 && j0 < kSC;
                 ulonglong2 Ja[4];
-                f2 Jz[4];
+                ulonglong2 Jz[4];  // {z pair, -} (16-byte staging rows measured faster than 8-byte ones)
                 float2 Jlo[4], Jhi[4];
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
                     Ja[p] = reinterpret_cast<const ulonglong2&>(S.sa[p][c]);
-                    Jz[p] = reinterpret_cast<const f2&>(S.sz[p][c]);
+                    Jz[p].x = reinterpret_cast<const f2&>(S.sz[p][c]);
                     if constexpr (SYM) Jlo[p] = S.sy.slo[p][c], Jhi[p] = S.sy.shi[p][c];
                 }
                 bool hit = false;
@@ -502,8 +577,8 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
                         const float hii = S.ihi[ii * 8 + b];
 #pragma unroll
                         for (int p = 0; p < 4; ++p) {
-                            const f2 dx = f2sub(xi2, Ja[p].x), dy = f2sub(yi2, Ja[p].y), dz = f2sub(zi2, Jz[p]);
                             float d2a, d2b;
+                            const f2 dx = f2sub(xi2, Ja[p].x), dy = f2sub(yi2, Ja[p].y), dz = f2sub(zi2, Jz[p].x);
                             f2u(f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx))), d2a, d2b);
                             if (kSelf) {
                                 if (iself == 2 * p) d2a = 3.0e38f;
@@ -527,28 +602,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
                 };
                 if (__any_sync(0xffffffffu, self)) rows(BoolC<true>());
                 else rows(BoolC<false>());
-                if (iv && !hit && band_rows) {
-#ifdef SFCNL_PHASE_PROF
-                    atomicAdd(A.prof + 10, 1ull);
-#endif
-                    // guard band: the reference's exact pair predicate, then its prefilter
-                    // (neighbor_build.cpp:136-155) -- any exact hit suffices
-                    const uint64_t jb = uint64_t(cc) * cj;
-                    bool ex = false;
-                    for (int ii = 0; ii < 8 && !ex; ++ii) {
-                        if (!((band_rows >> ii) & 1u)) continue;
-                        const uint64_t gi = p0 + b * 8 + ii;
-                        for (uint32_t jj = 0; jj < cj && !ex; ++jj) {
-                            if (jb + jj >= A.n || jb + jj == gi) continue;
-                            ex = exact_hit(A, A.x[gi], A.y[gi], A.z[gi], A.h[gi], jb + jj);
-                        }
-                    }
-                    if (ex) {
-                        const Geo ig = A.igeo[icl_base + b];
-                        const double pr = dmul(A.scale, SYM ? smax(ig.maxh, A.jgeo[cc].maxh) : ig.maxh);
-                        hit = !(aabb_dist_sq(ig, A.jgeo[cc], A.box) > dmul(pr, pr));
-                    }
-                }
+                if (iv && !hit && band_rows) hit = band_item<SYM>(A, p0, icl_base, b, cc, band_rows);
                 if (hit) atomicOr(&S.cmask[c], 1u << b);
             }
             __syncwarp();

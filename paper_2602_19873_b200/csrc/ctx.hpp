@@ -101,6 +101,7 @@ struct sfcnl_cu_ctx {
     sfcnl_cu::DBuf level_nodes;  // node indices grouped by depth (deepest processed first)
     std::vector<uint64_t> level_off;  // host: level d occupies [level_off[d], level_off[d+1])
     sfcnl_cu::DBuf node_geo;   // Geo[num_nodes]
+    sfcnl_cu::DBuf node_geo32; // node boxes in fp32 for the build traversal's pre-test
     bool node_geo_external = false;  // node_geo supplied by the caller (domain decomposition)
     sfcnl_cu::DBuf tree_scratch;
     // level-synchronous construction scratch, one entry per depth
