@@ -19,6 +19,10 @@
 //     value to the target's fp64 sum (shared memory, carried across chunks).
 // SCs whose periodic images are ambiguous in the SC frame ("unsafe") mark every slot.
 constexpr int kPxWarps = 4;
+#ifndef SFCNL_PX_SLOTS
+#define SFCNL_PX_SLOTS 4
+#endif
+constexpr int kPxSlots = SFCNL_PX_SLOTS;  // marked slots evaluated per step of a lane
 
 template <int K>
 struct alignas(16) PxSmem {
@@ -355,15 +359,12 @@ __global__ void __launch_bounds__(kPxWarps * 32, 3) k_pass_x64(const __grid_cons
                     next += __popc(nb);
                     if (!__any_sync(0xffffffffu, job >= 0)) break;
                     if (job < 0) continue;
-                    // two marked slots per step (independent fp64 chains), added in order
-                    uint32_t sl[2];
-                    bool two = false;
+                    // kPxSlots marked slots per step (independent fp64 chains), added in order
+                    uint32_t sl[kPxSlots];
+                    uint32_t nsl = 0;
 #pragma unroll
-                    for (int t = 0; t < 2; ++t) {
-                        if (t == 1) {
-                            two = jm != 0 || jnz != 0;
-                            if (!two) break;
-                        }
+                    for (int t = 0; t < kPxSlots; ++t) {
+                        if (jm == 0 && jnz == 0) break;
                         if (jm == 0) {
                             je = __ffs(jnz) - 1;
                             jnz &= jnz - 1;
@@ -371,18 +372,21 @@ __global__ void __launch_bounds__(kPxWarps * 32, 3) k_pass_x64(const __grid_cons
                         }
                         sl[t] = je * 8 + (__ffs(jm) - 1);
                         jm &= jm - 1;
+                        ++nsl;
                     }
-                    if (!two) sl[1] = sl[0];
-                    double d2[2], dx[2], dy[2], dz[2], v[2][4];
-                    int bad2[2];
 #pragma unroll
-                    for (int t = 0; t < 2; ++t) {
+                    for (int t = 1; t < kPxSlots; ++t)
+                        if (uint32_t(t) >= nsl) sl[t] = sl[0];
+                    double d2[kPxSlots], dx[kPxSlots], dy[kPxSlots], dz[kPxSlots], v[kPxSlots][4];
+                    int bad2[kPxSlots];
+#pragma unroll
+                    for (int t = 0; t < kPxSlots; ++t) {
                         d2[t] = pair_d2_exact(xi, yi, zi, S.jx[sl[t]], S.jy[sl[t]], S.jz[sl[t]], A.box, &dx[t], &dy[t], &dz[t]);
                         bad2[t] = eval_x64<K>(A, d2[t], dx[t], dy[t], dz[t], hh, sg, kPay ? S.jp[sl[t]] : 0.0, qci, v[t]);
                     }
 #pragma unroll
-                    for (int t = 0; t < 2; ++t) {
-                        if ((t == 1 && !two) || d2[t] > r2) continue;
+                    for (int t = 0; t < kPxSlots; ++t) {
+                        if (uint32_t(t) >= nsl || d2[t] > r2) continue;
                         if (bad2[t]) {
                             coincident = true;
                             continue;
