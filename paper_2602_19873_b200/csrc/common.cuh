@@ -52,19 +52,25 @@ __device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b 
 // One axis of periodic_delta (core.hpp:77-85): d -= L * rint(d / L).
 // |d| < L/2 (strictly, with margin) gives rint(d/L) == 0 and d - L*0 == d exactly,
 // so the division is skipped there; otherwise the reference chain is evaluated.
+static __device__ __noinline__ double min_image_wrap(double d, double L) { return dsub(d, dmul(L, rint(ddiv(d, L)))); }
+// OL: the rare wrap (and its long division) out of line -- smaller hot kernels (the list
+// build: 63.6 -> 59.8 ms at C2); the LJ pass's rare-slot path keeps it inline (faster there)
+template <bool OL = true>
 __device__ __forceinline__ double min_image_exact(double d, double L, int per) {
     if (!per) return d;
     if (fabs(d) < 0.4999 * L) return d;
+    if (OL) return min_image_wrap(d, L);
     return dsub(d, dmul(L, rint(ddiv(d, L))));
 }
 
 // Squared minimum-image distance exactly as periodic_delta + Vec3::norm2.
+template <bool OL = true>
 __device__ __forceinline__ double pair_d2_exact(double xi, double yi, double zi, double xj,
                                                 double yj, double zj, const Box& b, double* dx,
                                                 double* dy, double* dz) {
-    const double ax = min_image_exact(dsub(xi, xj), b.len[0], b.per[0]);
-    const double ay = min_image_exact(dsub(yi, yj), b.len[1], b.per[1]);
-    const double az = min_image_exact(dsub(zi, zj), b.len[2], b.per[2]);
+    const double ax = min_image_exact<OL>(dsub(xi, xj), b.len[0], b.per[0]);
+    const double ay = min_image_exact<OL>(dsub(yi, yj), b.len[1], b.per[1]);
+    const double az = min_image_exact<OL>(dsub(zi, zj), b.len[2], b.per[2]);
     if (dx) *dx = ax, *dy = ay, *dz = az;
     return dadd(dadd(dmul(ax, ax), dmul(ay, ay)), dmul(az, az));
 }

@@ -57,13 +57,13 @@ __device__ __forceinline__ float rcp_ftz(float x) {
 // Rare slot: cutoff inside the guard band, or an LJ pair closer than 1.22 sigma
 // (force-zero crossing / overflow range): the exact reference predicate and fp64
 // kernel value, accumulated into the SC's shared fp64 side sums.
-template <int K>
+template <int K, bool OL = true>  // OL: min-image wrap out of line (see common.cuh)
 __device__ __noinline__ int rare_slot(const PassArgs& A, uint64_t i, uint64_t j, double r2,
                                       double* side) {
     if (i == j) return 0;
     const double xi = A.x[i], yi = A.y[i], zi = A.z[i], hi = A.h[i];
     double dx, dy, dz;
-    const double d2 = pair_d2_exact(xi, yi, zi, A.x[j], A.y[j], A.z[j], A.box, &dx, &dy, &dz);
+    const double d2 = pair_d2_exact<OL>(xi, yi, zi, A.x[j], A.y[j], A.z[j], A.box, &dx, &dy, &dz);
     if (d2 > r2) return 0;
     double v[4];
     if (eval_exact<K>(A, i, j, d2, dx, dy, dz, hi, v)) return -1;

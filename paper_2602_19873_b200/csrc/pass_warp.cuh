@@ -275,11 +275,11 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                             const uint64_t jb = uint64_t(__shfl_sync(0xffffffffu, my_idx, e)) * CJ;
                             if (!active) continue;
                             if (jb + jq < A.n) {
-                                const int rc = rare_slot<K>(A, i, jb + jq, r2, side);
+                                const int rc = rare_slot<K, false>(A, i, jb + jq, r2, side);
                                 cnt += rc > 0, coincident |= rc < 0;
                             }
                             if (CJ == 8 && jb + jq + 4 < A.n) {
-                                const int rc = rare_slot<K>(A, i, jb + jq + 4, r2, side);
+                                const int rc = rare_slot<K, false>(A, i, jb + jq + 4, r2, side);
                                 cnt += rc > 0, coincident |= rc < 0;
                             }
                         }
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                             }
                         }
                         const double r = dmul(A.qs, A.h[i]);
-                        const int rc = rare_slot<K>(A, i, j, dmul(r, r), &S.acc[li][0]);
+                        const int rc = rare_slot<K, false>(A, i, j, dmul(r, r), &S.acc[li][0]);
                         cnt += rc > 0, coincident |= rc < 0;
                     };
                     auto compute = [&](uint32_t e, const Ld& L, auto SELF) {
