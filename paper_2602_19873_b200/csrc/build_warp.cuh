@@ -31,6 +31,7 @@
 // An SC that exceeds a capacity (frontier, entries, bytes) is listed for the
 // global-memory fallback kernel (k_build_global), which runs the generic build_sc.
 constexpr int kBwWarps = 4;
+#define SFCNL_UNLIKELY(c) __builtin_expect(!!(c), 0)  // cold blocks placed out of the hot path
 // main tier: no SC of the C2 / C3 workloads exceeds these (the medium tier takes the rest)
 constexpr uint32_t kBwF = 320;   // frontier entries per buffer
 constexpr uint32_t kBwE = 384;   // entries per SC (~170 at 200 neighbours)
@@ -408,7 +409,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
         const int jl0 = int(cand) * int(cj) - int(p0);
         const unsigned selfm = __ballot_sync(0xffffffffu, valid && jl0 >= -7 && jl0 < kSC);
         uint32_t mask = 0;
-        if (unsafe) {
+        if (SFCNL_UNLIKELY(unsafe)) {
             // reference loop in fp64, lane = candidate (neighbor_build.cpp:128-161)
             if (valid) mask = unsafe_mask<SYM>(A, cand, icl_base, nicl);
         } else {
@@ -602,7 +603,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
                 };
                 if (__any_sync(0xffffffffu, self)) rows(BoolC<true>());
                 else rows(BoolC<false>());
-                if (iv && !hit && band_rows) hit = band_item<SYM>(A, p0, icl_base, b, cc, band_rows);
+                if (SFCNL_UNLIKELY(iv && !hit && band_rows)) hit = band_item<SYM>(A, p0, icl_base, b, cc, band_rows);
                 if (hit) atomicOr(&S.cmask[c], 1u << b);
             }
             __syncwarp();
