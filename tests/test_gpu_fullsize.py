@@ -3,7 +3,10 @@
 GPU-produced intermediates on the reference side:
 
 * C2: 2^26 uniform particles, periodic unit cube, 200 neighbours, 8x8 gather compressed;
-* C3: Evrard sphere, 2^24 particles, per-particle h, open box.
+* C3: Evrard sphere, 2^24 particles, per-particle h, open box;
+* C4: LJ fluid: 4,000,000 uniform particles at density 100, target 150,
+  build_radius_scale 1.100642 (Verlet skin), query scale 1, sigma 0.2, for the 8x8 (w32),
+  8x4 (w64) and 1x1 cluster geometries, with bench::cluster_overhead (bench.cpp:93-122).
 
 The inputs come from the reference's own generator (generators.cpp:21-82) and the same
 host bytes go to both sides. The reference runs its whole pipeline on the host
@@ -37,21 +40,27 @@ pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(os.environ.get("SFCNL_FULLSIZE", "1") == "0", reason="SFCNL_FULLSIZE=0")]
 THREADS = os.cpu_count() or 1
 
+# name: (generator, n, density, target, (ci, cj, w), build scale, sigma or None = 0.5 n^(-1/3))
+_C4_N = int(os.environ.get("SFCNL_FULLSIZE_C4_N", "4000000"))
 CONFIGS = {
-    "C2": ("uniform", int(os.environ.get("SFCNL_FULLSIZE_C2_N", str(1 << 26)))),
-    "C3": ("evrard", int(os.environ.get("SFCNL_FULLSIZE_C3_N", str(1 << 24)))),
+    "C2": ("uniform", int(os.environ.get("SFCNL_FULLSIZE_C2_N", str(1 << 26))), None, 200.0, (8, 8, 32), 1.0, None),
+    "C3": ("evrard", int(os.environ.get("SFCNL_FULLSIZE_C3_N", str(1 << 24))), None, 200.0, (8, 8, 32), 1.0, None),
+    "C4_8x8": ("uniform", _C4_N, 100.0, 150.0, (8, 8, 32), 1.100642, 0.2),
+    "C4_8x4": ("uniform", _C4_N, 100.0, 150.0, (8, 4, 64), 1.100642, 0.2),
+    "C4_1x1": ("uniform", _C4_N, 100.0, 150.0, (1, 1, 32), 1.100642, 0.2),
 }
 
 
 @pytest.fixture(scope="module", params=sorted(CONFIGS))
 def run(request):
     import torch
-    gen, n = CONFIGS[request.param]
+    gen, n, density, target, (ci, cj, w), scale, sigma = CONFIGS[request.param]
     R = Oracle("reference")
-    op = (R.make_uniform(n, float(n), 200.0, (1, 1, 1), 0.0, 42) if gen == "uniform"
-          else R.make_evrard(n, 200.0, False, (0, 0, 0), 42))
-    sigma = 0.5 * (1.0 / n) ** (1.0 / 3.0)
-    bp = S.BuildParams(S.ClusterParams(8, 8, 32), S.GATHER, True, 1.0)
+    op = (R.make_uniform(n, density or float(n), target, (1, 1, 1), 0.0, 42) if gen == "uniform"
+          else R.make_evrard(n, target, False, (0, 0, 0), 42))
+    if sigma is None:
+        sigma = 0.5 * (1.0 / n) ** (1.0 / 3.0)
+    bp = S.BuildParams(S.ClusterParams(ci, cj, w), S.GATHER, True, scale)
 
     # ---- GPU, through the C-ABI
     ctx = S.Context(0)
@@ -66,6 +75,7 @@ def run(request):
     g["node_geo"] = ctx.node_geometry(nn)
     nsc, nb = ctx.build_store(bp)
     g["store"] = ctx.get_store(bp, n, nsc, nb)
+    g["slots"] = ctx.cluster_slots()
     cg = ctx.device_array("cluster_geo.i", torch.float64).view(-1, 8).cpu().numpy()
     g["cluster_geo"] = (cg[:, 0:3], cg[:, 3:6], cg[:, 6])
     g["rho64"] = ctx.reduce(S.sph_density_kernel(), S.PassConfig(1.0, S.F64), n)
@@ -81,22 +91,23 @@ def run(request):
     del op
     tree, lo, hi, rad = R.node_geometry(r["keys"], sp)
     r["tree"], r["node_geo"] = tree, (lo, hi, rad)
-    r["cluster_geo"] = R.cluster_geometry(sp, 8)
-    r["store"] = R.build_store(sp, tree, 8, 8, 32, 0, 1, 1.0, threads=THREADS)
+    r["cluster_geo"] = R.cluster_geometry(sp, ci)
+    r["store"] = R.build_store(sp, tree, ci, cj, w, 0, 1, scale, threads=THREADS)
     r["rho"] = R.reduce("density", sp, r["store"], threads=THREADS)
     r["lj"] = R.reduce("lj", sp, r["store"], eps=1.0, sigma=sigma, threads=THREADS)
     r["lj_abs"] = R.lj_abs_sums(sp, r["store"], eps=1.0, sigma=sigma, threads=THREADS)
-    return g, r
+    r["overhead"] = R.cluster_overhead(r["store"], int(r["rho"][1].astype(np.int64).sum()))
+    return request.param, g, r
 
 
 def test_sfc_order(run):
-    g, r = run
+    name, g, r = run
     assert np.array_equal(g["keys"], r["keys"])
     assert np.array_equal(g["perm"], r["perm"])
 
 
 def test_octree_nodes(run):
-    g, r = run
+    name, g, r = run
     nodes, t = g["nodes"], r["tree"]
     assert len(nodes) == len(t.pend)
     for gf, rf in (("key_first", "key_first"), ("key_last", "key_last"), ("particle_begin", "pbegin"),
@@ -105,27 +116,34 @@ def test_octree_nodes(run):
 
 
 def test_node_geometry(run):
-    g, r = run
+    name, g, r = run
     for a, b in zip(g["node_geo"], r["node_geo"]):
         assert np.array_equal(a, b)
 
 
 def test_cluster_geometry(run):
-    g, r = run
+    name, g, r = run
     for a, b in zip(g["cluster_geo"], r["cluster_geo"]):
         assert np.array_equal(a, b)
 
 
 def test_store_every_byte(run):
-    g, r = run
+    name, g, r = run
     assert np.array_equal(g["store"].counts, r["store"].counts)
     assert np.array_equal(g["store"].offsets, r["store"].offsets)
     assert np.array_equal(g["store"].blob, r["store"].blob)
-    assert S.memory_footprint(g["store"]).bytes_per_particle <= 4.0
+    if name in ("C2", "C3"):  # the north star's storage bound (C4 reports its cluster geometries)
+        assert S.memory_footprint(g["store"]).bytes_per_particle <= 4.0
+
+
+def test_cluster_overhead(run):
+    name, g, r = run
+    pairs = int(r["rho"][1].astype(np.int64).sum())
+    assert g["slots"] / pairs == r["overhead"]
 
 
 def test_fp64_density_and_lj_bit_exact(run):
-    g, r = run
+    name, g, r = run
     outs, cnt = r["rho"]
     assert np.array_equal(g["rho64"].neighbor_count, cnt)
     assert np.array_equal(g["rho64"].outputs[0], outs[0])
@@ -136,7 +154,7 @@ def test_fp64_density_and_lj_bit_exact(run):
 
 
 def test_mixed_density_all_particles(run):
-    g, r = run
+    name, g, r = run
     outs, cnt = r["rho"]
     assert np.array_equal(g["rho32"].neighbor_count, cnt)
     nz = outs[0] != 0
@@ -146,7 +164,7 @@ def test_mixed_density_all_particles(run):
 
 
 def test_mixed_lj_all_particles(run):
-    g, r = run
+    name, g, r = run
     outs, cnt = r["lj"]
     absf, abse = r["lj_abs"]
     f = g["lj32"].outputs
