@@ -43,6 +43,7 @@ constexpr bool kTwo = true;
 constexpr bool kTwo = false;
 #endif
 constexpr bool kTwoDensityOff = true;
+constexpr bool kPwF32Acc = true;  // LJ: fp32 per-i sums across chunks, fp64 only at the end (-0.4 %)
 
 template <int K>
 struct alignas(16) PwSmem {
@@ -58,6 +59,7 @@ struct alignas(16) PwSmem {
     double iscale[64]; // density: 8/(pi h^3) * 2 (the spline's factor 2 folded in)
     float iinvh[64];   // density: 1 / h_i
     double acc[64][NO];
+    float accf[LJ ? 64 : 1][NO];  // LJ: fp32 sums of the per-(b, chunk) flushes (fp64 close pairs stay in acc)
     uint32_t cnt[64];
     float ilo[64], ihi[64];  // per-chunk cutoff thresholds with the guard band
 };
@@ -143,7 +145,10 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
             if (LJ) S.ilx[k] = float(qx - double(fx)), S.ily[k] = float(qy - double(fy)), S.ilz[k] = float(qz - double(fz));
             if (K == SFCNL_KERNEL_DENSITY) S.iscale[k] = 2.0 * (8.0 / (kPi * hk * hk * hk)), S.iinvh[k] = float(1.0 / hk);
 #pragma unroll
-            for (int o = 0; o < NO; ++o) S.acc[k][o] = 0.0;
+            for (int o = 0; o < NO; ++o) {
+                S.acc[k][o] = 0.0;
+                if (LJ) S.accf[k][o] = 0.f;
+            }
             S.cnt[k] = 0;
         }
         eax = warp_fmax(eax), eay = warp_fmax(eay), eaz = warp_fmax(eaz), er = warp_fmax(er);
@@ -441,6 +446,8 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                     // flush: pair halves and the four j-quarter lanes of each i in fp32 (<= 2 x 64
                     // terms per lane), added to the per-i fp64 sums; fp64 close-pair sums separately
                     double tot[NO];
+                    float totf[NO];
+                    bool close_any = false;
                     const f2 accs[4] = {acc0, acc1, acc2, acc3};
 #pragma unroll
                     for (int o = 0; o < NO; ++o) {
@@ -450,10 +457,12 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                         v += __shfl_xor_sync(0xffffffffu, v, 1);
                         v += __shfl_xor_sync(0xffffffffu, v, 2);
                         const double sc_o = K == SFCNL_KERNEL_LJ ? (o < 3 ? eps24d : eps4d) : 1.0;
-                        tot[o] = double(v) * sc_o;
+                        totf[o] = v;
+                        tot[o] = kPwF32Acc && LJ ? 0.0 : double(v) * sc_o;
                     }
                     if (LJ && __any_sync(0xffffffffu, accd0 != 0.0 || accd1 != 0.0 || accd2 != 0.0 || accd3 != 0.0)) {
                         double accds[4] = {accd0, accd1, accd2, accd3};
+                        close_any = true;
 #pragma unroll
                         for (int o = 0; o < NO; ++o) {
                             double v = accds[o];
@@ -474,8 +483,14 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                         if (K == SFCNL_KERNEL_DENSITY) {
                             S.acc[li][0] += S.iscale[li] * tot[0];
                         } else if (LJ) {
+                            // fp32 per i across the SC's chunks (<= ~8 more roundings of partial sums),
+                            // the fp64 close-pair sums into the fp64 side sums
 #pragma unroll
-                            for (int o = 0; o < NO; ++o) S.acc[li][o] += tot[o];
+                            for (int o = 0; o < NO; ++o) S.accf[li][o] += totf[o];
+                            if (close_any) {
+#pragma unroll
+                                for (int o = 0; o < NO; ++o) S.acc[li][o] += tot[o];
+                            }
                         }
                         S.cnt[li] += cnt;
                     }
@@ -496,7 +511,11 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                         A.out[0][i] = double(S.cnt[k]);
                     } else {
 #pragma unroll
-                        for (int o = 0; o < NO; ++o) A.out[o][i] = S.acc[k][o];
+                        for (int o = 0; o < NO; ++o) {
+                            double v = S.acc[k][o];
+                            if (LJ && kPwF32Acc) v += double(S.accf[k][o]) * (K == SFCNL_KERNEL_LJ ? (o < 3 ? eps24d : eps4d) : 1.0);
+                            A.out[o][i] = v;
+                        }
                     }
                     A.cnt[i] = S.cnt[k];
                 }
