@@ -604,7 +604,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
                 if (__any_sync(0xffffffffu, self)) rows(BoolC<true>());
                 else rows(BoolC<false>());
                 if (SFCNL_UNLIKELY(iv && !hit && band_rows)) hit = band_item<SYM>(A, p0, icl_base, b, cc, band_rows);
-                if (hit) atomicOr(&S.cmask[c], 1u << b);
+                if (iv && hit) atomicOr(&S.cmask[c], 1u << b);
             }
             __syncwarp();
             PHASE(8);
