@@ -170,6 +170,37 @@ int sfcnl_cu_set_store(sfcnl_cu_ctx* ctx, const sfcnl_build_params* params, uint
 int sfcnl_cu_reduce(sfcnl_cu_ctx* ctx, const sfcnl_pass_params* params, double* const* outs,
                     uint32_t* neighbor_count);
 
+/* ---- (5a) device view for user pair kernels ------------------------------------
+ * reduce<Real, K> with a user kernel (make_pair_kernel / BasicPairKernel,
+ * pair_kernel.hpp:60-91; reduce.hpp:38-231) runs a header-only CUDA kernel in the
+ * caller's own CUDA translation unit (include/sfcnl/gpu_pair_kernel.cuh) over the
+ * context's device state: the sorted particle set, its fields and the store set by
+ * sfcnl_cu_set_sorted_field / sfcnl_cu_set_store. Pointers stay valid until the next
+ * call that changes that state. box_len[d] is the periodic length of axis d, 0 on
+ * open axes (the reference's box_len, reduce.hpp:80-81). */
+typedef struct {
+    uint64_t n;
+    uint64_t num_sc;
+    uint32_t ci;
+    uint32_t cj;
+    int32_t w;
+    int32_t mode;
+    int32_t compress;
+    double box_len[3];
+    const double* x;
+    const double* y;
+    const double* z;
+    const double* h;
+    const uint32_t* counts;
+    const uint64_t* offsets;
+    const uint8_t* blob;
+    uint64_t blob_bytes;
+    void* stream;
+} sfcnl_cu_device_view;
+int sfcnl_cu_get_device_view(sfcnl_cu_ctx* ctx, sfcnl_cu_device_view* out);
+/* device pointer of a field of the sorted slot (set by sfcnl_cu_set_sorted_field) */
+int sfcnl_cu_sorted_field_ptr(sfcnl_cu_ctx* ctx, const char* name, const double** out);
+
 /* ---- (5b) full Verlet list baseline -------------------------
  * The classic per-particle CSR list the paper measures the compressed list
  * against (baselines.hpp:27-38 FullVerletList, :42-44 build_full_list, :47-129

@@ -77,7 +77,8 @@ EXPORTS = [
     "sfcnl_cu_set_sorted_field", "sfcnl_cu_sort_by_sfc", "sfcnl_cu_get_order", "sfcnl_cu_set_order",
     "sfcnl_cu_apply_order", "sfcnl_cu_get_sorted", "sfcnl_cu_build_octree", "sfcnl_cu_get_octree",
     "sfcnl_cu_set_octree", "sfcnl_cu_node_geometry", "sfcnl_cu_build_store", "sfcnl_cu_get_store",
-    "sfcnl_cu_set_store", "sfcnl_cu_reduce", "sfcnl_codec_encode", "sfcnl_codec_decode_into",
+    "sfcnl_cu_set_store", "sfcnl_cu_reduce", "sfcnl_cu_get_device_view", "sfcnl_cu_sorted_field_ptr",
+    "sfcnl_codec_encode", "sfcnl_codec_decode_into",
     "sfcnl_hilbert_encode", "sfcnl_hilbert_decode", "sfcnl_last_host_error", "sfcnl_make_uniform",
     "sfcnl_make_evrard", "sfcnl_cu_build_store_range", "sfcnl_cu_alloc_sorted", "sfcnl_cu_write_sorted",
     "sfcnl_cu_read_sorted", "sfcnl_cu_read_order", "sfcnl_cu_set_keys", "sfcnl_cu_apply_order_into",

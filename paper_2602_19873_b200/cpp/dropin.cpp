@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <functional>
 #include <memory>
 #include <mutex>
 
@@ -281,6 +282,35 @@ void gpu::run_pass(const ParticleSet& ps, const SimulationBox& box, const Neighb
     for (int o = 0; o < no; ++o) outs[o] = outputs[o].data();
     const sfcnl_pass_params pp{req.kind, req.precision, req.query_scale, req.epsilon, req.sigma, req.coulomb_k};
     D.check(sfcnl_cu_reduce(D.ctx, &pp, outs, neighbor_count.data()));
+}
+
+void gpu::with_device_pass(const ParticleSet& ps, const SimulationBox& box, const NeighborStore& store,
+                           const std::vector<std::string>& fields, const PassConfig& cfg,
+                           const std::function<void(const sfcnl_cu_device_view&, const std::vector<const double*>&)>& fn) {
+    const std::size_t n = ps.size();
+    if (store.n != n) throw InputError("reduce: store/particle-set size mismatch");
+    if (cfg.query_scale > store.build.build_radius_scale)
+        throw InputError("reduce: query_scale exceeds the store's build radius scale");
+    if (store.build.mode != ListMode::gather)
+        throw InputError("reduce: user pair kernels on the GPU take gather stores");
+    Device& D = device();
+    std::lock_guard<std::mutex> lock(D.mu);
+    check_lengths(ps);
+    upload(D, ps, box, true, false);
+    std::vector<const double*> fp;
+    for (const auto& name : fields) {
+        D.check(sfcnl_cu_set_sorted_field(D.ctx, name.c_str(), ps.field(name).data()));
+        const double* d = nullptr;
+        D.check(sfcnl_cu_sorted_field_ptr(D.ctx, name.c_str(), &d));
+        fp.push_back(d);
+    }
+    const sfcnl_build_params p = to_params(store.build);
+    const std::uint8_t dummy = 0;
+    D.check(sfcnl_cu_set_store(D.ctx, &p, store.n, store.counts.size(), store.counts.data(), store.offsets.data(),
+                               store.blob.empty() ? &dummy : store.blob.data(), store.blob.size()));
+    sfcnl_cu_device_view v{};
+    D.check(sfcnl_cu_get_device_view(D.ctx, &v));
+    fn(v, fp);
 }
 
 // ------------------------------------------------------------------ full Verlet list

@@ -480,6 +480,36 @@ int sfcnl_cu_set_store(sfcnl_cu_ctx* c, const sfcnl_build_params* p, uint64_t n,
     return finish(c);
 }
 
+int sfcnl_cu_get_device_view(sfcnl_cu_ctx* c, sfcnl_cu_device_view* v) {
+    CallScope scope(c);
+    if (!v) return set_error(c, SFCNL_INPUT_ERROR, "null device view");
+    if (!c->sorted.valid) return set_error(c, SFCNL_INPUT_ERROR, "device view: no particles");
+    if (!c->has_store) return set_error(c, SFCNL_INPUT_ERROR, "device view: no neighbor store");
+    if (c->store_n != c->sorted.n) return set_error(c, SFCNL_INPUT_ERROR, "reduce: store/particle-set size mismatch");
+    if (c->sc_base != 0 || c->num_sc != (c->sorted.n + 63) / 64)
+        return set_error(c, SFCNL_INPUT_ERROR, "device view: the store covers a super-cluster range");
+    *v = sfcnl_cu_device_view{};
+    v->n = c->sorted.n;
+    v->num_sc = c->num_sc;
+    v->ci = c->sp.ci, v->cj = c->sp.cj;
+    v->w = c->sp.w, v->mode = c->sp.mode, v->compress = c->sp.compress;
+    for (int d = 0; d < 3; ++d) v->box_len[d] = c->sorted.box.per[d] ? c->sorted.box.len[d] : 0.0;
+    v->x = c->sorted.x.as<const double>(), v->y = c->sorted.y.as<const double>();
+    v->z = c->sorted.z.as<const double>(), v->h = c->sorted.h.as<const double>();
+    v->counts = c->counts.as<const uint32_t>(), v->offsets = c->offsets.as<const uint64_t>();
+    v->blob = c->blob.as<const uint8_t>(), v->blob_bytes = c->blob_bytes;
+    v->stream = (void*)c->stream;
+    return finish(c);
+}
+
+int sfcnl_cu_sorted_field_ptr(sfcnl_cu_ctx* c, const char* name, const double** out) {
+    CallScope scope(c);
+    auto* f = c->sorted.find(name);
+    if (!f) return set_error(c, SFCNL_INPUT_ERROR, std::string("ParticleSet: no such field: ") + name);
+    *out = f->data.as<const double>();
+    return finish(c);
+}
+
 int sfcnl_cu_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params* p, double* const* outs, uint32_t* count) {
     CallScope scope(c);
     if (!p) return set_error(c, SFCNL_INPUT_ERROR, "null pass params");
