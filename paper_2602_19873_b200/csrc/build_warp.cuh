@@ -36,7 +36,11 @@ constexpr int kBwWarps = 4;
 constexpr uint32_t kBwF = 320;   // frontier entries per buffer
 constexpr uint32_t kBwE = 384;   // entries per SC (~170 at 200 neighbours)
 constexpr uint32_t kBwBytes = 2560;  // encoded bytes (aliases the frontier)
-constexpr uint32_t kLeafCacheCap = 256;  // accepted leaves kept per SC by halo marking
+constexpr uint32_t kLeafCacheCap = 256;
+#ifndef SFCNL_BW_SZ8
+#define SFCNL_BW_SZ8 0
+#endif
+constexpr bool kBwSz8 = SFCNL_BW_SZ8;  // accepted leaves kept per SC by halo marking
 
 // Per-warp shared-memory slice. Two capacity tiers: the main kernel runs every SC with
 // the small one (5 CTAs x 4 warps per SM); SCs that exceed it (dense lists, wide skins,
@@ -50,10 +54,11 @@ struct BwSymJ {
 template <>
 struct BwSymJ<false> {};
 
-template <uint32_t F, uint32_t E, uint32_t B, bool SYM = false>
+template <uint32_t F, uint32_t E, uint32_t B, bool SYM = false, bool BFS = true>
 struct BwSmemT {
     static constexpr uint32_t kF = F, kE = E, kB = B;
     static constexpr bool kSym = SYM;
+    static constexpr bool kBfs = BFS;  // false: leaves from the traversal kernel's cache only
     union {
         struct {
             uint32_t fa[F], fb[F];  // traversal frontier, then per-leaf candidate prefix
@@ -61,7 +66,8 @@ struct BwSmemT {
         uint8_t ebuf[B];  // encoder output (after the masks: the frontier is dead)
     } u;
     float4 sa[4][32];  // staged j pairs [p][candidate]: {x_2p, x_2p+1, y_2p, y_2p+1}
-    float4 sz[4][32];  //                                 {z_2p, z_2p+1, -, -}
+    // {z_2p, z_2p+1 (, -, -)}: 16-byte rows measured faster in the traversing kernel
+    std::conditional_t<BFS && !kBwSz8, float4, float2> sz[4][32];
     float4 ia[64];     // [ii*8 + b] {x, y, z, lo} SC frame + cutoff threshold (guard band below)
     float ihi[64];     // [ii*8 + b] hi threshold (guard band above)
     float iab[8][6];
@@ -73,6 +79,9 @@ struct BwSmemT {
     BwSymJ<SYM> sy;
 };
 using BwSmem = BwSmemT<kBwF, kBwE, kBwBytes>;
+// gather main tier after the traversal kernel (k_halo_warp fills the leaf cache, <= 256
+// leaves per SC): no traversal code, SCs without cached leaves go to the medium tier
+using BwSmemCached = BwSmemT<kLeafCacheCap, kBwE, 2048, false, false>;
 using BwSmemM = BwSmemT<1024, 1024, 8192>;
 using BwSmemSym = BwSmemT<kBwF, kBwE, kBwBytes, true>;
 using BwSmemMSym = BwSmemT<1024, 1024, 8192, true>;
@@ -353,7 +362,10 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
             fa = S.u.t.fa, nA = cnt;
         }
     }
-    if (nA == ~0u) nA = warp_bfs(A, scg, r2, S.u.t.fa, S.u.t.fb, &fa, Sm::kF);
+    if (nA == ~0u) {
+        if constexpr (Sm::kBfs) nA = warp_bfs(A, scg, r2, S.u.t.fa, S.u.t.fb, &fa, Sm::kF);
+        else return false;  // not cached: the medium tier traverses
+    }
     if (nA == ~0u) return false;
     uint32_t* fb = fa == S.u.t.fa ? S.u.t.fb : S.u.t.fa;
 
@@ -507,7 +519,7 @@ __device__ bool build_sc_warp(const BuildArgs& A, Sm& S, uint64_t sc) {
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
                     const float4 a = S.sa[p][lane];
-                    const float4 z = S.sz[p][lane];
+                    const auto z = S.sz[p][lane];
                     if (a.x != 1e30f) {
                         jlo[0] = fminf(jlo[0], a.x), jhi[0] = fmaxf(jhi[0], a.x);
                         jlo[1] = fminf(jlo[1], a.z), jhi[1] = fmaxf(jhi[1], a.z);
@@ -777,7 +789,8 @@ __global__ void __launch_bounds__(256) k_halo_warp(const __grid_constant__ Build
         }
         for (uint32_t k = lane; k < nA; k += 32) {
             const Node nd = A.nodes[fa[k] & ~kTag];
-            for (uint32_t j = nd.pbegin / A.cj; j <= (nd.pend - 1) / A.cj; ++j) jflags[j] = 1;
+            if (jflags)
+                for (uint32_t j = nd.pbegin / A.cj; j <= (nd.pend - 1) / A.cj; ++j) jflags[j] = 1;
             if (A.leaf_cache && nA <= kLeafCacheCap) A.leaf_cache[(sc - A.leaf_sc0) * kLeafCacheCap + k] = fa[k];
         }
         if (A.leaf_count && lane == 0) A.leaf_count[sc - A.leaf_sc0] = nA <= kLeafCacheCap ? nA : ~0u;
