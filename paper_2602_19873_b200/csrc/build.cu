@@ -554,7 +554,7 @@ __global__ void k_validate(uint64_t n, const double* __restrict__ x, const doubl
 }
 
 #ifndef SFCNL_TRAV_CTAS
-#define SFCNL_TRAV_CTAS 3
+#define SFCNL_TRAV_CTAS 6
 #endif
 constexpr int kTravCtas = SFCNL_TRAV_CTAS;  // CTAs (8 warps) per SM of the traversal kernel
 
