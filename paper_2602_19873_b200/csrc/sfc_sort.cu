@@ -86,16 +86,35 @@ __device__ __forceinline__ uint64_t hilbert_key(uint32_t gx, uint32_t gy, uint32
 }
 
 // grid_coords(box.wrap(p)) for one axis (core.hpp:65-73, hilbert.hpp:94-107).
-__device__ __forceinline__ uint32_t grid_axis(double p, const Box& b, int d, double cells) {
+// Two exact shortcuts around the fp64 divisions (values unchanged):
+//  * wrap: for lo <= p with fl(p - lo) < L, fl(fl(p - lo) / L) < 1 (division is monotone and
+//    fl(L / L) = 1), so floor(.) = 0 and p - L * 0 == p: the division is skipped;
+//  * cell: cells = 2^bits, so fl(q) * cells is exact and the cell is floor(fl(q) * cells)
+//    with q = fl(p - lo) / len. f' = fl(p - lo) * inv_len * cells (inv_len = fl(1 / len)) is
+//    within a few ulps of it (|f' - f| < 2^-48 f <= 2^-27 here), so floor(f') is the cell
+//    unless f' lies within 2^-20 of an integer; only then is the exact division evaluated.
+__device__ __forceinline__ uint32_t grid_axis(double p, const Box& b, int d, double cells, double inv_len) {
     if (b.per[d]) {
         const double L = b.len[d];
-        p = dsub(p, dmul(L, floor(ddiv(dsub(p, b.lo[d]), L))));
-        if (p >= b.hi[d]) p = b.lo[d];
+        const double r = dsub(p, b.lo[d]);
+        if (!(r >= 0.0 && r < L)) {
+            p = dsub(p, dmul(L, floor(ddiv(r, L))));
+            if (p >= b.hi[d]) p = b.lo[d];
+        }
     }
-    double f = dmul(ddiv(dsub(p, b.lo[d]), b.len[d]), cells);
-    if (f < 0) f = 0;
-    double c = floor(f);
-    if (c > cells - 1) c = cells - 1;
+    const double r = dsub(p, b.lo[d]);
+    const double fa = dmul(dmul(r, inv_len), cells);
+    const double fl_ = floor(fa);
+    double c;
+    if (fa - fl_ > 9.5367431640625e-07 && fa - fl_ < 1.0 - 9.5367431640625e-07 && fa < cells - 1.0) {
+        c = fl_;
+    } else {
+        double f = dmul(ddiv(r, b.len[d]), cells);
+        if (f < 0) f = 0;
+        c = floor(f);
+        if (c > cells - 1) c = cells - 1;
+    }
+    if (c < 0) c = 0;
     return uint32_t(c);
 }
 
@@ -113,6 +132,7 @@ __global__ void __launch_bounds__(kBlockKeys) k_keygen(uint64_t n, const double*
     for (int k = threadIdx.x; k < 8 * 256; k += blockDim.x) (&sh[0][0])[k] = 0;
     __syncthreads();
     const double cells = double(uint64_t(1) << bits);
+    const double inv_len[3] = {1.0 / box.len[0], 1.0 / box.len[1], 1.0 / box.len[2]};
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
         const double px = x[i], py = y[i], pz = z[i];
@@ -120,8 +140,8 @@ __global__ void __launch_bounds__(kBlockKeys) k_keygen(uint64_t n, const double*
         if (!isfinite(px) || !isfinite(py) || !isfinite(pz)) {
             raise_error(err, i, SFCNL_INPUT_ERROR, 1, 0);
         } else {
-            key = hilbert_key(grid_axis(px, box, 0, cells), grid_axis(py, box, 1, cells),
-                              grid_axis(pz, box, 2, cells), bits, tab);
+            key = hilbert_key(grid_axis(px, box, 0, cells, inv_len[0]), grid_axis(py, box, 1, cells, inv_len[1]),
+                              grid_axis(pz, box, 2, cells, inv_len[2]), bits, tab);
         }
         keys[i] = key;
         vals[i] = uint32_t(i);
