@@ -675,12 +675,14 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
     c->store_n = n;
     c->num_sc = num_sc;
     c->has_store = false;
+    ++c->store_gen;
     SFCNL_CUDA_TRY(c->counts.reserve(std::max<uint64_t>(num_sc, 1) * 4));
     SFCNL_CUDA_TRY(c->offsets.reserve((num_sc + 1) * 8));
     if (num_sc == 0) {
         SFCNL_CUDA_TRY(cudaMemsetAsync(c->offsets.p, 0, 8, c->stream));
         c->blob_bytes = 0;
         c->has_store = true;
+        ++c->store_gen;
         return 0;
     }
     {
@@ -846,6 +848,7 @@ int run_build_store(sfcnl_cu_ctx* c, const sfcnl_build_params& p, uint64_t sc0, 
     stage_end(c, kEncode);
     c->blob_bytes = blob_bytes;
     c->has_store = true;
+    ++c->store_gen;
     return 0;
 }
 

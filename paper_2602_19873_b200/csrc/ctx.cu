@@ -476,6 +476,7 @@ int sfcnl_cu_set_store(sfcnl_cu_ctx* c, const sfcnl_build_params* p, uint64_t n,
     c->num_sc = num_sc;
     c->blob_bytes = blob_bytes;
     c->has_store = true;
+    ++c->store_gen;
     c->sc_base = 0;
     return finish(c);
 }
@@ -622,6 +623,7 @@ int sfcnl_cu_alloc_sorted(sfcnl_cu_ctx* c, uint64_t n, const sfcnl_box* box, con
     s.n = n;
     s.box = make_box(box);
     c->has_store = false;
+    ++c->store_gen;
     drop_external(c);
     for (DBuf* b : {&s.x, &s.y, &s.z, &s.h}) SFCNL_CUDA_TRY(b->reserve(std::max<uint64_t>(n, 1) * 8));
     // keep the allocations of fields that survive (steps re-allocate the same set)

@@ -118,6 +118,9 @@ struct sfcnl_cu_ctx {
 
     // (4) store
     bool has_store = false;
+    uint64_t store_gen = 0;                   // bumped whenever the store changes
+    sfcnl_cu::DBuf dec_idx, dec_base;         // the store's decoded index lists (pass.cu), for store_gen
+    uint64_t dec_gen = ~0ull;
     sfcnl_build_params sp{};
     bool clgeo_whole = false;  // igeo/jgeo hold every cluster of the current sorted set (device_array)
     uint64_t store_n = 0, num_sc = 0, blob_bytes = 0;

@@ -355,6 +355,7 @@ int sfcnl_cu_dd_place(sfcnl_cu_ctx* c, uint64_t n_global, uint64_t p0, uint64_t 
                halo_rows, tab_out);
     if (n_local) launch(c, k_dd_fill, dim3(blocks(n_local)), dim3(256), 0, n_local, cj, (const uint32_t*)lc2g, ncols, tab_out);
     c->has_store = false;
+    ++c->store_gen;
     return finish_dd(c);
 }
 
@@ -369,6 +370,7 @@ int sfcnl_cu_dd_localize(sfcnl_cu_ctx* c, uint32_t cj, const uint32_t* lpos, con
     c->dd_lc2g = lc2g;
     c->dd_g2l = lpos;
     c->has_store = false;
+    ++c->store_gen;
     drop_external(c);
     return finish_dd(c);
 }

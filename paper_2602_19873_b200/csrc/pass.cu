@@ -72,6 +72,8 @@ struct PassArgs {
     double* out[4];
     uint32_t* cnt;
     const uint32_t* g2l;  // domain decomposition (dd.cu): decoded global cluster id -> local, or null
+    const uint32_t* dec;       // the store's decoded index lists (k_decode_store), or null: decode in the pass
+    const uint64_t* dec_base;  // first decoded entry of SC sc_begin + s
     DevError* err;
 };
 
@@ -350,6 +352,97 @@ __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& 
 #include "pass_symf.cuh"
 #include "pass_x64.cuh"
 
+// One decode per store (codec::decode_into, nibble_codec.cpp:136-178, with
+// decode_entry_indices' checks, neighbor_store.cpp:18-42), shared by every pass over it:
+// warp per SC, raw cluster ids (the domain decomposition's g2l map is applied by the
+// passes), errors recorded exactly as the passes record them.
+__global__ void __launch_bounds__(256) k_decode_store(const __grid_constant__ PassArgs A, uint32_t* __restrict__ dec,
+                                                      unsigned long long* __restrict__ work) {
+    __shared__ uint32_t sidx[8][64];
+    const unsigned lane = lane_id(), wp = threadIdx.x >> 5;
+    const uint32_t w = uint32_t(A.w);
+    for (;;) {
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(work, 1ull);
+        const uint64_t sc = A.sc_begin + __shfl_sync(0xffffffffu, t, 0);
+        if (sc >= A.num_sc) break;
+        const uint32_t count = A.counts[sc];
+        if (!count) continue;
+        const uint64_t begin = A.offsets[sc], end = A.offsets[sc + 1];
+        const uint64_t mb = uint64_t(count) * A.mask_bytes;
+        if (begin + mb > end) {
+            if (lane == 0) raise_error(A.err, sc, SFCNL_DECODE_ERROR, kMsgMaskSlice, begin);
+            continue;
+        }
+        const uint8_t* idata = A.blob + begin + mb;
+        const uint64_t ilen = end - begin - mb;
+        uint32_t* out = dec + A.dec_base[sc - A.sc_begin];
+        if (!A.compress) {
+            if (ilen != uint64_t(count) * 4) {
+                if (lane == 0) raise_error(A.err, sc, SFCNL_DECODE_ERROR, kMsgRawLen, ilen);
+                continue;
+            }
+            for (uint32_t k = lane; k < count; k += 32) {
+                const uint8_t* p = idata + 4ull * k;
+                out[k] = uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16) | (uint32_t(p[3]) << 24);
+            }
+            continue;
+        }
+        uint64_t pos = 0, running = 0;
+        for (uint32_t bb = 0; bb < count; bb += w) {
+            const uint32_t len = tmin<uint32_t>(w, count - bb);
+            uint64_t off = 0;
+            int msg = 0;
+            const uint64_t np2 = warp_decode_block(idata, ilen, pos, len, int(w), running, sidx[wp], &off, &msg);
+            if (np2 == ~0ull) {
+                if (lane == 0) raise_error(A.err, sc, SFCNL_DECODE_ERROR, msg, off);
+                break;
+            }
+            pos = np2;
+            if (bb + len == count && pos != ilen) {
+                if (lane == 0) raise_error(A.err, sc, SFCNL_DECODE_ERROR, kMsgTrailing, pos);
+                break;
+            }
+            __syncwarp();
+            for (uint32_t k = lane; k < len; k += 32) out[bb + k] = sidx[wp][k];
+            __syncwarp();
+        }
+    }
+}
+
+// The decoded lists of the current store (decoded once per store generation).
+int ensure_decoded(sfcnl_cu_ctx* c, PassArgs& A) {
+    A.dec = nullptr, A.dec_base = nullptr;
+    if (getenv("SFCNL_NO_PREDECODE")) return 0;
+    const uint64_t num_sc = A.num_sc - A.sc_begin;
+    if (num_sc == 0) return 0;
+    if (c->dec_gen != c->store_gen) {
+        SFCNL_CUDA_TRY(c->dec_base.reserve((num_sc + 1) * 8));
+        if (int rc = excl_scan(c, A.counts + A.sc_begin, c->dec_base.as<uint64_t>(), num_sc)) return rc;
+        uint64_t total = 0;
+        if (int rc_rb = readback(c, &total, c->dec_base.as<uint64_t>() + num_sc, 8)) return rc_rb;
+        SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        SFCNL_CUDA_TRY(c->dec_idx.reserve(std::max<uint64_t>(total, 1) * 4));
+        A.dec_base = c->dec_base.as<const uint64_t>();
+        SFCNL_CUDA_TRY(c->work_ctr.reserve(8));
+        SFCNL_CUDA_TRY(cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream));
+        const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((num_sc + 7) / 8, uint64_t(c->num_sms) * 8)));
+        launch(c, k_decode_store, dim3(grid), dim3(256), 0, A, c->dec_idx.as<uint32_t>(), c->work_ctr.as<unsigned long long>());
+        SFCNL_CUDA_TRY(cudaGetLastError());
+        DevError e{};
+        if (int rc_rb = readback(c, &e, c->derr.p, sizeof(DevError))) return rc_rb;
+        SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        if (e.key != ~0ull) {  // a malformed store: the pass decodes (and reports) it itself
+            A.dec_base = nullptr;
+            return 0;
+        }
+        c->dec_gen = c->store_gen;
+    }
+    A.dec = c->dec_idx.as<const uint32_t>();
+    A.dec_base = c->dec_base.as<const uint64_t>();
+    return 0;
+}
+
 template <int K, int CJ>
 void launch_pass_warp(sfcnl_cu_ctx* c, const PassArgs& A) {
     const size_t smem = pw_smem<K>();
@@ -621,6 +714,8 @@ int run_reduce(sfcnl_cu_ctx* c, const sfcnl_pass_params& p) {
     A.err = c->derr.as<DevError>();
     A.g2l = c->dd_g2l;
     stage_begin(c, kPass);
+    if (!symmetric && A.ci == 8 && (A.cj == 8 || A.cj == 4))
+        if (int rc = ensure_decoded(c, A)) return rc;
     if (symmetric) {
         const bool sym_fast = p.precision == 1 && c->sp.ci == 8 && (c->sp.cj == 8 || c->sp.cj == 4) &&
                               !getenv("SFCNL_SYM_EXACT");

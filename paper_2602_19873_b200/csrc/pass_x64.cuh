@@ -181,7 +181,10 @@ __global__ void __launch_bounds__(kPxWarps * 32, 3) k_pass_x64(const __grid_cons
         for (uint32_t bb = 0; !bad && bb < count; bb += w) {
             const uint32_t len = tmin<uint32_t>(w, count - bb);
             // ---- decode one codec block into S.idx[0, len)
-            if (A.compress) {
+            if (A.dec) {  // decoded once per store (k_decode_store)
+                const uint32_t* src = A.dec + A.dec_base[sc - A.sc_begin] + bb;
+                for (uint32_t k = lane; k < len; k += 32) S.idx[k] = src[k];
+            } else if (A.compress) {
                 uint64_t off = 0;
                 int msg = 0;
                 const uint64_t np2 = warp_decode_block(idata, ilen, pos, len, int(w), running, S.idx, &off, &msg);
