@@ -356,16 +356,99 @@ __device__ __noinline__ void sc_exact(const PassArgs& A, uint64_t sc, ScStream& 
 // decode_entry_indices' checks, neighbor_store.cpp:18-42), shared by every pass over it:
 // warp per SC, raw cluster ids (the domain decomposition's g2l map is applied by the
 // passes), errors recorded exactly as the passes record them.
-__global__ void __launch_bounds__(256) k_decode_store(const __grid_constant__ PassArgs A, uint32_t* __restrict__ dec,
-                                                      unsigned long long* __restrict__ work) {
-    __shared__ uint32_t sidx[8][64];
+constexpr uint32_t kDecStage = 1024;  // bytes of an SC's index data staged in shared memory per warp
+constexpr uint32_t kDecSlack = 16;    // readable bytes past the staged data (word windows)
+
+__device__ __forceinline__ uint32_t nib_rev32(uint32_t x) {  // nibble order reversed
+    x = __byte_perm(x, 0, 0x0123);
+    return ((x >> 4) & 0x0F0F0F0Fu) | ((x & 0x0F0F0F0Fu) << 4);
+}
+// 8 bytes starting at p (shared memory, any alignment) as a little-endian word
+__device__ __forceinline__ uint64_t smem_win8(const uint8_t* p) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+    const uint32_t sh = 8u * uint32_t(a & 3), w0 = w[0], w1 = w[1], w2 = w[2];
+    return (uint64_t(__funnelshift_r(w1, w2, sh)) << 32) | __funnelshift_r(w0, w1, sh);
+}
+
+// warp_decode_block over the staged shared-memory copy (bytes [0, size) valid, kDecSlack
+// readable beyond): a difference's nibbles come from one 8-byte window (nibble-reversed
+// instead of a dependent byte loop), and the sums run in 32 bits -- the outputs are the
+// low 32 bits of the same sums, the error checks and offsets are warp_decode_block's
+template <int NS>  // element slots per lane: 1 for w <= 32, 2 for w = 64
+__device__ __forceinline__ uint32_t warp_decode_block_s(const uint8_t* data, uint32_t size, uint32_t pos, uint32_t len,
+                                                        int w, uint32_t& running, uint32_t* out, uint64_t* err_off,
+                                                        int* err_msg) {
+    const unsigned lane = lane_id();
+    const uint32_t mbytes = uint32_t(w) / 8;
+    if (pos + mbytes > size) {
+        *err_off = pos;
+        *err_msg = kMsgTruncMask;
+        return ~0u;
+    }
+    const uint64_t win = smem_win8(data + pos);
+    const unsigned long long bm = mbytes == 8 ? win : (win & ((1ull << (8 * mbytes)) - 1ull));
+    const unsigned long long used = len == 64 ? bm : (bm & ((1ull << len) - 1ull));
+    const uint32_t ninfo = __popcll(used);
+    const uint32_t nib0 = (pos + mbytes) * 2, limit = size * 2;
+    if (nib0 + ninfo > limit) {
+        *err_off = size;
+        *err_msg = kMsgTruncNib;
+        return ~0u;
+    }
+    uint32_t nd[2] = {0, 0}, info[2] = {0, 0}, isset[2] = {0, 0};
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const uint32_t k = lane + 32u * s;
+        isset[s] = ((used >> k) & 1ull) ? 1u : 0u;
+        if (isset[s]) {
+            const uint32_t t = nib0 + __popcll(used & ((1ull << k) - 1ull));
+            info[s] = (data[t >> 1] >> (4 * (t & 1))) & 15u;
+            nd[s] = info[s] < 8 ? info[s] + 1 : 0;
+        }
+    }
+    const uint32_t inc0 = warp_incl_scan(nd[0]);
+    const uint32_t tot0 = __shfl_sync(0xffffffffu, inc0, 31);
+    const uint32_t inc1 = NS == 2 ? warp_incl_scan(nd[1]) : 0u;
+    const uint32_t ndata = tot0 + (NS == 2 ? __shfl_sync(0xffffffffu, inc1, 31) : 0u);
+    if (nib0 + ninfo + ndata > limit) {
+        *err_off = size;
+        *err_msg = kMsgTruncNib;
+        return ~0u;
+    }
+    uint32_t dv[2] = {1, 1};
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        if (isset[s]) {
+            if (info[s] >= 8) {
+                dv[s] = info[s] - 6;
+            } else {
+                const uint32_t t = nib0 + ninfo + (s == 0 ? inc0 - nd[0] : tot0 + inc1 - nd[1]);
+                const uint32_t seg = uint32_t(smem_win8(data + (t >> 1)) >> (4 * (t & 1)));
+                dv[s] = nib_rev32(seg) >> (32 - 4 * nd[s]);
+            }
+        }
+    }
+    const uint32_t a = warp_incl_scan(dv[0]);
+    const uint32_t atot = __shfl_sync(0xffffffffu, a, 31);
+    if (lane < len) out[lane] = running + a - 1;
+    if (NS == 2) {
+        const uint32_t b = warp_incl_scan(dv[1]) + atot;
+        if (lane + 32 < len) out[lane + 32] = running + b - 1;
+        running += __shfl_sync(0xffffffffu, b, 31) - (uint32_t(w) - len);
+    } else {
+        running += atot - (uint32_t(w) - len);
+    }
+    return pos + mbytes + (ninfo + ndata + 1) / 2;
+}
+__global__ void __launch_bounds__(256) k_decode_store(const __grid_constant__ PassArgs A, uint32_t* __restrict__ dec) {
+    __shared__ __align__(16) uint8_t sbuf[8][kDecStage];
     const unsigned lane = lane_id(), wp = threadIdx.x >> 5;
     const uint32_t w = uint32_t(A.w);
-    for (;;) {
-        unsigned long long t = 0;
-        if (lane == 0) t = atomicAdd(work, 1ull);
-        const uint64_t sc = A.sc_begin + __shfl_sync(0xffffffffu, t, 0);
-        if (sc >= A.num_sc) break;
+    // static warp-strided SCs: the decode cost per SC is nearly uniform, and one shared
+    // work counter (a same-address atomic per SC) capped the kernel at ~2.3 ms for 2^20 SCs
+    const uint64_t nwarps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    for (uint64_t sc = A.sc_begin + uint64_t(blockIdx.x) * (blockDim.x >> 5) + wp; sc < A.num_sc; sc += nwarps) {
         const uint32_t count = A.counts[sc];
         if (!count) continue;
         const uint64_t begin = A.offsets[sc], end = A.offsets[sc + 1];
@@ -388,12 +471,53 @@ __global__ void __launch_bounds__(256) k_decode_store(const __grid_constant__ Pa
             }
             continue;
         }
+        // stage the index data in one coalesced sweep (aligned words, head / tail bytes);
+        // the block decodes then read shared memory instead of dependent global byte loads
+        const uint8_t* src = idata;
+        const bool staged = ilen + 3 + kDecSlack <= kDecStage;
+        if (staged) {
+            const uint64_t gs = reinterpret_cast<uint64_t>(idata), ge = gs + ilen;
+            const uint64_t ws = (gs + 3) & ~3ull, we = ge & ~3ull;
+            uint8_t* base = sbuf[wp] + (gs & 3);  // base[a - gs] holds the byte at address a
+            if (ws < we) {
+                const uint32_t* g = reinterpret_cast<const uint32_t*>(ws);
+                uint32_t* d = reinterpret_cast<uint32_t*>(base + (ws - gs));
+                for (uint32_t k = lane; k < uint32_t((we - ws) >> 2); k += 32) d[k] = __ldg(g + k);
+                if (lane < ws - gs) base[lane] = idata[lane];
+                if (lane < ge - we) base[(we - gs) + lane] = idata[(we - gs) + lane];
+            } else {
+                for (uint32_t k = lane; k < ilen; k += 32) base[k] = idata[k];
+            }
+            __syncwarp();
+            src = base;
+        }
+        if (staged) {
+            uint32_t pos = 0, running = 0;
+            for (uint32_t bb = 0; bb < count; bb += w) {
+                const uint32_t len = tmin<uint32_t>(w, count - bb);
+                uint64_t off = 0;
+                int msg = 0;
+                const uint32_t np2 = w > 32 ? warp_decode_block_s<2>(src, uint32_t(ilen), pos, len, int(w), running, out + bb, &off, &msg)
+                                            : warp_decode_block_s<1>(src, uint32_t(ilen), pos, len, int(w), running, out + bb, &off, &msg);
+                if (np2 == ~0u) {
+                    if (lane == 0) raise_error(A.err, sc, SFCNL_DECODE_ERROR, msg, off);
+                    break;
+                }
+                pos = np2;
+                if (bb + len == count && pos != ilen) {
+                    if (lane == 0) raise_error(A.err, sc, SFCNL_DECODE_ERROR, kMsgTrailing, pos);
+                    break;
+                }
+            }
+            __syncwarp();  // the staging buffer is reused by the next SC
+            continue;
+        }
         uint64_t pos = 0, running = 0;
         for (uint32_t bb = 0; bb < count; bb += w) {
             const uint32_t len = tmin<uint32_t>(w, count - bb);
             uint64_t off = 0;
             int msg = 0;
-            const uint64_t np2 = warp_decode_block(idata, ilen, pos, len, int(w), running, sidx[wp], &off, &msg);
+            const uint64_t np2 = warp_decode_block(src, ilen, pos, len, int(w), running, out + bb, &off, &msg);
             if (np2 == ~0ull) {
                 if (lane == 0) raise_error(A.err, sc, SFCNL_DECODE_ERROR, msg, off);
                 break;
@@ -403,10 +527,8 @@ __global__ void __launch_bounds__(256) k_decode_store(const __grid_constant__ Pa
                 if (lane == 0) raise_error(A.err, sc, SFCNL_DECODE_ERROR, kMsgTrailing, pos);
                 break;
             }
-            __syncwarp();
-            for (uint32_t k = lane; k < len; k += 32) out[bb + k] = sidx[wp][k];
-            __syncwarp();
         }
+        __syncwarp();  // the staging buffer is reused by the next SC
     }
 }
 
@@ -424,10 +546,8 @@ int ensure_decoded(sfcnl_cu_ctx* c, PassArgs& A) {
         SFCNL_CUDA_TRY(cudaStreamSynchronize(c->stream));
         SFCNL_CUDA_TRY(c->dec_idx.reserve(std::max<uint64_t>(total, 1) * 4));
         A.dec_base = c->dec_base.as<const uint64_t>();
-        SFCNL_CUDA_TRY(c->work_ctr.reserve(8));
-        SFCNL_CUDA_TRY(cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream));
         const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((num_sc + 7) / 8, uint64_t(c->num_sms) * 8)));
-        launch(c, k_decode_store, dim3(grid), dim3(256), 0, A, c->dec_idx.as<uint32_t>(), c->work_ctr.as<unsigned long long>());
+        launch(c, k_decode_store, dim3(grid), dim3(256), 0, A, c->dec_idx.as<uint32_t>());
         SFCNL_CUDA_TRY(cudaGetLastError());
         DevError e{};
         if (int rc_rb = readback(c, &e, c->derr.p, sizeof(DevError))) return rc_rb;
