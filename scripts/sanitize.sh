@@ -10,8 +10,8 @@ for tool in memcheck racecheck initcheck synccheck; do
   echo "smoke $tool rc=$?" | tee -a $D/summary.txt
 done
 for tool in memcheck racecheck; do
-  timeout 1500 $CS --tool $tool --error-exitcode 9 python -m pytest tests/test_gpu_edge.py tests/test_gpu_errors.py tests/test_gpu_x64.py -x -q -p no:cacheprovider \
+  timeout 1500 $CS --tool $tool --error-exitcode 9 python -m pytest tests/test_gpu_edge.py tests/test_gpu_errors.py tests/test_gpu_x64.py tests/test_gpu_predecode.py -x -q -p no:cacheprovider \
     > $D/edge_$tool.log 2>&1
-  echo "edge+errors+x64 $tool rc=$? $(tail -1 $D/edge_$tool.log)" | tee -a $D/summary.txt
+  echo "edge+errors+x64+predecode $tool rc=$? $(tail -1 $D/edge_$tool.log)" | tee -a $D/summary.txt
 done
 grep -h "ERROR SUMMARY" $D/*.log | sort | uniq -c | tee -a $D/summary.txt
