@@ -84,12 +84,16 @@ def sc_partition(n_total: int, world: int):
 class Comm:
     """Collectives over a torch.distributed process group on the engine's tensors."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, always: bool = False):
+        """always (or SFCNL_COMM_ALWAYS=1): issue the collectives at world size 1 too
+        instead of short-circuiting them (exercises the NCCL path on one GPU)."""
+        import os
         dist = _torch().distributed
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.staged = dist.get_backend(group) != "nccl"
+        self.alone = self.world == 1 and not (always or os.environ.get("SFCNL_COMM_ALWAYS") == "1")
 
     def _in(self, t):
         return t.cpu() if (self.staged and t.is_cuda) else t
@@ -97,7 +101,7 @@ class Comm:
     def allreduce_(self, t, op="sum"):
         dist = _torch().distributed
         o = {"sum": dist.ReduceOp.SUM, "min": dist.ReduceOp.MIN, "max": dist.ReduceOp.MAX}[op]
-        if self.world == 1:
+        if self.alone:
             return t
         c = self._in(t)
         dist.all_reduce(c, op=o, group=self.group)
@@ -108,7 +112,7 @@ class Comm:
     def all_gather(self, t):
         """Equal-size all-gather along dim 0 -> [world, *t.shape]."""
         torch = _torch()
-        if self.world == 1:
+        if self.alone:
             return t.unsqueeze(0).clone()
         c = self._in(t.contiguous())
         out = torch.empty((self.world * c.shape[0],) + tuple(c.shape[1:]), dtype=c.dtype, device=c.device)
@@ -118,7 +122,7 @@ class Comm:
     def all_gather_v(self, t, counts: Sequence[int]):
         """Concatenation over ranks of t (dim 0), rank q contributing counts[q] rows."""
         torch = _torch()
-        if self.world == 1:
+        if self.alone:
             return t.clone()
         m = max(max(counts), 1)
         pad = torch.zeros((m,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
@@ -128,7 +132,7 @@ class Comm:
 
     def all_to_all_v(self, t, send: Sequence[int], recv: Sequence[int]):
         torch = _torch()
-        if self.world == 1:
+        if self.alone:
             return t.clone()
         c = self._in(t.contiguous())
         out = torch.empty((int(sum(recv)),) + tuple(c.shape[1:]), dtype=c.dtype, device=c.device)

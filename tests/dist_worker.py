@@ -34,7 +34,12 @@ def shares(n, world):
 
 def main():
     out_dir, cfg = sys.argv[1], json.loads(sys.argv[2])
-    dist.init_process_group(cfg.get("backend", "gloo"))
+    if cfg.get("backend", "gloo") == "nccl":
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     from oracle.oracle import Oracle
     o = Oracle("port")

@@ -94,7 +94,7 @@ def check(parts, cfg, exact=True):
                 assert np.array_equal(got, ref), (k, j)
             else:
                 assert np.allclose(got, ref, rtol=1e-5, atol=1e-5 * np.abs(ref).max()), (k, j)
-    assert all(int(p["halo"]) > 0 for p in parts)
+    assert len(parts) == 1 or all(int(p["halo"]) > 0 for p in parts)  # one rank: no halo
     t = single_domain.tree
     for p in parts:  # every rank holds the single-domain octree (distributed build)
         if "t_kf" in p:
@@ -115,6 +115,14 @@ CPU_CASES = [
 def test_domain_decomposition_oracle_engine(tmp_path, world, case):
     cfg = dict(CPU_CASES[case], engine="oracle")
     check(launch(world, cfg, tmp_path), cfg)
+
+
+def test_domain_decomposition_one_rank_collectives_issued(tmp_path, monkeypatch):
+    """World size 1 with every collective issued (SFCNL_COMM_ALWAYS=1; the GPU twin of
+    this test runs it over NCCL) equals the single-domain run."""
+    monkeypatch.setenv("SFCNL_COMM_ALWAYS", "1")
+    cfg = dict(CPU_CASES[0], engine="oracle")
+    check(launch(1, cfg, tmp_path), cfg)
 
 
 def test_domain_decomposition_legacy_orchestration(tmp_path, monkeypatch):
@@ -153,6 +161,18 @@ def test_domain_decomposition_symmetric_fp64(tmp_path, world, case):
     order, so the distributed outputs are bit-equal to the single-domain reduce<double>."""
     cfg = dict(SYM_CASES[case], engine="cuda", precision=0)
     check(launch(world, cfg, tmp_path), cfg)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [0, 2])
+def test_domain_decomposition_nccl_one_rank(tmp_path, monkeypatch, case):
+    """The NCCL branch of Comm (device tensors: all_reduce SUM/MIN/MAX,
+    all_gather_into_tensor, all_to_all_single with split sizes) on the one GPU this
+    harness has: a world-1 NCCL group with the collectives issued instead of
+    short-circuited (SFCNL_COMM_ALWAYS=1) reproduces the single-domain run."""
+    monkeypatch.setenv("SFCNL_COMM_ALWAYS", "1")
+    cfg = dict(GPU_CASES[case], engine="cuda", precision=0, backend="nccl")
+    check(launch(1, cfg, tmp_path), cfg)
 
 
 @pytest.mark.gpu

@@ -57,3 +57,22 @@ def test_keys_at_cell_and_box_boundaries(ctx, box6, periodic):
     order = S.sort_by_sfc(ps, box, ctx=ctx)
     assert np.array_equal(order.keys, keys)
     assert np.array_equal(order.perm, perm)
+
+
+@pytest.mark.parametrize("nf", [0, 1, 2, 3, 5])
+@pytest.mark.parametrize("n", [1, 255, 256, 257, 100003])
+def test_apply_order_record_widths(ctx, nf, n):
+    """apply_sfc_order (hilbert.cpp:28-44) is a gather by perm for every record width:
+    4 + nf doubles per particle (the 4- and 6-wide records take the staged pack and the
+    16-byte gather, the others the per-double kernels), ragged tails of the 256-particle
+    pack blocks included."""
+    rng = np.random.default_rng(n + nf)
+    x, y, z, h = (rng.uniform(-1, 1, n) for _ in range(4))
+    fields = {f"f{k}": rng.standard_normal(n) for k in range(nf)}
+    perm = rng.permutation(n).astype(np.uint32)
+    keys = np.arange(n, dtype=np.uint64)
+    out = S.apply_sfc_order(S.ParticleSet(x, y, z, h, fields), S.SfcOrder(keys, perm, 21), ctx=ctx)
+    for a, b in ((out.x, x), (out.y, y), (out.z, z), (out.h, h)):
+        assert np.array_equal(a, b[perm])
+    for k in range(nf):
+        assert np.array_equal(out.fields[f"f{k}"], fields[f"f{k}"][perm])
