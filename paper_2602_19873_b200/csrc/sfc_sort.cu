@@ -281,8 +281,8 @@ __global__ void k_pack_records(uint64_t n, int narr, int stride, const double* c
         for (int a = 0; a < narr; ++a) rec[k * stride + a] = __ldg(src[a] + k);
 }
 
-// Even record widths (4 / 6 doubles, 16-byte aligned records): pack through shared memory
-// so the records leave as contiguous 16-byte stores, gather with 16-byte loads.
+// Records of 4-6 doubles: pack through shared memory so the records leave as contiguous
+// 16-byte stores; gather even widths (16-byte aligned records) with 16-byte loads.
 #ifndef SFCNL_PERMUTE_V2
 #define SFCNL_PERMUTE_V2 1
 #endif
@@ -298,8 +298,9 @@ __global__ void __launch_bounds__(256) k_pack_records_v(uint64_t n, const double
         }
         __syncthreads();
         const ulonglong2* sv = reinterpret_cast<const ulonglong2*>(s);
-        ulonglong2* dv = reinterpret_cast<ulonglong2*>(rec + b0 * NA);
+        ulonglong2* dv = reinterpret_cast<ulonglong2*>(rec + b0 * NA);  // 16-byte aligned: b0 % 256 == 0
         for (uint32_t k = threadIdx.x; k < m * NA / 2; k += 256) dv[k] = sv[k];
+        if ((m * NA) & 1u && threadIdx.x == 0) rec[b0 * NA + m * NA - 1] = s[m * NA - 1];  // odd width, odd tail
         __syncthreads();
     }
 }
@@ -466,12 +467,15 @@ int run_apply_order(sfcnl_cu_ctx* c, int64_t into) {
     const uint32_t* pm = c->perm.as<uint32_t>();
     const double* rc = c->records.as<double>();
     double* const* dt = (double* const*)(tbl + narr);
-    if (SFCNL_PERMUTE_V2 && (narr == 4 || narr == 6)) {
+    if (SFCNL_PERMUTE_V2 && narr >= 4 && narr <= 6) {
         const int gp = int(std::min<uint64_t>((n + 255) / 256, uint64_t(c->num_sms) * 8));
         const double* const* sp = (const double* const*)tbl;
         if (narr == 4) {
             launch(c, k_pack_records_v<4>, dim3(gp), dim3(256), 0, n, sp, c->records.as<double>());
             launch(c, k_gather_records_v<4>, dim3(grid), dim3(256), 0, n, pm, rc, dt);
+        } else if (narr == 5) {  // 40-byte records: 8-byte gather loads
+            launch(c, k_pack_records_v<5>, dim3(gp), dim3(256), 0, n, sp, c->records.as<double>());
+            launch(c, k_gather_records<5>, dim3(grid), dim3(256), 0, n, pm, narr, stride, rc, dt);
         } else {
             launch(c, k_pack_records_v<6>, dim3(gp), dim3(256), 0, n, sp, c->records.as<double>());
             launch(c, k_gather_records_v<6>, dim3(grid), dim3(256), 0, n, pm, rc, dt);
