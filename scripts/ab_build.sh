@@ -8,5 +8,6 @@ while [ $# -ge 2 ]; do
   name=$1; extra=$2; shift 2
   make -s OBJ=build_$name EXTRA="$extra" -j16 libsfcnl_b200.so 2>&1 | grep -E "error" || true
   mkdir -p ../abv/$name && mv libsfcnl_b200.so ../abv/$name/
+  rm -rf "build_$name"  # variant objects (would bloat the gpurun snapshot)
 done
 make -s -j16 libsfcnl_b200.so
