@@ -576,17 +576,24 @@ void launch_pass_warp(sfcnl_cu_ctx* c, const PassArgs& A) {
     launch(c, k_pass_warp<K, CJ>, dim3(grid), dim3(kPwWarps * 32), smem, A, c->work_ctr.as<unsigned long long>());
 }
 
-template <int K, int CJ>
-void launch_pass_item(sfcnl_cu_ctx* c, const PassArgs& A) {
+template <int K, int CJ, bool NM>
+void launch_pass_item_t(sfcnl_cu_ctx* c, const PassArgs& A) {
     const size_t smem = pi_smem<K>();
-    cudaFuncSetAttribute(k_pass_item<K, CJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_pass_item<K, CJ, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass_item<K, CJ>, kPiWarps * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass_item<K, CJ, NM>, kPiWarps * 32, smem);
     const uint64_t warps = A.num_sc - A.sc_begin;
     const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((warps + kPiWarps - 1) / kPiWarps,
                                                                             uint64_t(c->num_sms) * std::max(per_sm, 1))));
     cudaMemsetAsync(c->work_ctr.p, 0, 8, c->stream);
-    launch(c, k_pass_item<K, CJ>, dim3(grid), dim3(kPiWarps * 32), smem, A, c->work_ctr.as<unsigned long long>());
+    launch(c, k_pass_item<K, CJ, NM>, dim3(grid), dim3(kPiWarps * 32), smem, A, c->work_ctr.as<unsigned long long>());
+}
+
+template <int K, int CJ>
+void launch_pass_item(sfcnl_cu_ctx* c, const PassArgs& A) {
+    // density at query scale >= 1: W(q) = 0 beyond the support, so out-of-range slots need no mask
+    if (K == SFCNL_KERNEL_DENSITY && SFCNL_PI_NOMASK && A.qs >= 1.0) launch_pass_item_t<K, CJ, true>(c, A);
+    else launch_pass_item_t<K, CJ, false>(c, A);
 }
 
 template <int K>

@@ -64,7 +64,14 @@ constexpr size_t pi_smem() {
 __device__ __forceinline__ f2 f2lo(ulonglong2 v) { return v.x; }
 __device__ __forceinline__ f2 f2hi(ulonglong2 v) { return v.y; }
 
-template <int K, int CJ>
+// NM (density, query scale >= 1): a slot out of range has d2_f32 > hi = r^2 + guard with
+// r = qs h >= h, so its fp32 q is >= 1 up to the sqrt / 1/h rounding (~4e-7, below the
+// guard's relative margin) and W = max(1-q,0)^3 - 4 max(1/2-q,0)^3 is 0 -- no mask needed;
+// a guard-band slot (decided by the fp64 path) keeps an fp32 W below (1e-6)^3 W(0).
+#ifndef SFCNL_PI_NOMASK
+#define SFCNL_PI_NOMASK 1
+#endif
+template <int K, int CJ, bool NM = false>
 __global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : 5) k_pass_item(const __grid_constant__ PassArgs A,
                                                              unsigned long long* __restrict__ work) {
     constexpr bool LJ = PiSmem<K>::LJ;
@@ -412,7 +419,7 @@ __global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : 5) k_pass_i
                                     const f2 uu = f2p(fmaxf(u0_, 0.f), fmaxf(u1_, 0.f));
                                     const f2 t3 = f2mul(f2mul(tt, tt), tt), u3 = f2mul(f2mul(uu, uu), uu);
                                     const f2 wv = f2fma(f2p(-4.f, -4.f), u3, t3);
-                                    acc0 = f2fma(f2mul(f2hi(Jb[p]), f2p(ma, mb)), wv, acc0);
+                                    acc0 = f2fma(NM ? f2hi(Jb[p]) : f2mul(f2hi(Jb[p]), f2p(ma, mb)), wv, acc0);
                                 } else if (LJ) {
                                     // close pairs leave the fp32 sums (evaluated in fp64 below)
                                     const bool cla = ma != 0.f && d2a < close2, clb = mb != 0.f && d2b < close2;
