@@ -165,7 +165,10 @@ __global__ void k_digit_base(const uint32_t* hist, uint32_t* base, int npass) {
 }
 
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
+#ifndef SFCNL_SORT_ITEMS
+#define SFCNL_SORT_ITEMS 12
+#endif
+constexpr int kSortItems = SFCNL_SORT_ITEMS;  // keys per thread of a 256-thread tile
 constexpr int kTile = kSortThreads * kSortItems;
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
