@@ -71,8 +71,11 @@ __device__ __forceinline__ f2 f2hi(ulonglong2 v) { return v.y; }
 #ifndef SFCNL_PI_NOMASK
 #define SFCNL_PI_NOMASK 1
 #endif
+#ifndef SFCNL_PI_CTAS
+#define SFCNL_PI_CTAS 5
+#endif
 template <int K, int CJ, bool NM = false>
-__global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : 5) k_pass_item(const __grid_constant__ PassArgs A,
+__global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : SFCNL_PI_CTAS) k_pass_item(const __grid_constant__ PassArgs A,
                                                              unsigned long long* __restrict__ work) {
     constexpr bool LJ = PiSmem<K>::LJ;
     constexpr int NO = nout<K>();
