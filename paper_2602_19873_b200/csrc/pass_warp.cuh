@@ -78,6 +78,10 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
     PwSmem<K>& S = reinterpret_cast<PwSmem<K>*>(dsm)[threadIdx.x >> 5];
     const unsigned lane = lane_id();
     const uint32_t il = lane >> 2, jq = lane & 3;
+    // the lane's j-quarter base in the shared window, pinned in a register (an opaque
+    // mov keeps the compiler from re-deriving (e * 4 + jq) * stride in the entry loop)
+    uint32_t sjq;
+    asm volatile("mov.b32 %0, %1;" : "=r"(sjq) : "r"(uint32_t(__cvta_generic_to_shared(S.sj + jq * (LJ ? 12 : 8)))));
     const uint32_t w = uint32_t(A.w);
     const float sig2 = float(A.sigma * A.sigma);
     const float eps24 = float(24.0 * A.eps), eps4 = float(4.0 * A.eps);
@@ -317,13 +321,17 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                     };
                     auto load = [&](uint32_t e) {
                         Ld L;
-                        const ulonglong2* pb = reinterpret_cast<const ulonglong2*>(S.sj + (e * 4 + jq) * (LJ ? 12 : 8));
-                        const ulonglong2 P0 = pb[0], P1 = pb[1];
+                        // one IMAD per entry: the lane's j-quarter base is fixed per warp
+                        const uint32_t a = sjq + e * (4 * (LJ ? 12 : 8) * 4);
+                        ulonglong2 P0, P1;
+                        asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(P0.x), "=l"(P0.y) : "r"(a));
+                        asm volatile("ld.shared.v2.u64 {%0, %1}, [%2 + 16];" : "=l"(P1.x), "=l"(P1.y) : "r"(a));
                         L.dx = f2sub(xi2, P0.x);
                         L.dy = f2sub(yi2, P0.y);
                         L.dz = f2sub(zi2, P1.x);
                         if (LJ) {
-                            const ulonglong2 P2 = pb[2];  // {ly, lz} pairs; lx pair is P1.y
+                            ulonglong2 P2;  // {ly, lz} pairs; lx pair is P1.y
+                            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2 + 32];" : "=l"(P2.x), "=l"(P2.y) : "r"(a));
                             L.dx = f2add(L.dx, f2sub(lxi2, P1.y));
                             L.dy = f2add(L.dy, f2sub(lyi2, P2.x));
                             L.dz = f2add(L.dz, f2sub(lzi2, P2.y));
@@ -404,8 +412,11 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                             const f2 s2 = f2mul(f2p(A.sig2f, A.sig2f), inv2);
                             const f2 s6 = f2mul(f2mul(s2, s2), s2);
                             // 24 eps / 4 eps are applied at the flush (K == LJ)
-                            f2 cf = f2mul(inv2, f2mul(s6, f2fma(f2p(2.f, 2.f), s6, f2p(-1.f, -1.f))));
-                            f2 ee = f2fma(s6, s6, f2mul(s6, f2p(-1.f, -1.f)));
+                            // t = s6 - 1 (exact for s6 in [1/2, 2], where the factors cross zero),
+                            // 2 s6 - 1 = s6 + t: one instruction less than the fma/mul forms
+                            const f2 t = f2add(s6, f2p(-1.f, -1.f));
+                            f2 cf = f2mul(f2mul(s6, inv2), f2add(s6, t));
+                            f2 ee = f2mul(s6, t);  // LJ: fused into the energy sum below
                             if (K == SFCNL_KERNEL_LJ_COULOMB) {
                                 cf = f2mul(cf, f2p(eps24, eps24));
                                 ee = f2mul(ee, f2p(eps4, eps4));
@@ -423,7 +434,8 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                             acc0 = f2fma(cf, L.dx, acc0);
                             acc1 = f2fma(cf, L.dy, acc1);
                             acc2 = f2fma(cf, L.dz, acc2);
-                            acc3 = f2add(acc3, ee);
+                            if (K == SFCNL_KERNEL_LJ) acc3 = f2fma(s6, t, acc3);  // energy s6 (s6 - 1), fused
+                            else acc3 = f2add(acc3, ee);
                         }
                     };
                     unsigned ms = mine & selfm;
