@@ -387,7 +387,6 @@ __global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : SFCNL_PI_CT
                                 const float lzi = S.ic[ii * 8 + b];
                                 lxi2 = f2p(T.z, T.z), lyi2 = f2p(T.w, T.w), lzi2 = f2p(lzi, lzi);
                             }
-                            const f2 invh2 = f2p(I.w, I.w);
                             f2 acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0, nin = 0, nhi = 0;
                             uint32_t crow = 0;
                             const int iself = kSelf && self ? int(b * 8 + ii) - jl0 : -1;
@@ -412,14 +411,12 @@ __global__ void __launch_bounds__(kPiWarps * 32, PiSmem<K>::LJ ? 4 : SFCNL_PI_CT
                                 nhi = f2add(nhi, f2p(fset_le(d2a, hi), fset_le(d2b, hi)));
                                 if (K == SFCNL_KERNEL_DENSITY) {
                                     // W(q)/(2 sigma) = max(1-q,0)^3 - 4 max(1/2-q,0)^3
-                                    const f2 sq = f2p(sqrt_ftz(d2a), sqrt_ftz(d2b));
-                                    const f2 omq = f2fma(f2p(-1.f, -1.f), f2mul(sq, invh2), f2p(1.f, 1.f));
-                                    const f2 hmq = f2sub(omq, f2p(0.5f, 0.5f));
-                                    float t0_, t1_, u0_, u1_;
-                                    f2u(omq, t0_, t1_);
-                                    f2u(hmq, u0_, u1_);
-                                    const f2 tt = f2p(fmaxf(t0_, 0.f), fmaxf(t1_, 0.f));
-                                    const f2 uu = f2p(fmaxf(u0_, 0.f), fmaxf(u1_, 0.f));
+                                    // max(1 - q, 0) and max(1/2 - q, 0) as saturated scalar fmas
+                                    // (q = |d| / h >= 0, so the clamp at 1 never binds): four
+                                    // FFMA.SAT instead of FMUL2 + FFMA2 + FADD2 + four FMNMX
+                                    const float sa = sqrt_ftz(d2a), sb = sqrt_ftz(d2b);
+                                    const f2 tt = f2p(__saturatef(fmaf(-sa, I.w, 1.f)), __saturatef(fmaf(-sb, I.w, 1.f)));
+                                    const f2 uu = f2p(__saturatef(fmaf(-sa, I.w, 0.5f)), __saturatef(fmaf(-sb, I.w, 0.5f)));
                                     const f2 t3 = f2mul(f2mul(tt, tt), tt), u3 = f2mul(f2mul(uu, uu), uu);
                                     const f2 wv = f2fma(f2p(-4.f, -4.f), u3, t3);
                                     acc0 = f2fma(NM ? f2hi(Jb[p]) : f2mul(f2hi(Jb[p]), f2p(ma, mb)), wv, acc0);
