@@ -311,7 +311,6 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                     }
                     float inv_h = 0.f;
                     if (K == SFCNL_KERNEL_DENSITY) inv_h = S.iinvh[li];
-                    const f2 invh2 = f2p(inv_h, inv_h);
                     f2 acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0, cntf = 0;
                     double accd0 = 0.0, accd1 = 0.0, accd2 = 0.0, accd3 = 0.0;  // LJ close pairs (fp64)
 
@@ -396,13 +395,10 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                         cntf = f2add(cntf, m2);
                         if (K == SFCNL_KERNEL_DENSITY) {
                             // W(q)/(2 sigma) = max(1-q,0)^3 - 4 max(1/2-q,0)^3
-                            const f2 q = f2mul(f2p(sqrt_ftz(d2a), sqrt_ftz(d2b)), invh2);
-                            const f2 omq = f2sub(f2p(1.f, 1.f), q), hmq = f2sub(f2p(0.5f, 0.5f), q);
-                            float t0, t1, u0, u1;
-                            f2u(omq, t0, t1);
-                            f2u(hmq, u0, u1);
-                            const f2 t = f2p(fmaxf(t0, 0.f), fmaxf(t1, 0.f));
-                            const f2 u = f2p(fmaxf(u0, 0.f), fmaxf(u1, 0.f));
+                            // max(1 - q, 0), max(1/2 - q, 0) as saturated fmas (q >= 0)
+                            const float sa = sqrt_ftz(d2a), sb = sqrt_ftz(d2b);
+                            const f2 t = f2p(__saturatef(fmaf(-sa, inv_h, 1.f)), __saturatef(fmaf(-sb, inv_h, 1.f)));
+                            const f2 u = f2p(__saturatef(fmaf(-sa, inv_h, 0.5f)), __saturatef(fmaf(-sb, inv_h, 0.5f)));
                             const f2 t3 = f2mul(f2mul(t, t), t), u3 = f2mul(f2mul(u, u), u);
                             const f2 wv = f2fma(f2p(-4.f, -4.f), u3, t3);
                             acc0 = f2fma(f2mul(f2p(L.pma, L.pmb), m2), wv, acc0);
@@ -441,8 +437,12 @@ __global__ void __launch_bounds__(kPwWarps * 32, PwSmem<K>::kMinBlocks) k_pass_w
                     unsigned ms = mine & selfm;
                     mine &= ~selfm;
                     while (mine) {
-                        const uint32_t e1 = __ffs(mine) - 1;
-                        mine &= mine - 1;
+                        // highest entry first: FLO gives it directly (ffs needs a bit reversal),
+                        // BMSK keeps the bits below it (no shifted-one constant to hold)
+                        uint32_t e1, below;
+                        asm("bfind.u32 %0, %1;" : "=r"(e1) : "r"(mine));
+                        asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(below) : "r"(e1));
+                        mine &= below;
                         if (kTwo && (LJ || !kTwoDensityOff) && mine) {  // two entries in flight
                             const uint32_t e2 = __ffs(mine) - 1;
                             mine &= mine - 1;
